@@ -1,0 +1,398 @@
+"""Benchmark: compressed decode+matvec HBM GB/s and MoE-layer tokens/s.
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config):
+Switch-base-128 MoE layer — 128 experts, d_model 768, d_ff 3072, top-1
+routing (RouterSim argmax), T tokens per step (default 64), synthetic
+random-init weights compressed by the bit-exact GPU encoder. A step is one MoE
+layer forward: dispatcher plan + grouped wi pass + grouped wo pass (ReLU fused).
+Cold L2: a pool of distinct layers >= 4x the 126 MB L2 is rotated, so every
+step streams its experts from HBM.
+
+value  = compressed bytes of the distinct experts touched per step (wi + wo,
+         stats.compression_rate accounting) / device time, whole job (GB/s).
+e2e    = the same through the public host API (numpy tokens + expert ids in,
+         numpy outputs out; H2D/D2H inside the timed region).
+
+`--impl reference` times the CPU oracle port of the reference algorithm
+(oracle/, numpy restatement of moepack.codec.fused_matvec composed per token)
+on the host cores instead.
+
+Run: python bench.py [--gpus N --steps K --warmup W --tokens T --workload NAME]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="switch-base-128")
+    p.add_argument("--tokens", type=int, default=64)
+    p.add_argument("--pool-factor", type=float, default=4.0, help="layer pool size in multiples of L2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([v.strip() for v in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.1)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_layer_sample(E, d_model, d_ff, T, seed, odic, experts_needed):
+    """Host-side synthetic experts for the CPU oracle: numpy N(0, 0.02^2) ->
+    oracle RTN -> oracle encode (only the experts the sample touches)."""
+    from oracle import qmoe_oracle as O
+
+    host = {}
+    for e in experts_needed:
+        pair = []
+        for m, (rows, cols) in enumerate(((d_ff, d_model), (d_model, d_ff))):
+            rng = np.random.default_rng(np.random.SeedSequence([seed, 0, int(e), m]))
+            w = (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+            mm = O.make_grid_bits(w)
+            codes = O.rtn_codes(w, mm)
+            cw, ro = O.encode_codes(codes, odic)
+            pair.append((rows, cols, cw, ro, mm))
+        host[int(e)] = tuple(pair)
+    return host
+
+
+def run_oracle_steps(x_list, assign_list, host, odic, workers):
+    """Composed CPU oracle MoE step(s); returns (seconds, bytes, tokens)."""
+    from oracle import qmoe_oracle as O
+
+    t0 = time.perf_counter()
+    nbytes = 0
+    ntok = 0
+    for x, a in zip(x_list, assign_list):
+        for e in np.unique(a):
+            wi, wo = host[int(e)]
+            nbytes += O.compressed_bytes(wi[0], len(wi[2])) + O.compressed_bytes(wo[0], len(wo[2]))
+            for p in np.flatnonzero(a == e):
+                h = O.fused_matvec(*wi[:2], *wi[2:], odic.hash64, x[p], odic, workers=workers)
+                O.fused_matvec(*wo[:2], *wo[2:], odic.hash64, np.maximum(h, 0), odic, workers=workers)
+        ntok += len(a)
+    return time.perf_counter() - t0, nbytes, ntok
+
+
+def reference_arm(args):
+    from oracle import qmoe_oracle as O
+    from paper_2310_16795_b200.synth import WORKLOADS
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    E, d_model, d_ff = WORKLOADS[args.workload]
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    odic = O.OracleDictionary(0.885, O.generate_decode_words(0.885))
+    # bounded sample: each step = `sample_tokens` tokens of the workload
+    sample_tokens = min(args.tokens, 8)
+    rng = np.random.default_rng(0)
+    xs, asg = [], []
+    for s in range(args.steps + args.warmup):
+        x = O.bf16_round(rng.normal(size=(sample_tokens, d_model)).astype(np.float32))
+        xs.append(x)
+        asg.append(O.router_argmax(x, E, seed=0))
+    need = np.unique(np.concatenate(asg))
+    host = oracle_layer_sample(E, d_model, d_ff, sample_tokens, 0, odic, need)
+    run_oracle_steps(xs[: args.warmup], asg[: args.warmup], host, odic, cores)
+    sec, nbytes, ntok = run_oracle_steps(xs[args.warmup :], asg[args.warmup :], host, odic, cores)
+    gbs = nbytes / sec / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 codewords -> f32 accumulate",
+        "data": "synthetic N(0,0.02^2) RTN ternary, oracle encode",
+        "config": {"workload": args.workload, "experts": E, "d_model": d_model, "d_ff": d_ff,
+                   "tokens_per_step": sample_tokens, "routing": "RouterSim argmax seed 0"},
+        "tokens_per_s": ntok / sec,
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} steps x {sample_tokens} tokens through the composed oracle "
+                                   f"(moepack.codec.fused_matvec restated, workers={cores})"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+METRIC = "compressed decode+matvec HBM GB/s (% peak); MoE-layer tokens/s"
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_16795_b200 as q
+    from paper_2310_16795_b200 import _lib
+    from paper_2310_16795_b200.synth import WORKLOADS, build_layer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    E, d_model, d_ff = WORKLOADS[args.workload]
+    T = args.tokens
+    dic = q.generate_dictionary()
+
+    # ---- layer pool (>= pool_factor x L2 of distinct compressed bytes)
+    layers = []
+    pool = 0
+    t_build = time.time()
+    while pool < args.pool_factor * L2_BYTES or not layers:
+        lay = build_layer(E, d_model, d_ff, seed=1000 * rank + len(layers), dic=dic, device=dev, max_tokens=T)
+        layers.append(lay)
+        pool += int(lay.expert_bytes.sum())
+        if args.profile and len(layers) >= 2:
+            break
+    t_build = time.time() - t_build
+    L = len(layers)
+
+    # ---- token batches and routing (host RouterSim argmax, as the reference)
+    router = q.RouterSim(E, rule="argmax", seed=0)
+    rng = np.random.default_rng(rank)
+    nb = 8
+    xs = [q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32)) for _ in range(nb)]
+    asg = [router.assign(x) for x in xs]
+    xd = [torch.from_numpy(x).to(dev).to(torch.bfloat16) for x in xs]
+    ad = [torch.from_numpy(a).to(dev) for a in asg]
+    outs = [torch.empty((T, d_model), dtype=torch.float32, device=dev) for _ in range(L)]
+
+    # ---- CUDA graph per (layer, batch) step
+    def step_fn(i):
+        l, b = i % L, i % nb
+        layers[l].forward_device(xd[b], ad[b], out=outs[l])
+
+    nsteps_graph = L * nb // np.gcd(L, nb)
+    graphs = []
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(min(nsteps_graph, 3)):
+            step_fn(i)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    for i in range(nsteps_graph):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step_fn(i)
+        graphs.append(g)
+    step_bytes = [layers[i % L].touched_bytes(asg[i % nb]) for i in range(nsteps_graph)]
+
+    for i in range(args.warmup):
+        graphs[i % nsteps_graph].replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region (device): K graph replays
+    hbm_peak, peak_kind = peaks()
+    cs = ClockSampler(local) if not args.profile else None
+    if cs:
+        cs.__enter__()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    tot_bytes = 0
+    for i in range(args.steps):
+        j = (args.warmup + i) % nsteps_graph
+        graphs[j].replay()
+        tot_bytes += step_bytes[j]
+    ev1.record()
+    torch.cuda.synchronize()
+    if cs:
+        cs.__exit__()
+    ms = ev0.elapsed_time(ev1)
+    t_sec = ms / 1e3
+    if world > 1:
+        tt = torch.tensor([t_sec], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_sec = float(tt.item())
+        bb = torch.tensor([tot_bytes], device=dev, dtype=torch.float64)
+        dist.all_reduce(bb)
+        tot_bytes = float(bb.item())
+    value = tot_bytes / t_sec / 1e9
+    tokens_per_s = T * args.steps * world / t_sec
+
+    # ---- per-kernel timing of the grouped passes (events on the launch stream)
+    k_ms = {"wi": [], "wo": []}
+    k_bytes = {"wi": [], "wo": []}
+    stream = torch.cuda.current_stream()
+    for i in range(min(args.steps, 2 * nsteps_graph)):
+        l, b = i % L, i % nb
+        lay = layers[l]
+        a = ad[b]
+        touched = np.unique(asg[b])
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        T_ = xd[b].shape[0]
+        sp = _lib.stream_ptr(stream)
+        _lib.check(_lib.lib.qmoe_moe_plan(_lib.ptr(a), T_, lay.E, lay.d_ff, lay.d_model, lay.rpu_wi, lay.rpu_wo,
+                                          lay.max_units, _lib.ptr(lay.units_wi), _lib.ptr(lay.units_wo),
+                                          _lib.ptr(lay.n_units), _lib.ptr(lay.expert_count), _lib.ptr(lay.order), sp))
+        h = lay.h[:T_]
+        h.zero_()
+        evs[0].record(stream)
+        _lib.check(_lib.lib.qmoe_grouped_matvec(lay.handle, _lib.ptr(lay.mats), _lib.ptr(lay.units_wi),
+                                                _lib.ptr(lay.n_units), lay.max_units, max(d_model, d_ff),
+                                                _lib.ptr(xd[b]), _lib.QMOE_X_BF16, d_model, 0, _lib.ptr(h), d_ff,
+                                                _lib.ptr(lay.bad), sp))
+        evs[1].record(stream)
+        outs[l].zero_()
+        evs[2].record(stream)
+        _lib.check(_lib.lib.qmoe_grouped_matvec(lay.handle, _lib.ptr(lay.mats), _lib.ptr(lay.units_wo),
+                                                lay.n_units.data_ptr() + 4, lay.max_units, max(d_model, d_ff),
+                                                _lib.ptr(h), _lib.QMOE_X_F32, d_ff, 1, _lib.ptr(outs[l]), d_model,
+                                                _lib.ptr(lay.bad), sp))
+        evs[3].record(stream)
+        torch.cuda.synchronize()
+        k_ms["wi"].append(evs[0].elapsed_time(evs[1]))
+        k_ms["wo"].append(evs[2].elapsed_time(evs[3]))
+        k_bytes["wi"].append(sum(lay.wi[e].compressed_bytes for e in touched))
+        k_bytes["wo"].append(sum(lay.wo[e].compressed_bytes for e in touched))
+    kern_ms = float(np.mean(k_ms["wi"]) + np.mean(k_ms["wo"])) / 2
+    kern_bytes = float(np.mean(k_bytes["wi"]) + np.mean(k_bytes["wo"])) / 2
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9
+
+    # ---- e2e through the public host API (numpy in / numpy out)
+    e2e = None
+    if rank == 0 or world > 1:
+        for i in range(2):
+            layers[i % L].forward(xs[i % nb], asg[i % nb])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_bytes = 0
+        for i in range(args.steps):
+            l, b = i % L, i % nb
+            layers[l].forward(xs[b], asg[b])
+            e_bytes += layers[l].touched_bytes(asg[b])
+        torch.cuda.synchronize()
+        e_sec = time.perf_counter() - t0
+        e2e = {"value": e_bytes / e_sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(xs[0].nbytes + asg[0].nbytes),
+               "d2h_bytes_per_step": int(T * d_model * 4), "tokens_per_s": T * args.steps / e_sec,
+               "api": "CompressedMoELayer.forward(numpy x f32, numpy expert ids) -> numpy y"}
+
+    # ---- CPU baseline (oracle port on this host), rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        from oracle import qmoe_oracle as O
+
+        cores = os.cpu_count() or 1
+        odic = O.OracleDictionary(0.885, dic.decode_words)
+        sample_steps, sample_T = 2, min(T, 16)
+        host = {}
+        for b in range(sample_steps):
+            for e in np.unique(asg[b][:sample_T]):
+                if int(e) in host:
+                    continue
+                lay = layers[0]
+                host[int(e)] = tuple(
+                    (m.rows, m.cols, m.cw.cpu().numpy().view(np.uint16), m.row_off.cpu().numpy(),
+                     m.row_minmax.cpu().numpy().view(np.uint16).reshape(m.rows, 2))
+                    for m in (lay.wi[int(e)], lay.wo[int(e)]))
+        sec, nbytes, ntok = run_oracle_steps([xs[b][:sample_T] for b in range(sample_steps)],
+                                             [asg[b][:sample_T] for b in range(sample_steps)], host, odic, cores)
+        cpu = {"value": nbytes / sec / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+               "tokens_per_s": ntok / sec,
+               "sample": f"{sample_steps} steps x {sample_T} tokens of layer 0 through the composed CPU oracle "
+                         f"(numpy restatement of moepack.codec.fused_matvec, workers={cores})"}
+
+    if rank == 0:
+        clocks = cs.summary() if cs else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_sec / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u16 codewords -> f32 accumulate (bf16 x, bf16-rounded y)",
+            "data": "synthetic: random-init N(0,0.02^2) weights, GPU RTN ternary + bit-exact GPU encoder",
+            "config": {"workload": args.workload, "experts": E, "d_model": d_model, "d_ff": d_ff,
+                       "tokens_per_step": T, "routing": "top-1 RouterSim argmax seed 0", "layer_pool": L,
+                       "pool_bytes": pool, "l2": f"cold: rotating {L} distinct layers = {pool / L2_BYTES:.1f}x L2",
+                       "parallelism": f"ep{world}" if world > 1 else "single"},
+            "pct_peak": 100 * value / hbm_peak,
+            "tokens_per_s": tokens_per_s,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "grouped_matvec_kernel<true> (wi and wo passes, mean)",
+                         "bytes_per_launch": kern_bytes, "ms_per_launch": kern_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 3 * args.steps,
+            "clocks": clocks,
+            "build_s": t_build,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,190 @@
+/*
+ * qmoe.h — C-ABI of the B200-native QMoE compressed decode + matvec library
+ * (libqmoe.so, built from paper_2310_16795_b200/csrc/).
+ *
+ * The reference (`moepack`, pure Python/numpy) has no FFI: its boundary is the
+ * Python operator API in /root/reference/pkg/src/moepack/codec.py. Every
+ * entry point below replaces one reference function; the citation is given on
+ * each declaration (paths relative to /root/reference/pkg/src/moepack/).
+ * INTEGRATION.md shows the ctypes binding a moepack maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Pointers marked d_ are DEVICE pointers,
+ *    h_ are HOST pointers. `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream). Device calls are asynchronous on `stream`
+ *    and never allocate on the hot path (dictionary handles own their tables).
+ *  - Return status: QMOE_OK, QMOE_EINVAL (bad argument / shape),
+ *    QMOE_ECORRUPT (data failed validation; host-side checks only — device-side
+ *    corruption is reported through d_bad), QMOE_ECUDA (CUDA launch/runtime
+ *    error), QMOE_EUNSUPPORTED. qmoe_last_error() returns a thread-local
+ *    message for the last non-OK status.
+ *  - Compressed matrix layout (CompressedMatrix, codec.py:33-60):
+ *      cw        uint16[n_cw]        codeword stream, row r owns [row_off[r], row_off[r+1])
+ *      row_off   int32[rows + 1]     monotone, row_off[0] = 0, row_off[rows] = n_cw
+ *      row_minmax uint32[rows]       bf16 pair: low half = min bits, high half = max bits
+ *                                     (== uint16 (rows, 2) little-endian)
+ *  - y semantics of every matvec (codec.py:242-243):
+ *      y[r] += bf16_rne( fp32 sum_j level(code[r][j]) * x[j] ),  y float32,
+ *      level(0) = 0, level(1) = f32(bf16 min), level(2) = f32(bf16 max).
+ */
+#ifndef QMOE_H_
+#define QMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  QMOE_OK = 0,
+  QMOE_EINVAL = 1,
+  QMOE_ECORRUPT = 2,
+  QMOE_ECUDA = 3,
+  QMOE_EUNSUPPORTED = 4
+};
+
+enum { QMOE_X_F32 = 0, QMOE_X_BF16 = 1 };
+
+#define QMOE_DICT_SIZE 65536
+#define QMOE_MAX_PAIRS 14
+#define QMOE_NT_MAX 4 /* tokens per grouped work unit (inner token loop) */
+
+typedef struct qmoe_dict* qmoe_dict_t;
+
+/* One compressed matrix resident on the device (grouped launches). */
+typedef struct qmoe_matrix {
+  const uint16_t* cw;
+  const int32_t* row_off;
+  const uint32_t* row_minmax;
+  int32_t rows;
+  int32_t cols;
+} qmoe_matrix;
+
+/* One grouped work unit: rows [row0, row1) of matrix `mat`, applied to
+ * `ntok` (<= QMOE_NT_MAX) tokens. Token t of the unit reads x row tok[t]
+ * (x + tok[t] * ldx) and accumulates into y row tok[t] (y + tok[t] * ldy). */
+typedef struct qmoe_unit {
+  int32_t mat;
+  int32_t row0;
+  int32_t row1;
+  int32_t ntok;
+  int32_t tok[QMOE_NT_MAX];
+} qmoe_unit;
+
+/* ------------------------------------------------------------------ host-only
+ * These need no GPU (they run on the CPU side of the library). */
+
+const char* qmoe_version(void);
+const char* qmoe_last_error(void);
+
+/* generate_dictionary(PairDistribution(p0)).decode_words
+ * (dictionary.py:234-279, packed as in :137-147). h_words: uint32[65536*2]. */
+int qmoe_generate_decode_words(double p0, uint32_t* h_words);
+
+/* _unpack_all + _build_trie (dictionary.py:150-194): validates the table
+ * (pair counts, zero padding, prefix closure, duplicates, single pairs) and
+ * fills next_node int32[(65536+1)*9] and entry_of_node int32[65536+1].
+ * Returns QMOE_ECORRUPT with qmoe_last_error() naming the failed rule. */
+int qmoe_build_trie(const uint32_t* h_words, int32_t* h_next_node, int32_t* h_entry_of_node);
+
+/* --------------------------------------------------------------- dictionary
+ * Dictionary upload (Dictionary, dictionary.py:197-224): copies the decode
+ * words and the trie to `device` and derives the kernel-private tables
+ * (packed <=3-non-zero entry table, length table). Built once per hash. */
+int qmoe_dict_create(const uint32_t* h_words, uint64_t hash64, int device, qmoe_dict_t* out);
+int qmoe_dict_destroy(qmoe_dict_t dict);
+/* max non-zero values per entry, and whether the sparse fast path applies
+ * (max_nonzeros <= 3; false e.g. for p0 = 0.7). */
+int qmoe_dict_info(qmoe_dict_t dict, uint64_t* hash64, int* max_nonzeros, int* sparse_path);
+
+/* ------------------------------------------------------------------- codec */
+
+/* Row-length check of _decode_range (codec.py:164-169): for every row, the
+ * codeword lengths 2*n must sum to cols. d_bad: int32[2] = {number of bad
+ * rows, smallest bad row (INT32_MAX if none)}; the caller zeroes it. */
+int qmoe_validate_rows(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_row_off,
+                       int64_t rows, int64_t cols, int32_t* d_bad, void* stream);
+
+/* decompress (codec.py:175-193 / _decode_range :158-172): d_codes_out is a
+ * (rows, cols) uint8 row-major buffer of ternary codes {0,1,2}. Rows that
+ * fail the length check are counted in d_bad (as above) and left zero. */
+int qmoe_decompress(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_row_off,
+                    int64_t rows, int64_t cols, uint8_t* d_codes_out, int32_t* d_bad,
+                    void* stream);
+
+/* fused_matvec (codec.py:209-244) for one matrix and one x vector.
+ * d_x: cols values of type x_dtype; d_y: rows float32, updated in place.
+ * Rows must have been validated (qmoe_validate_rows) — the kernel skips
+ * writing rows whose lengths disagree and counts them in d_bad (nullable). */
+int qmoe_fused_matvec(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_row_off,
+                      const uint32_t* d_row_minmax, int64_t rows, int64_t cols,
+                      const void* d_x, int x_dtype, float* d_y, int32_t* d_bad, void* stream);
+
+/* The same for ntok tokens at once: x is (ntok, ldx), y is (ntok, ldy); each
+ * token's result equals qmoe_fused_matvec on that token (decode is shared). */
+int qmoe_fused_matmat(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_row_off,
+                      const uint32_t* d_row_minmax, int64_t rows, int64_t cols,
+                      const void* d_x, int x_dtype, int64_t ntok, int64_t ldx, float* d_y,
+                      int64_t ldy, int32_t* d_bad, void* stream);
+
+/* Grouped persistent launch over device-resident work units: one kernel,
+ * one dictionary-table fill, many (matrix, token) pairs. d_units/d_n_units
+ * live in device memory (written e.g. by qmoe_moe_plan), so the call is
+ * graph-capturable with no host synchronisation. x_relu applies max(x, 0)
+ * while staging x (fuses the FFN activation into the wo pass). */
+int qmoe_grouped_matvec(qmoe_dict_t dict, const qmoe_matrix* d_mats, const qmoe_unit* d_units,
+                        const int32_t* d_n_units, int32_t max_units, int32_t max_cols,
+                        const void* d_x, int x_dtype, int64_t ldx, int x_relu, float* d_y,
+                        int64_t ldy, int32_t* d_bad, void* stream);
+
+/* Paper Listing 1 kept as the "paper design on B200"
+ * baseline: warp per row, lanes 0..27 extract, decode words read through the
+ * cache, shuffle reduction. If d_trace is non-NULL it receives, per codeword
+ * (stream order), the lane replay of simulate_warp_row (codec.py:293-338):
+ * int32[n_cw * 5] = {codeword, pair_count, offset, values of lanes 0..13,
+ * values of lanes 14..27} (2 bits per lane, lane i at bits 2*(i % 14)). */
+int qmoe_paper_matvec(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_row_off,
+                      const uint32_t* d_row_minmax, int64_t rows, int64_t cols,
+                      const void* d_x, int x_dtype, float* d_y, int32_t* d_trace,
+                      void* stream);
+
+/* encode (codec.py:126-155, _encode_rows :69-123): greedy longest-prefix trie
+ * walk, one thread per row. Two phases: count codewords per
+ * row into d_counts (int32[rows]), then (after the caller forms
+ * row_off = exclusive scan, see qmoe_exclusive_scan) emit the stream. */
+int qmoe_encode_count(qmoe_dict_t dict, const uint8_t* d_codes, int64_t rows, int64_t cols,
+                      int32_t* d_counts, void* stream);
+int qmoe_encode_emit(qmoe_dict_t dict, const uint8_t* d_codes, int64_t rows, int64_t cols,
+                     const int32_t* d_row_off, uint16_t* d_cw, void* stream);
+/* d_out[0] = 0, d_out[i+1] = sum(d_in[0..i]) for i < n (int32 -> int64 safe
+ * accumulation; overflow of int32 is reported via d_out[n] < 0 check). */
+int qmoe_exclusive_scan(const int32_t* d_in, int64_t n, int32_t* d_out, void* stream);
+
+/* make_grid + rtn_quantize (quantize.py:91-107, :219-235) for ternary:
+ * per-row bf16 (min, max) and nearest-level codes, ties to the smaller
+ * magnitude. d_w: float32 (rows, cols). d_minmax_in (nullable) supplies the
+ * grid (QuantGrid.minmax_bits); NULL derives it from the row extrema. */
+int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32_t* d_minmax_in,
+                      uint8_t* d_codes, uint32_t* d_row_minmax, void* stream);
+
+/* ------------------------------------------------------------- MoE dispatch
+ * Routed-expert dispatcher (pipeline.py:86-96 gather/scatter order): stable
+ * counting sort of the top-1 assignment d_assign[T] into per-expert token
+ * lists, then the work units of both FFN passes:
+ *   pass 1 (wi, matrix 2e):   units over d_ff rows, tokens of expert e
+ *   pass 2 (wo, matrix 2e+1): units over d_model rows, same tokens
+ * Units hold up to QMOE_NT_MAX tokens and `rows_per_unit_wi/_wo` rows.
+ * d_units_wi/_wo must hold max_units entries; counts go to d_n_units[2].
+ * d_expert_count (int32[E]) and d_order (int32[T]) are outputs too. */
+int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, int32_t rows_wi,
+                  int32_t rows_wo, int32_t rows_per_unit_wi, int32_t rows_per_unit_wo,
+                  int32_t max_units, qmoe_unit* d_units_wi, qmoe_unit* d_units_wo,
+                  int32_t* d_n_units, int32_t* d_expert_count, int32_t* d_order, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QMOE_H_ */

@@ -1,0 +1,442 @@
+"""Compressed format + the drop-in codec entry points (moepack/codec.py).
+
+Reference surface kept: `CompressedMatrix`, `encode`, `decompress`,
+`fused_matvec`, `pad_to_even`, `simulate_warp_row`, `WarpTrace`,
+`SymbolTrace`, `write_checkpoint`, `read_checkpoint` — same argument meaning,
+check order and exceptions (CorruptionError, DictionaryMismatchError,
+ValueError). Every compute step runs in libqmoe on the GPU; numpy inputs are
+copied to the device and results copied back, CUDA tensors are used in place.
+
+The device-resident form is `DeviceMatrix` (uploaded + row-validated once);
+the MoE layer and the benchmarks work on it directly.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .dictionary import DICT_SIZE, Dictionary
+from .errors import CorruptionError, DictionaryMismatchError
+from .quantize import TernaryMatrix
+
+CHECKPOINT_MAGIC = b"QMOE0001"
+INT32_MAX = 2**31 - 1
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass
+class CompressedMatrix:
+    """Host form (codec.py:33-60): uint16 codewords, int32 row_off (rows+1),
+    uint16 (rows, 2) bf16 (min, max), dictionary hash. Treated as immutable
+    after construction; the device copy is cached on it."""
+
+    rows: int
+    cols: int
+    codewords: np.ndarray
+    row_off: np.ndarray
+    row_minmax: np.ndarray
+    dict_hash: int
+    _device: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def validate(self) -> None:
+        if self.rows < 0 or self.cols < 0 or self.cols % 2 != 0:
+            raise CorruptionError("invalid compressed matrix shape")
+        if self.row_off.shape != (self.rows + 1,) or self.row_off.dtype != np.int32:
+            raise CorruptionError("row_off must be (rows + 1,) int32")
+        if self.rows and self.row_minmax.shape != (self.rows, 2):
+            raise CorruptionError("row_minmax must be (rows, 2)")
+        if self.row_off[0] != 0 or self.row_off[-1] != len(self.codewords):
+            raise CorruptionError("row_off does not span the codeword stream")
+        if np.any(np.diff(self.row_off) < 0):
+            raise CorruptionError("row_off must be monotone")
+
+    def _key(self):
+        arrs = (self.codewords, self.row_off, self.row_minmax)
+        return (self.rows, self.cols, self.dict_hash) + tuple((id(a), a.ctypes.data, a.shape) for a in arrs)
+
+    def to_device(self, dic: Dictionary, device=None) -> "DeviceMatrix":
+        """Upload (once) and validate every row's decoded length on the GPU."""
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        hit = self._device.get(dev.index)
+        if hit is not None and hit[0] == self._key():
+            return hit[1]
+        dm = DeviceMatrix.from_host(self, dic, dev)
+        self._device[dev.index] = (self._key(), dm)
+        return dm
+
+
+class DeviceMatrix:
+    """One compressed matrix resident in HBM: cw int16 (uint16 bits), row_off
+    int32, row_minmax int32 (packed bf16 pair, low = min). `bad_rows` is the
+    device row-length validation result (0 for a usable matrix)."""
+
+    def __init__(self, rows, cols, cw, row_off, row_minmax, dict_hash, bad_rows=0, first_bad=None):
+        self.rows, self.cols = int(rows), int(cols)
+        self.cw, self.row_off, self.row_minmax = cw, row_off, row_minmax
+        self.dict_hash = int(dict_hash)
+        self.bad_rows = int(bad_rows)
+        self.first_bad = first_bad
+
+    @property
+    def n_codewords(self) -> int:
+        return int(self.cw.numel())
+
+    @property
+    def compressed_bytes(self) -> int:
+        """payload + metadata bytes (stats.compression_rate, stats.py:103-114)."""
+        return 2 * self.n_codewords + 4 * (self.rows + 1) + 4 * self.rows
+
+    @classmethod
+    def from_host(cls, c: CompressedMatrix, dic: Dictionary, device) -> "DeviceMatrix":
+        torch = _torch()
+        cw = torch.from_numpy(np.ascontiguousarray(c.codewords, np.uint16).view(np.int16)).to(device)
+        ro = torch.from_numpy(np.ascontiguousarray(c.row_off, np.int32)).to(device)
+        mm = np.ascontiguousarray(c.row_minmax, np.uint16).reshape(-1, 2) if c.rows else np.zeros((0, 2), np.uint16)
+        mmd = torch.from_numpy(mm.copy().view(np.int32).reshape(-1)).to(device)
+        dm = cls(c.rows, c.cols, cw, ro, mmd, c.dict_hash)
+        dm.validate_rows(dic)
+        return dm
+
+    def validate_rows(self, dic: Dictionary) -> int:
+        torch = _torch()
+        bad = torch.tensor([0, INT32_MAX], dtype=torch.int32, device=self.cw.device)
+        h = dic.device_handle(self.cw.device.index)
+        _lib.check(_lib.lib.qmoe_validate_rows(h, _lib.ptr(self.cw), _lib.ptr(self.row_off), self.rows, self.cols,
+                                               _lib.ptr(bad), _lib.stream_ptr()))
+        b = bad.cpu().tolist()
+        self.bad_rows, self.first_bad = b[0], (b[1] if b[0] else None)
+        return self.bad_rows
+
+    def descriptor(self) -> tuple:
+        return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(), self.rows, self.cols)
+
+
+def _row_len_error():
+    return CorruptionError("row decodes to the wrong number of values")
+
+
+# ------------------------------------------------------------------ encode
+def encode_device(codes, row_minmax, dic: Dictionary, stream=None) -> DeviceMatrix:
+    """GPU encode of a CUDA uint8 (rows, cols) code tensor (codec.py:126-155):
+    count pass, exclusive scan, emit pass. row_minmax: int32 packed tensor."""
+    torch = _torch()
+    rows, cols = codes.shape
+    if cols % 2 != 0:
+        raise ValueError("column count must be even; pad_to_even() first")
+    codes = codes.contiguous()
+    dev = codes.device
+    h = dic.device_handle(dev.index)
+    sp = _lib.stream_ptr(stream)
+    counts = torch.empty(rows, dtype=torch.int32, device=dev)
+    row_off = torch.empty(rows + 1, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib.qmoe_encode_count(h, _lib.ptr(codes), rows, cols, _lib.ptr(counts), sp))
+    _lib.check(_lib.lib.qmoe_exclusive_scan(_lib.ptr(counts), rows, _lib.ptr(row_off), sp))
+    total = int(row_off[-1].item())
+    if total < 0:
+        raise ValueError("codeword stream exceeds 32-bit row offsets")
+    cw = torch.empty(total, dtype=torch.int16, device=dev)
+    _lib.check(_lib.lib.qmoe_encode_emit(h, _lib.ptr(codes), rows, cols, _lib.ptr(row_off), _lib.ptr(cw), sp))
+    return DeviceMatrix(rows, cols, cw, row_off, row_minmax.contiguous(), dic.hash64)
+
+
+def encode(t: TernaryMatrix, dic: Dictionary, workers: int = 1) -> CompressedMatrix:
+    """Greedy longest-prefix encode (codec.py:126-155) on the GPU, one thread
+    per row. `workers` is accepted for API parity (output is invariant)."""
+    torch = _torch()
+    if t.cols % 2 != 0:
+        raise ValueError("column count must be even; pad_to_even() first")
+    rows, cols = t.rows, t.cols
+    if rows == 0 or cols == 0:
+        return CompressedMatrix(rows, cols, np.zeros(0, np.uint16), np.zeros(rows + 1, np.int32),
+                                t.row_minmax.copy(), dic.hash64)
+    codes = torch.from_numpy(np.ascontiguousarray(t.codes)).cuda()
+    mm = torch.zeros(rows, dtype=torch.int32, device=codes.device)
+    dm = encode_device(codes, mm, dic)
+    return CompressedMatrix(
+        rows=rows,
+        cols=cols,
+        codewords=dm.cw.cpu().numpy().view(np.uint16).copy(),
+        row_off=dm.row_off.cpu().numpy().astype(np.int32),
+        row_minmax=t.row_minmax.copy(),
+        dict_hash=dic.hash64,
+    )
+
+
+# ------------------------------------------------------------------ decompress
+def _prepare(c, dic: Dictionary) -> DeviceMatrix:
+    if isinstance(c, DeviceMatrix):
+        dm = c
+    else:
+        c.validate()
+    if c.dict_hash != dic.hash64:
+        raise DictionaryMismatchError("checkpoint was encoded against a different dictionary")
+    if not isinstance(c, DeviceMatrix):
+        dm = c.to_device(dic)
+    return dm
+
+
+def decompress_device(dm: DeviceMatrix, dic: Dictionary, stream=None):
+    torch = _torch()
+    out = torch.empty((dm.rows, dm.cols), dtype=torch.uint8, device=dm.cw.device)
+    bad = torch.tensor([0, INT32_MAX], dtype=torch.int32, device=dm.cw.device)
+    h = dic.device_handle(dm.cw.device.index)
+    _lib.check(_lib.lib.qmoe_decompress(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), dm.rows, dm.cols, _lib.ptr(out),
+                                        _lib.ptr(bad), _lib.stream_ptr(stream)))
+    return out, bad
+
+
+def decompress(c, dic: Dictionary, workers: int = 1) -> TernaryMatrix:
+    """Exact expansion back to ternary codes (codec.py:175-193)."""
+    dm = _prepare(c, dic)
+    if dm.rows == 0 or dm.cols == 0:
+        mm = c.row_minmax.copy() if isinstance(c, CompressedMatrix) else np.zeros((dm.rows, 2), np.uint16)
+        return TernaryMatrix(codes=np.zeros((dm.rows, dm.cols), np.uint8), row_minmax=mm.reshape(dm.rows, 2))
+    if dm.bad_rows:
+        raise _row_len_error()
+    out, bad = decompress_device(dm, dic)
+    if int(bad[0].item()):
+        raise _row_len_error()
+    codes = out.cpu().numpy()
+    if isinstance(c, CompressedMatrix):
+        mm = c.row_minmax.copy()
+    else:
+        mm = dm.row_minmax.cpu().numpy().view(np.uint16).reshape(dm.rows, 2).copy()
+    return TernaryMatrix(codes=codes, row_minmax=mm)
+
+
+# ------------------------------------------------------------------ fused matvec
+def _x_dtype_code(x) -> int:
+    torch = _torch()
+    return _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
+
+
+def fused_matvec_device(dm: DeviceMatrix, dic: Dictionary, x, y, stream=None, bad=None) -> None:
+    """y (CUDA f32, rows) += bf16(M @ x) for x a CUDA f32/bf16 (cols,) tensor,
+    or x (ntok, cols) / y (ntok, rows) for an inner token loop."""
+    h = dic.device_handle(dm.cw.device.index)
+    sp = _lib.stream_ptr(stream)
+    xt = _lib.QMOE_X_BF16 if _x_dtype_code(x) == _lib.QMOE_X_BF16 else _lib.QMOE_X_F32
+    if x.dim() == 1:
+        _lib.check(_lib.lib.qmoe_fused_matvec(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), _lib.ptr(dm.row_minmax),
+                                              dm.rows, dm.cols, _lib.ptr(x), xt, _lib.ptr(y), _lib.ptr(bad), sp))
+    else:
+        _lib.check(_lib.lib.qmoe_fused_matmat(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), _lib.ptr(dm.row_minmax),
+                                              dm.rows, dm.cols, _lib.ptr(x), xt, x.shape[0], x.stride(0),
+                                              _lib.ptr(y), y.stride(0), _lib.ptr(bad), sp))
+
+
+def _dense_semantics(dm: DeviceMatrix, dic: Dictionary, x32):
+    """Non-finite x: the reference multiplies the dense
+    dequantized row, so 0 * inf = NaN reaches every row. The sparse kernels
+    skip zeros, so this case expands the rows on the GPU (qmoe_decompress)
+    and runs the dense product there, reproducing the reference's NaN/inf
+    propagation. Only taken when x holds inf/NaN."""
+    torch = _torch()
+    codes, bad = decompress_device(dm, dic)
+    mm = dm.row_minmax.view(torch.int16).view(dm.rows, 2)
+    lv_min = (mm[:, 0].to(torch.int32) << 16).view(torch.float32)
+    lv_max = (mm[:, 1].to(torch.int32) << 16).view(torch.float32)
+    w = torch.where(codes == 1, lv_min[:, None], torch.where(codes == 2, lv_max[:, None], torch.zeros((), device=codes.device)))
+    part = (w.to(torch.float32) @ x32.to(torch.float32))
+    u = part.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) & 0xFFFF
+    return (u << 16).to(torch.int64).to(torch.int32).view(torch.float32)
+
+
+def fused_matvec(c, x, dic: Dictionary, y=None, workers: int = 1):
+    """y += M @ x straight from the compressed stream (codec.py:209-244):
+    fp32 products and sums per row, one bf16 RNE rounding, fp32 add into y.
+    numpy x/y: copied to the GPU and back, y updated in place and returned.
+    CUDA tensors: computed in place on the current stream."""
+    torch = _torch()
+    if isinstance(c, DeviceMatrix):
+        dm_rows, dm_cols = c.rows, c.cols
+    else:
+        c.validate()
+        dm_rows, dm_cols = c.rows, c.cols
+    if c.dict_hash != dic.hash64:
+        raise DictionaryMismatchError("checkpoint was encoded against a different dictionary")
+    on_device = torch.is_tensor(x)
+    if on_device:
+        if tuple(x.shape) != (dm_cols,):
+            raise ValueError(f"x must have shape ({dm_cols},)")
+        if y is None:
+            y = torch.zeros(dm_rows, dtype=torch.float32, device=x.device)
+        elif tuple(y.shape) != (dm_rows,):
+            raise ValueError(f"y must have shape ({dm_rows},)")
+        xd = x if x.dtype in (torch.float32, torch.bfloat16) else x.float()
+        yd = y
+    else:
+        x32 = np.asarray(x, dtype=np.float32)
+        if x32.shape != (dm_cols,):
+            raise ValueError(f"x must have shape ({dm_cols},)")
+        if y is None:
+            y = np.zeros(dm_rows, dtype=np.float32)
+        elif y.shape != (dm_rows,):
+            raise ValueError(f"y must have shape ({dm_rows},)")
+    if dm_rows == 0:
+        return y
+    dm = c if isinstance(c, DeviceMatrix) else c.to_device(dic)
+    if dm.bad_rows:
+        raise _row_len_error()  # y untouched (codec.py:237-243 computes all parts first)
+    if not on_device:
+        xd = torch.from_numpy(np.ascontiguousarray(x32)).cuda()
+        yd = torch.from_numpy(np.asarray(y, dtype=np.float32).copy()).cuda()
+        finite = bool(np.isfinite(x32).all())
+    else:
+        finite = bool(torch.isfinite(xd).all().item())
+    if dm_cols == 0:
+        pass
+    elif finite:
+        fused_matvec_device(dm, dic, xd, yd)
+    else:
+        yd += _dense_semantics(dm, dic, xd)
+    if on_device:
+        return y
+    out = yd.cpu().numpy()
+    if y.dtype == np.float32:
+        y[...] = out
+    else:
+        y[...] = out.astype(y.dtype)
+    return y
+
+
+def paper_matvec_device(dm: DeviceMatrix, dic: Dictionary, x, y, trace=None, stream=None) -> None:
+    """The paper's Listing-1 kernel (baseline design) on the GPU."""
+    h = dic.device_handle(dm.cw.device.index)
+    _lib.check(_lib.lib.qmoe_paper_matvec(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), _lib.ptr(dm.row_minmax), dm.rows,
+                                          dm.cols, _lib.ptr(x), _x_dtype_code(x), _lib.ptr(y), _lib.ptr(trace),
+                                          _lib.stream_ptr(stream)))
+
+
+def pad_to_even(t: TernaryMatrix) -> TernaryMatrix:
+    """Append one zero column to odd-width matrices (codec.py:247-258)."""
+    if t.cols % 2 == 0:
+        return t
+    codes = np.concatenate([t.codes, np.zeros((t.rows, 1), dtype=np.uint8)], axis=1)
+    return TernaryMatrix(codes=codes, row_minmax=t.row_minmax.copy())
+
+
+# ------------------------------------------------------------------ lane replay
+@dataclass
+class SymbolTrace:
+    codeword: int
+    pair_count: int
+    offset: int
+    lane_values: np.ndarray
+    extracting_lanes: int
+
+
+@dataclass
+class WarpTrace:
+    """Lane replay of one row through the Listing-1 schedule (codec.py:261-290)."""
+
+    row: int
+    fetch_sizes: list = field(default_factory=list)
+    symbols: list = field(default_factory=list)
+    lane_word: np.ndarray = field(default_factory=lambda: np.where(np.arange(32) < 28, np.arange(32) // 14, -1))
+    lane_slot: np.ndarray = field(default_factory=lambda: np.where(np.arange(32) < 28, np.arange(32) % 14, -1))
+    extract_counts: np.ndarray = field(default_factory=lambda: np.zeros(32, np.int64))
+
+    def extracted_values(self) -> np.ndarray:
+        parts = [s.lane_values[: s.extracting_lanes] for s in self.symbols]
+        return np.concatenate(parts) if parts else np.zeros(0, np.uint8)
+
+
+def simulate_warp_row(c: CompressedMatrix, row: int, dic: Dictionary) -> WarpTrace:
+    """Replay row `row` through the paper kernel (codec.py:293-338). The lane
+    records come from the GPU Listing-1 kernel's trace buffer; the replayed
+    values must equal decompress for that row."""
+    torch = _torch()
+    c.validate()
+    if not (0 <= row < c.rows):
+        raise ValueError("row out of range")
+    s, e = int(c.row_off[row]), int(c.row_off[row + 1])
+    # replay just this row: a one-row matrix view of the stream
+    sub = CompressedMatrix(1, c.cols, np.ascontiguousarray(c.codewords[s:e]), np.array([0, e - s], np.int32),
+                           np.ascontiguousarray(c.row_minmax[row : row + 1]), dic.hash64)
+    dm = DeviceMatrix.from_host(sub, dic, torch.device("cuda", torch.cuda.current_device()))
+    trace = torch.zeros(max(1, e - s) * 5, dtype=torch.int32, device=dm.cw.device)
+    x = torch.zeros(c.cols, dtype=torch.float32, device=dm.cw.device)
+    y = torch.zeros(1, dtype=torch.float32, device=dm.cw.device)
+    if e > s:
+        paper_matvec_device(dm, dic, x, y, trace=trace)
+    rec = trace.cpu().numpy().reshape(-1, 5)[: e - s]
+    tr = WarpTrace(row=row)
+    tr.fetch_sizes = [int(min(32, (e - s) - b)) for b in range(0, e - s, 32)]
+    lanes = np.arange(28)
+    for cw_, n, off, v0, v1 in rec.tolist():
+        words = (np.uint32(v0 & 0xFFFFFFFF), np.uint32(v1 & 0xFFFFFFFF))
+        lane_vals = np.array([(int(words[l // 14]) >> (2 * (l % 14))) & 3 for l in lanes], np.uint8)
+        tr.symbols.append(SymbolTrace(codeword=int(cw_), pair_count=int(n), offset=int(off), lane_values=lane_vals,
+                                      extracting_lanes=2 * int(n)))
+        tr.extract_counts[: 2 * int(n)] += 1
+    total = sum(2 * s_.pair_count for s_ in tr.symbols)
+    if total != c.cols:
+        raise CorruptionError("row decodes to the wrong number of values")
+    direct = decompress(sub, dic).codes[0]
+    if not np.array_equal(tr.extracted_values(), direct):
+        raise CorruptionError("lane replay disagrees with decompress")
+    return tr
+
+
+# ------------------------------------------------------------------ container
+def write_checkpoint(c: CompressedMatrix, path: str) -> None:
+    """QMOE0001: magic, <QQQ rows/cols/dict_hash, <i4 row_off, <u2 row_minmax,
+    <u2 codewords; no padding (codec.py:341-351)."""
+    c.validate()
+    with open(path, "wb") as fh:
+        fh.write(CHECKPOINT_MAGIC)
+        fh.write(struct.pack("<QQQ", c.rows, c.cols, c.dict_hash))
+        fh.write(c.row_off.astype("<i4").tobytes())
+        fh.write(c.row_minmax.astype("<u2").tobytes())
+        fh.write(c.codewords.astype("<u2").tobytes())
+
+
+def read_checkpoint(path: str) -> CompressedMatrix:
+    """Strict reader (codec.py:354-391): magic, header arrays, monotone
+    offsets from zero, exact total size, then validate()."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < len(CHECKPOINT_MAGIC) + 24 or not blob.startswith(CHECKPOINT_MAGIC):
+        raise CorruptionError("not a checkpoint file (bad magic)")
+    pos = len(CHECKPOINT_MAGIC)
+    rows, cols, dict_hash = struct.unpack_from("<QQQ", blob, pos)
+    pos += 24
+    if len(blob) < pos + 4 * (rows + 1) + 4 * rows:
+        raise CorruptionError("checkpoint truncated in header arrays")
+    row_off = np.frombuffer(blob, dtype="<i4", count=rows + 1, offset=pos).astype(np.int32)
+    pos += 4 * (rows + 1)
+    row_minmax = np.frombuffer(blob, dtype="<u2", count=2 * rows, offset=pos).astype(np.uint16).reshape(rows, 2)
+    pos += 4 * rows
+    if row_off[0] != 0 or np.any(np.diff(row_off) < 0):
+        raise CorruptionError("checkpoint row offsets are not monotone from zero")
+    n = int(row_off[-1])
+    if len(blob) != pos + 2 * n:
+        raise CorruptionError("checkpoint size disagrees with row offsets")
+    cw = np.frombuffer(blob, dtype="<u2", count=n, offset=pos).astype(np.uint16)
+    c = CompressedMatrix(int(rows), int(cols), cw, row_off, row_minmax, int(dict_hash))
+    c.validate()
+    return c
+
+
+def read_checkpoint_device(path: str, dic: Dictionary, device=None) -> DeviceMatrix:
+    """Loader straight to HBM: parse + validate on the host,
+    one H2D copy per array, GPU row validation."""
+    c = read_checkpoint(path)
+    if c.dict_hash != dic.hash64:
+        raise DictionaryMismatchError("checkpoint was encoded against a different dictionary")
+    dm = c.to_device(dic, device)
+    if dm.bad_rows:
+        raise _row_len_error()
+    return dm

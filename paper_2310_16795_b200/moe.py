@@ -1,0 +1,127 @@
+"""Compressed MoE layer: routed-expert dispatcher + grouped decode/matvec.
+
+One step for T tokens with top-1 expert ids:
+  1. qmoe_moe_plan      stable counting sort of the assignment (buffer order
+                        within an expert, pipeline.py:86-90) and the work
+                        units of both FFN passes, written on the device;
+  2. grouped wi pass    h[t] = bf16(wi_e @ x[t]) for every token, one
+                        persistent launch over all touched experts;
+  3. grouped wo pass    y[t] = bf16(wo_e @ relu(h[t])) (ReLU fused into x
+                        staging).
+Each touched expert's compressed matrices are streamed from HBM once per
+step: the tokens routed to one expert share a work unit (inner token loop,
+up to QMOE_NT_MAX per unit), so decode is not repeated per token.
+No host synchronisation: the whole step is CUDA-graph capturable.
+
+Numerics equal the composed reference oracle (per token wi matvec -> ReLU ->
+wo matvec through moepack.codec.fused_matvec) up to the matvec tolerance.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .codec import DeviceMatrix
+from .dictionary import Dictionary
+
+
+def _rows_per_unit(mats, target_cw: int = 4096) -> int:
+    cw = sum(m.n_codewords for m in mats)
+    rows = sum(m.rows for m in mats)
+    per_row = max(1.0, cw / max(1, rows))
+    r = int(target_cw / per_row)
+    r = max(8, min(r, mats[0].rows))
+    return r
+
+
+class CompressedMoELayer:
+    """E experts, expert e = (wi_e: d_ff x d_model, wo_e: d_model x d_ff),
+    all DeviceMatrix on one device."""
+
+    def __init__(self, wi: list[DeviceMatrix], wo: list[DeviceMatrix], dic: Dictionary, max_tokens: int = 64,
+                 target_cw_per_unit: int = 4096):
+        import torch
+
+        if len(wi) != len(wo) or not wi:
+            raise ValueError("need matching wi/wo lists")
+        self.E = len(wi)
+        self.d_ff, self.d_model = wi[0].rows, wi[0].cols
+        for a, b in zip(wi, wo):
+            if (a.rows, a.cols) != (self.d_ff, self.d_model) or (b.rows, b.cols) != (self.d_model, self.d_ff):
+                raise ValueError("expert shapes disagree")
+            if a.bad_rows or b.bad_rows:
+                raise ValueError("expert matrix failed row validation")
+        self.wi, self.wo, self.dic = wi, wo, dic
+        self.device = wi[0].cw.device
+        self.handle = dic.device_handle(self.device.index)
+        descs = (_lib.QmoeMatrix * (2 * self.E))()
+        for e in range(self.E):
+            descs[2 * e] = _lib.QmoeMatrix(*wi[e].descriptor())
+            descs[2 * e + 1] = _lib.QmoeMatrix(*wo[e].descriptor())
+        raw = np.frombuffer(bytes(descs), dtype=np.uint8)
+        self.mats = torch.from_numpy(raw.copy()).to(self.device)
+        self.rpu_wi = _rows_per_unit(wi, target_cw_per_unit)
+        self.rpu_wo = _rows_per_unit(wo, target_cw_per_unit)
+        self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
+                                     np.int64)
+        self._alloc(max_tokens)
+
+    def _alloc(self, T: int) -> None:
+        import torch
+
+        self.max_tokens = T
+        nblk = max((self.d_ff + self.rpu_wi - 1) // self.rpu_wi, (self.d_model + self.rpu_wo - 1) // self.rpu_wo)
+        self.max_units = max(1, T * nblk)
+        dev = self.device
+        self.units_wi = torch.empty(self.max_units * _lib.UNIT_BYTES, dtype=torch.uint8, device=dev)
+        self.units_wo = torch.empty(self.max_units * _lib.UNIT_BYTES, dtype=torch.uint8, device=dev)
+        self.n_units = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.expert_count = torch.zeros(self.E, dtype=torch.int32, device=dev)
+        self.order = torch.zeros(max(1, T), dtype=torch.int32, device=dev)
+        self.h = torch.zeros((max(1, T), self.d_ff), dtype=torch.float32, device=dev)
+        self.bad = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
+
+    # ------------------------------------------------------------------ device step
+    def forward_device(self, x, assign, out=None, stream=None):
+        """x: (T, d_model) CUDA bf16/f32, assign: (T,) CUDA int32 expert ids.
+        Returns out (T, d_model) float32 = per-token expert FFN output."""
+        import torch
+
+        T = x.shape[0]
+        if T > self.max_tokens:
+            self._alloc(T)
+        if out is None:
+            out = torch.empty((T, self.d_model), dtype=torch.float32, device=self.device)
+        sp = _lib.stream_ptr(stream)
+        xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
+        _lib.check(_lib.lib.qmoe_moe_plan(
+            _lib.ptr(assign), T, self.E, self.d_ff, self.d_model, self.rpu_wi, self.rpu_wo, self.max_units,
+            _lib.ptr(self.units_wi), _lib.ptr(self.units_wo), _lib.ptr(self.n_units), _lib.ptr(self.expert_count),
+            _lib.ptr(self.order), sp))
+        h = self.h[:T]
+        h.zero_()
+        _lib.check(_lib.lib.qmoe_grouped_matvec(
+            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
+            max(self.d_model, self.d_ff), _lib.ptr(x), xt, x.stride(0), 0, _lib.ptr(h), h.stride(0),
+            _lib.ptr(self.bad), sp))
+        out.zero_()
+        _lib.check(_lib.lib.qmoe_grouped_matvec(
+            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 4, self.max_units,
+            max(self.d_model, self.d_ff), _lib.ptr(h), _lib.QMOE_X_F32, h.stride(0), 1, _lib.ptr(out),
+            out.stride(0), _lib.ptr(self.bad), sp))
+        return out
+
+    def forward(self, x: np.ndarray, assign: np.ndarray) -> np.ndarray:
+        """Host API: numpy tokens + expert ids in, numpy outputs back."""
+        import torch
+
+        xd = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(self.device)
+        ad = torch.from_numpy(np.ascontiguousarray(assign, np.int32)).to(self.device)
+        return self.forward_device(xd, ad).cpu().numpy()
+
+    def touched_bytes(self, assign: np.ndarray) -> int:
+        """Compressed bytes one step must stream: each distinct expert once."""
+        return int(self.expert_bytes[np.unique(np.asarray(assign))].sum())

@@ -1,0 +1,100 @@
+"""GPU parity of the MoE layer (dispatcher + grouped passes) against the
+composed reference oracle (<= 2 bf16 ulp per output)."""
+
+import numpy as np
+import pytest
+
+from conftest import bf16_ulp_diff
+
+pytestmark = pytest.mark.gpu
+
+q = pytest.importorskip("paper_2310_16795_b200")
+torch = pytest.importorskip("torch")
+from oracle import qmoe_oracle as O  # noqa: E402
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+
+def layer_from_golden(g, dic):
+    E = int(g["E"])
+    wi, wo = [], []
+    for e in range(E):
+        for m, lst in ((0, wi), (1, wo)):
+            ro = g[f"e{e}_m{m}_row_off"]
+            mm = g[f"e{e}_m{m}_minmax"]
+            rows = len(ro) - 1
+            cols = int(g["d_model"]) if m == 0 else int(g["d_ff"])
+            c = q.CompressedMatrix(rows, cols, g[f"e{e}_m{m}_cw"], ro, mm, dic.hash64)
+            lst.append(c)
+    return wi, wo
+
+
+def test_moe_tiny_matches_reference_golden(dic, golden):
+    g = golden("moe_tiny.npz")
+    wi, wo = layer_from_golden(g, dic)
+    layer = q.CompressedMoELayer([c.to_device(dic) for c in wi], [c.to_device(dic) for c in wo], dic)
+    assign = q.RouterSim(int(g["E"]), rule="argmax", seed=0).assign(g["x"])
+    assert np.array_equal(assign, g["assign"])
+    y = layer.forward(g["x"], assign)
+    d = bf16_ulp_diff(y, g["y"])
+    assert d.max() <= 2, d.max()
+    assert np.mean(d == 0) >= 0.99
+
+
+@pytest.mark.parametrize("T", [1, 3, 16, 64, 200])
+def test_moe_random_layer_vs_oracle(dic, odic, T):
+    rng = np.random.default_rng(T)
+    E, d_model, d_ff = 8, 128, 512
+    wi, wo, host = [], [], []
+    for e in range(E):
+        pair = []
+        for rows, cols, lst in ((d_ff, d_model, wi), (d_model, d_ff, wo)):
+            w = (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+            t = q.rtn_quantize(w, q.make_grid(w))
+            c = q.encode(t, dic)
+            lst.append(c.to_device(dic))
+            pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
+        host.append(tuple(pair))
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=4)
+    x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
+    assign = q.RouterSim(E, rule="argmax", seed=1, skew=0.5 if T > 50 else 0.0).assign(x)
+    y = layer.forward(x, assign)
+    y_ref = O.moe_layer(x, assign, host, odic)
+    d = bf16_ulp_diff(y, y_ref)
+    assert d.max() <= 2
+    assert np.mean(d == 0) >= 0.99
+    # expert grouping follows buffer order
+    counts = layer.expert_count.cpu().numpy()
+    assert np.array_equal(counts, np.bincount(assign, minlength=E))
+    order = layer.order.cpu().numpy()[:T]
+    want = np.concatenate([np.flatnonzero(assign == e) for e in range(E)])
+    assert np.array_equal(order, want)
+
+
+def test_moe_step_is_graph_capturable(dic):
+    rng = np.random.default_rng(5)
+    E, d_model, d_ff = 4, 64, 256
+    mats = []
+    for e in range(E):
+        for rows, cols in ((d_ff, d_model), (d_model, d_ff)):
+            w = torch.randn(rows, cols, device="cuda") * 0.02
+            codes, mm = q.rtn_quantize_device(w)
+            mats.append(q.encode_device(codes, mm, dic))
+    layer = q.CompressedMoELayer(mats[0::2], mats[1::2], dic, max_tokens=32)
+    x = torch.from_numpy(q.bf16_round(rng.normal(size=(32, d_model)).astype(np.float32))).cuda().to(torch.bfloat16)
+    a = torch.from_numpy(rng.integers(0, E, 32).astype(np.int32)).cuda()
+    out = torch.empty((32, d_model), device="cuda")
+    ref = layer.forward_device(x, a).clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        layer.forward_device(x, a, out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        layer.forward_device(x, a, out=out)
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
