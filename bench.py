@@ -191,7 +191,6 @@ def main():
     import torch.distributed as dist
 
     import paper_2310_16795_b200 as q
-    from paper_2310_16795_b200 import _lib
     from paper_2310_16795_b200.synth import WORKLOADS, build_layer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -294,25 +293,13 @@ def main():
         a = ad[b]
         touched = np.unique(asg[b])
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        T_ = xd[b].shape[0]
-        sp = _lib.stream_ptr(stream)
-        _lib.check(_lib.lib.qmoe_moe_plan(_lib.ptr(a), T_, lay.E, lay.d_ff, lay.d_model, lay.rpu_wi, lay.rpu_wo,
-                                          lay.max_units, _lib.ptr(lay.units_wi), _lib.ptr(lay.units_wo),
-                                          _lib.ptr(lay.n_units), _lib.ptr(lay.expert_count), _lib.ptr(lay.order), sp))
-        h = lay.h[:T_]
-        h.zero_()
+        lay.plan(a, stream)
         evs[0].record(stream)
-        _lib.check(_lib.lib.qmoe_grouped_matvec(lay.handle, _lib.ptr(lay.mats), _lib.ptr(lay.units_wi),
-                                                _lib.ptr(lay.n_units), lay.max_units, max(d_model, d_ff),
-                                                _lib.ptr(xd[b]), _lib.QMOE_X_BF16, d_model, 0, _lib.ptr(h), d_ff,
-                                                _lib.ptr(lay.bad), sp))
+        lay.pass_wi(xd[b], stream)
         evs[1].record(stream)
         outs[l].zero_()
         evs[2].record(stream)
-        _lib.check(_lib.lib.qmoe_grouped_matvec(lay.handle, _lib.ptr(lay.mats), _lib.ptr(lay.units_wo),
-                                                lay.n_units.data_ptr() + 4, lay.max_units, max(d_model, d_ff),
-                                                _lib.ptr(h), _lib.QMOE_X_F32, d_ff, 1, _lib.ptr(outs[l]), d_model,
-                                                _lib.ptr(lay.bad), sp))
+        lay.pass_wo(outs[l], stream)
         evs[3].record(stream)
         torch.cuda.synchronize()
         k_ms["wi"].append(evs[0].elapsed_time(evs[1]))

@@ -54,16 +54,21 @@ enum { QMOE_X_F32 = 0, QMOE_X_BF16 = 1 };
 typedef struct qmoe_dict* qmoe_dict_t;
 
 /* One compressed matrix resident on the device (grouped launches). */
+/* The three arrays must start 16-byte aligned (they are streamed into shared
+ * memory with cp.async.bulk); n_cw = row_off[rows]. */
 typedef struct qmoe_matrix {
   const uint16_t* cw;
   const int32_t* row_off;
   const uint32_t* row_minmax;
   int32_t rows;
   int32_t cols;
+  int32_t n_cw;
+  int32_t pad_;
 } qmoe_matrix;
 
-/* One grouped work unit: rows [row0, row1) of matrix `mat`, applied to
- * `ntok` (<= QMOE_NT_MAX) tokens. Token t of the unit reads x row tok[t]
+/* One grouped work unit: rows [row0, row1) of matrix `mat` (codewords
+ * [cw0, cw1) = [row_off[row0], row_off[row1])), applied to `ntok`
+ * (<= QMOE_NT_MAX) tokens. Token t of the unit reads x row tok[t]
  * (x + tok[t] * ldx) and accumulates into y row tok[t] (y + tok[t] * ldy). */
 typedef struct qmoe_unit {
   int32_t mat;
@@ -71,7 +76,16 @@ typedef struct qmoe_unit {
   int32_t row1;
   int32_t ntok;
   int32_t tok[QMOE_NT_MAX];
+  int32_t cw0;
+  int32_t cw1;
 } qmoe_unit;
+
+/* y modes of the grouped launch */
+enum {
+  QMOE_Y_ACCUM_F32 = 0,     /* y (f32) += bf16(dot)                       (codec.py:243) */
+  QMOE_Y_RELU_BF16 = 1      /* y (bf16) = relu(bf16(dot)) — the FFN hidden h, written
+                               once from zero: equals relu(fused_matvec(wi, x, y=0)) */
+};
 
 /* ------------------------------------------------------------------ host-only
  * These need no GPU (they run on the CPU side of the library). */
@@ -132,12 +146,13 @@ int qmoe_fused_matmat(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_r
 /* Grouped persistent launch over device-resident work units: one kernel,
  * one dictionary-table fill, many (matrix, token) pairs. d_units/d_n_units
  * live in device memory (written e.g. by qmoe_moe_plan), so the call is
- * graph-capturable with no host synchronisation. x_relu applies max(x, 0)
- * while staging x (fuses the FFN activation into the wo pass). */
+ * graph-capturable with no host synchronisation. max_ntok (<= QMOE_NT_MAX)
+ * bounds unit.ntok (sizes the x staging). y_mode: QMOE_Y_ACCUM_F32 or
+ * QMOE_Y_RELU_BF16 (fuses the FFN activation into the wi pass epilogue). */
 int qmoe_grouped_matvec(qmoe_dict_t dict, const qmoe_matrix* d_mats, const qmoe_unit* d_units,
                         const int32_t* d_n_units, int32_t max_units, int32_t max_cols,
-                        const void* d_x, int x_dtype, int64_t ldx, int x_relu, float* d_y,
-                        int64_t ldy, int32_t* d_bad, void* stream);
+                        int32_t max_ntok, const void* d_x, int x_dtype, int64_t ldx, void* d_y,
+                        int y_mode, int64_t ldy, int32_t* d_bad, void* stream);
 
 /* Paper Listing 1 kept as the "paper design on B200"
  * baseline: warp per row, lanes 0..27 extract, decode words read through the
@@ -175,13 +190,16 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
  * lists, then the work units of both FFN passes:
  *   pass 1 (wi, matrix 2e):   units over d_ff rows, tokens of expert e
  *   pass 2 (wo, matrix 2e+1): units over d_model rows, same tokens
- * Units hold up to QMOE_NT_MAX tokens and `rows_per_unit_wi/_wo` rows.
+ * Units hold up to tokens_per_unit (<= QMOE_NT_MAX) tokens and
+ * `rows_per_unit_wi/_wo` rows; d_mats (2E matrices: wi_e = 2e, wo_e = 2e+1)
+ * supplies row_off so each unit carries its codeword range.
  * d_units_wi/_wo must hold max_units entries; counts go to d_n_units[2].
  * d_expert_count (int32[E]) and d_order (int32[T]) are outputs too. */
-int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, int32_t rows_wi,
-                  int32_t rows_wo, int32_t rows_per_unit_wi, int32_t rows_per_unit_wo,
-                  int32_t max_units, qmoe_unit* d_units_wi, qmoe_unit* d_units_wo,
-                  int32_t* d_n_units, int32_t* d_expert_count, int32_t* d_order, void* stream);
+int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats,
+                  int32_t rows_wi, int32_t rows_wo, int32_t rows_per_unit_wi,
+                  int32_t rows_per_unit_wo, int32_t tokens_per_unit, int32_t max_units,
+                  qmoe_unit* d_units_wi, qmoe_unit* d_units_wo, int32_t* d_n_units,
+                  int32_t* d_expert_count, int32_t* d_order, void* stream);
 
 #ifdef __cplusplus
 }

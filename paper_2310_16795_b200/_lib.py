@@ -37,11 +37,16 @@ i32 = ctypes.c_int32
 
 
 class QmoeMatrix(ctypes.Structure):
-    _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("rows", i32), ("cols", i32)]
+    _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("rows", i32), ("cols", i32), ("n_cw", i32),
+                ("pad_", i32)]
 
 
 class QmoeUnit(ctypes.Structure):
-    _fields_ = [("mat", i32), ("row0", i32), ("row1", i32), ("ntok", i32), ("tok", i32 * NT_MAX)]
+    _fields_ = [("mat", i32), ("row0", i32), ("row1", i32), ("ntok", i32), ("tok", i32 * NT_MAX), ("cw0", i32),
+                ("cw1", i32)]
+
+
+QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16 = 0, 1
 
 
 UNIT_BYTES = ctypes.sizeof(QmoeUnit)
@@ -60,14 +65,14 @@ _SIGS = {
     "qmoe_decompress": (ctypes.c_int, [vp, vp, vp, i64, i64, vp, vp, vp]),
     "qmoe_fused_matvec": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, vp, vp, vp]),
     "qmoe_fused_matmat": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, i64, i64, vp, i64, vp, vp]),
-    "qmoe_grouped_matvec": (ctypes.c_int, [vp, vp, vp, vp, i32, i32, vp, ctypes.c_int, i64, ctypes.c_int, vp,
-                                           i64, vp, vp]),
+    "qmoe_grouped_matvec": (ctypes.c_int, [vp, vp, vp, vp, i32, i32, i32, vp, ctypes.c_int, i64, vp,
+                                           ctypes.c_int, i64, vp, vp]),
     "qmoe_paper_matvec": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, vp, vp, vp]),
     "qmoe_encode_count": (ctypes.c_int, [vp, vp, i64, i64, vp, vp]),
     "qmoe_encode_emit": (ctypes.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "qmoe_exclusive_scan": (ctypes.c_int, [vp, i64, vp, vp]),
     "qmoe_rtn_quantize": (ctypes.c_int, [vp, i64, i64, vp, vp, vp, vp]),
-    "qmoe_moe_plan": (ctypes.c_int, [vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "qmoe_moe_plan": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -109,6 +114,28 @@ def ptr(a) -> int:
     if isinstance(a, np.ndarray):
         return a.ctypes.data
     return a.data_ptr()
+
+
+def padded_empty(n: int, dtype, device):
+    """Device buffer of n elements whose storage is 16-byte aligned and
+    readable up to the next 16-byte boundary past element n (the contract of
+    the bulk-copy staging in libqmoe)."""
+    import torch
+
+    esz = torch.empty((), dtype=dtype).element_size()
+    pad = (16 + 15) // esz + 1
+    return torch.empty(n + pad, dtype=dtype, device=device)[:n]
+
+
+def padded_copy(t):
+    """Contiguous padded device copy of tensor t (see padded_empty)."""
+    out = padded_empty(t.numel(), t.dtype, t.device).view(t.shape) if t.dim() <= 1 else None
+    if out is None:
+        flat = padded_empty(t.numel(), t.dtype, t.device)
+        flat.copy_(t.reshape(-1))
+        return flat.view(t.shape)
+    out.copy_(t)
+    return out
 
 
 def stream_ptr(stream=None) -> int:

@@ -103,7 +103,7 @@ class DeviceMatrix:
         ro = torch.from_numpy(np.ascontiguousarray(c.row_off, np.int32)).to(device)
         mm = np.ascontiguousarray(c.row_minmax, np.uint16).reshape(-1, 2) if c.rows else np.zeros((0, 2), np.uint16)
         mmd = torch.from_numpy(mm.copy().view(np.int32).reshape(-1)).to(device)
-        dm = cls(c.rows, c.cols, cw, ro, mmd, c.dict_hash)
+        dm = cls(c.rows, c.cols, _lib.padded_copy(cw), _lib.padded_copy(ro), _lib.padded_copy(mmd), c.dict_hash)
         dm.validate_rows(dic)
         return dm
 
@@ -118,7 +118,9 @@ class DeviceMatrix:
         return self.bad_rows
 
     def descriptor(self) -> tuple:
-        return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(), self.rows, self.cols)
+        """qmoe_matrix fields (include/qmoe.h)."""
+        return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(), self.rows, self.cols,
+                self.n_codewords, 0)
 
 
 def _row_len_error():
@@ -138,15 +140,15 @@ def encode_device(codes, row_minmax, dic: Dictionary, stream=None) -> DeviceMatr
     h = dic.device_handle(dev.index)
     sp = _lib.stream_ptr(stream)
     counts = torch.empty(rows, dtype=torch.int32, device=dev)
-    row_off = torch.empty(rows + 1, dtype=torch.int32, device=dev)
+    row_off = _lib.padded_empty(rows + 1, torch.int32, dev)
     _lib.check(_lib.lib.qmoe_encode_count(h, _lib.ptr(codes), rows, cols, _lib.ptr(counts), sp))
     _lib.check(_lib.lib.qmoe_exclusive_scan(_lib.ptr(counts), rows, _lib.ptr(row_off), sp))
     total = int(row_off[-1].item())
     if total < 0:
         raise ValueError("codeword stream exceeds 32-bit row offsets")
-    cw = torch.empty(total, dtype=torch.int16, device=dev)
+    cw = _lib.padded_empty(total, torch.int16, dev)
     _lib.check(_lib.lib.qmoe_encode_emit(h, _lib.ptr(codes), rows, cols, _lib.ptr(row_off), _lib.ptr(cw), sp))
-    return DeviceMatrix(rows, cols, cw, row_off, row_minmax.contiguous(), dic.hash64)
+    return DeviceMatrix(rows, cols, cw, row_off, _lib.padded_copy(row_minmax.contiguous()), dic.hash64)
 
 
 def encode(t: TernaryMatrix, dic: Dictionary, workers: int = 1) -> CompressedMatrix:
@@ -226,6 +228,7 @@ def fused_matvec_device(dm: DeviceMatrix, dic: Dictionary, x, y, stream=None, ba
     h = dic.device_handle(dm.cw.device.index)
     sp = _lib.stream_ptr(stream)
     xt = _lib.QMOE_X_BF16 if _x_dtype_code(x) == _lib.QMOE_X_BF16 else _lib.QMOE_X_F32
+    x = _staging_x(x)
     if x.dim() == 1:
         _lib.check(_lib.lib.qmoe_fused_matvec(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), _lib.ptr(dm.row_minmax),
                                               dm.rows, dm.cols, _lib.ptr(x), xt, _lib.ptr(y), _lib.ptr(bad), sp))
@@ -233,6 +236,24 @@ def fused_matvec_device(dm: DeviceMatrix, dic: Dictionary, x, y, stream=None, ba
         _lib.check(_lib.lib.qmoe_fused_matmat(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), _lib.ptr(dm.row_minmax),
                                               dm.rows, dm.cols, _lib.ptr(x), xt, x.shape[0], x.stride(0),
                                               _lib.ptr(y), y.stride(0), _lib.ptr(bad), sp))
+
+
+def _staging_x(x):
+    """x rows must start 16-byte aligned with a 16-byte-multiple stride and be
+    readable to the next 16-byte boundary (bulk-copy staging): copy into a
+    padded buffer unless the tensor already satisfies it."""
+    torch = _torch()
+    esz = x.element_size()
+    if x.dim() == 1:
+        x2 = x.reshape(1, -1)
+    else:
+        x2 = x
+    cols = x2.shape[1]
+    ld = ((cols * esz + 15) // 16) * 16 // esz
+    buf = _lib.padded_empty(x2.shape[0] * ld, x.dtype, x.device).view(x2.shape[0], ld)
+    buf[:, :cols].copy_(x2)
+    out = buf[:, :cols]
+    return out.reshape(-1) if x.dim() == 1 else out
 
 
 def _dense_semantics(dm: DeviceMatrix, dic: Dictionary, x32):
@@ -248,6 +269,11 @@ def _dense_semantics(dm: DeviceMatrix, dic: Dictionary, x32):
     lv_max = (mm[:, 1].to(torch.int32) << 16).view(torch.float32)
     w = torch.where(codes == 1, lv_min[:, None], torch.where(codes == 2, lv_max[:, None], torch.zeros((), device=codes.device)))
     part = (w.to(torch.float32) @ x32.to(torch.float32))
+    # The reference rounds with no NaN special case (bf16.py:16-17); on its
+    # x86 host 0 * inf yields the default NaN 0xFFC00000, which survives the
+    # rounding. CUDA's canonical NaN (0x7FFFFFFF) would round to -0.0, so NaNs
+    # are first set to the x86 default pattern.
+    part = torch.where(torch.isnan(part), torch.tensor(-0x400000, dtype=torch.int32, device=part.device).view(torch.float32), part)
     u = part.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
     u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) & 0xFFFF
     return (u << 16).to(torch.int64).to(torch.int32).view(torch.float32)

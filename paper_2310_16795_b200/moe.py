@@ -4,10 +4,10 @@ One step for T tokens with top-1 expert ids:
   1. qmoe_moe_plan      stable counting sort of the assignment (buffer order
                         within an expert, pipeline.py:86-90) and the work
                         units of both FFN passes, written on the device;
-  2. grouped wi pass    h[t] = bf16(wi_e @ x[t]) for every token, one
-                        persistent launch over all touched experts;
-  3. grouped wo pass    y[t] = bf16(wo_e @ relu(h[t])) (ReLU fused into x
-                        staging).
+  2. grouped wi pass    h[t] = relu(bf16(wi_e @ x[t])) written as bf16 (the
+                        ReLU and the bf16 store fused into the epilogue) for
+                        every token, one persistent launch over all experts;
+  3. grouped wo pass    y[t] = bf16(wo_e @ h[t]) accumulated into fp32 y.
 Each touched expert's compressed matrices are streamed from HBM once per
 step: the tokens routed to one expert share a work unit (inner token loop,
 up to QMOE_NT_MAX per unit), so decode is not repeated per token.
@@ -33,7 +33,7 @@ def _rows_per_unit(mats, target_cw: int = 4096) -> int:
     rows = sum(m.rows for m in mats)
     per_row = max(1.0, cw / max(1, rows))
     r = int(target_cw / per_row)
-    r = max(8, min(r, mats[0].rows))
+    r = max(8, min(r, mats[0].rows, 512))
     return r
 
 
@@ -42,7 +42,7 @@ class CompressedMoELayer:
     all DeviceMatrix on one device."""
 
     def __init__(self, wi: list[DeviceMatrix], wo: list[DeviceMatrix], dic: Dictionary, max_tokens: int = 64,
-                 target_cw_per_unit: int = 4096):
+                 target_cw_per_unit: int = 4096, tokens_per_unit: int = 2):
         import torch
 
         if len(wi) != len(wo) or not wi:
@@ -63,6 +63,7 @@ class CompressedMoELayer:
             descs[2 * e + 1] = _lib.QmoeMatrix(*wo[e].descriptor())
         raw = np.frombuffer(bytes(descs), dtype=np.uint8)
         self.mats = torch.from_numpy(raw.copy()).to(self.device)
+        self.tokens_per_unit = int(tokens_per_unit)
         self.rpu_wi = _rows_per_unit(wi, target_cw_per_unit)
         self.rpu_wo = _rows_per_unit(wo, target_cw_per_unit)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
@@ -81,13 +82,43 @@ class CompressedMoELayer:
         self.n_units = torch.zeros(4, dtype=torch.int32, device=dev)
         self.expert_count = torch.zeros(self.E, dtype=torch.int32, device=dev)
         self.order = torch.zeros(max(1, T), dtype=torch.int32, device=dev)
-        self.h = torch.zeros((max(1, T), self.d_ff), dtype=torch.float32, device=dev)
+        # FFN hidden: relu(bf16(wi @ x)) per token, bf16 rows (wo-pass x)
+        self.h = _lib.padded_empty(max(1, T) * self.d_ff, torch.bfloat16, dev).view(max(1, T), self.d_ff)
         self.bad = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
 
+    @staticmethod
+    def _aligned_rows(x) -> bool:
+        esz = x.element_size()
+        return (x.data_ptr() % 16 == 0 and (x.stride(0) * esz) % 16 == 0 and (x.shape[1] * esz) % 16 == 0
+                and x.stride(1) == 1)
+
     # ------------------------------------------------------------------ device step
+    def plan(self, assign, stream=None) -> None:
+        T = assign.shape[0]
+        _lib.check(_lib.lib.qmoe_moe_plan(
+            _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.d_ff, self.d_model, self.rpu_wi, self.rpu_wo,
+            self.tokens_per_unit, self.max_units, _lib.ptr(self.units_wi), _lib.ptr(self.units_wo),
+            _lib.ptr(self.n_units), _lib.ptr(self.expert_count), _lib.ptr(self.order), _lib.stream_ptr(stream)))
+
+    def pass_wi(self, x, stream=None) -> None:
+        import torch
+
+        xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
+        _lib.check(_lib.lib.qmoe_grouped_matvec(
+            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
+            self.d_model, self.tokens_per_unit, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h),
+            _lib.QMOE_Y_RELU_BF16, self.h.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
+
+    def pass_wo(self, out, stream=None) -> None:
+        _lib.check(_lib.lib.qmoe_grouped_matvec(
+            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 4, self.max_units,
+            self.d_ff, self.tokens_per_unit, _lib.ptr(self.h), _lib.QMOE_X_BF16, self.h.stride(0), _lib.ptr(out),
+            _lib.QMOE_Y_ACCUM_F32, out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
+
     def forward_device(self, x, assign, out=None, stream=None):
         """x: (T, d_model) CUDA bf16/f32, assign: (T,) CUDA int32 expert ids.
-        Returns out (T, d_model) float32 = per-token expert FFN output."""
+        Returns out (T, d_model) float32 = per-token expert FFN output
+        wo_e @ relu(wi_e @ x_t) with the reference's per-matvec rounding."""
         import torch
 
         T = x.shape[0]
@@ -95,23 +126,16 @@ class CompressedMoELayer:
             self._alloc(T)
         if out is None:
             out = torch.empty((T, self.d_model), dtype=torch.float32, device=self.device)
-        sp = _lib.stream_ptr(stream)
-        xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
-        _lib.check(_lib.lib.qmoe_moe_plan(
-            _lib.ptr(assign), T, self.E, self.d_ff, self.d_model, self.rpu_wi, self.rpu_wo, self.max_units,
-            _lib.ptr(self.units_wi), _lib.ptr(self.units_wo), _lib.ptr(self.n_units), _lib.ptr(self.expert_count),
-            _lib.ptr(self.order), sp))
-        h = self.h[:T]
-        h.zero_()
-        _lib.check(_lib.lib.qmoe_grouped_matvec(
-            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
-            max(self.d_model, self.d_ff), _lib.ptr(x), xt, x.stride(0), 0, _lib.ptr(h), h.stride(0),
-            _lib.ptr(self.bad), sp))
+        if x.dtype not in (torch.bfloat16, torch.float32):
+            x = x.float()
+        if not self._aligned_rows(x):
+            buf = _lib.padded_empty(T * self.d_model, x.dtype, x.device).view(T, self.d_model)
+            buf.copy_(x)
+            x = buf
+        self.plan(assign, stream)
+        self.pass_wi(x, stream)
         out.zero_()
-        _lib.check(_lib.lib.qmoe_grouped_matvec(
-            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 4, self.max_units,
-            max(self.d_model, self.d_ff), _lib.ptr(h), _lib.QMOE_X_F32, h.stride(0), 1, _lib.ptr(out),
-            out.stride(0), _lib.ptr(self.bad), sp))
+        self.pass_wo(out, stream)
         return out
 
     def forward(self, x: np.ndarray, assign: np.ndarray) -> np.ndarray:

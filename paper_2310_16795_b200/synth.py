@@ -10,6 +10,7 @@ per-expert DeviceMatrix views.
 
 from __future__ import annotations
 
+from . import _lib
 from .codec import DeviceMatrix, encode_device
 from .dictionary import Dictionary
 from .moe import CompressedMoELayer
@@ -33,9 +34,9 @@ def _stacked(E: int, rows: int, cols: int, seed: int, dic: Dictionary, device, c
         starts = ro[:: rows].tolist()  # row_off at every expert boundary (ne + 1 values)
         for k in range(ne):
             a, b = starts[k], starts[k + 1]
-            cw = big.cw[a:b].clone()
-            r = (ro[k * rows : (k + 1) * rows + 1] - a).contiguous()
-            m = mm[k * rows : (k + 1) * rows].clone()
+            cw = _lib.padded_copy(big.cw[a:b])
+            r = _lib.padded_copy(ro[k * rows : (k + 1) * rows + 1] - a)
+            m = _lib.padded_copy(mm[k * rows : (k + 1) * rows])
             mats.append(DeviceMatrix(rows, cols, cw, r, m, dic.hash64))
         del big, mm
     return mats
