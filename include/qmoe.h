@@ -66,19 +66,23 @@ typedef struct qmoe_matrix {
   int32_t pad_;
 } qmoe_matrix;
 
-/* One grouped work unit: rows [row0, row1) of matrix `mat` (codewords
- * [cw0, cw1) = [row_off[row0], row_off[row1])), applied to `ntok`
- * (<= QMOE_NT_MAX) tokens. Token t of the unit reads x row tok[t]
- * (x + tok[t] * ldx) and accumulates into y row tok[t] (y + tok[t] * ldy). */
-typedef struct qmoe_unit {
-  int32_t mat;
+/* One grouped work unit (self-contained, 64 bytes): rows [row0, row1) of the
+ * matrix whose arrays are cw / row_off / row_minmax (codewords [cw0, cw1) =
+ * [row_off[row0], row_off[row1])), applied to `ntok` (<= QMOE_NT_MAX) tokens.
+ * Token t reads x row tok[t] (x + tok[t] * ldx) and writes y row tok[t]
+ * (y + tok[t] * ldy). Written by qmoe_moe_plan (or by the caller). */
+typedef struct qmoe_work {
+  const uint16_t* cw;
+  const int32_t* row_off;
+  const uint32_t* row_minmax;
+  int32_t cols;
   int32_t row0;
   int32_t row1;
   int32_t ntok;
-  int32_t tok[QMOE_NT_MAX];
   int32_t cw0;
   int32_t cw1;
-} qmoe_unit;
+  int32_t tok[QMOE_NT_MAX];
+} qmoe_work;
 
 /* y modes of the grouped launch */
 enum {
@@ -123,10 +127,11 @@ int qmoe_validate_rows(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_
 
 /* decompress (codec.py:175-193 / _decode_range :158-172): d_codes_out is a
  * (rows, cols) uint8 row-major buffer of ternary codes {0,1,2}. Rows that
- * fail the length check are counted in d_bad (as above) and left zero. */
-int qmoe_decompress(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_row_off,
-                    int64_t rows, int64_t cols, uint8_t* d_codes_out, int32_t* d_bad,
-                    void* stream);
+ * fail the length check are counted in d_bad (as above) and left zero.
+ * d_table: NULL (dictionary order) or a frequency codebook (see below). */
+int qmoe_decompress(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d_cw,
+                    const int32_t* d_row_off, int64_t rows, int64_t cols, uint8_t* d_codes_out,
+                    int32_t* d_bad, void* stream);
 
 /* fused_matvec (codec.py:209-244) for one matrix and one x vector.
  * d_x: cols values of type x_dtype; d_y: rows float32, updated in place.
@@ -144,15 +149,31 @@ int qmoe_fused_matmat(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_r
                       int64_t ldy, int32_t* d_bad, void* stream);
 
 /* Grouped persistent launch over device-resident work units: one kernel,
- * one dictionary-table fill, many (matrix, token) pairs. d_units/d_n_units
+ * one dictionary-table fill, many (matrix, token) pairs. d_work/d_n_work
  * live in device memory (written e.g. by qmoe_moe_plan), so the call is
  * graph-capturable with no host synchronisation. max_ntok (<= QMOE_NT_MAX)
- * bounds unit.ntok (sizes the x staging). y_mode: QMOE_Y_ACCUM_F32 or
- * QMOE_Y_RELU_BF16 (fuses the FFN activation into the wi pass epilogue). */
-int qmoe_grouped_matvec(qmoe_dict_t dict, const qmoe_matrix* d_mats, const qmoe_unit* d_units,
-                        const int32_t* d_n_units, int32_t max_units, int32_t max_cols,
+ * bounds work.ntok (sizes the x staging). y_mode: QMOE_Y_ACCUM_F32 or
+ * QMOE_Y_RELU_BF16 (fuses the FFN activation into the wi pass epilogue).
+ * d_table: packed entry table the streams are indexed in — NULL for the
+ * dictionary's own order, or a codebook from qmoe_codebook_table (streams
+ * re-indexed with qmoe_remap). */
+int qmoe_grouped_matvec(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_work* d_work,
+                        const int32_t* d_n_work, int32_t max_work, int32_t max_cols,
                         int32_t max_ntok, const void* d_x, int x_dtype, int64_t ldx, void* d_y,
                         int y_mode, int64_t ldy, int32_t* d_bad, void* stream);
+
+/* ------------------------------------------------------- frequency codebook
+ * Kernel-private re-indexing of the codeword streams of one model/layer by
+ * codeword frequency, so the shared-memory resident prefix of the entry table
+ * holds the most used entries (same stream size, decode unchanged):
+ *   qmoe_histogram  d_counts[c] += occurrences of c in d_cw[0..n)   (uint32[65536])
+ *   qmoe_codebook_table  h_order[k] = codeword of rank k (a permutation of
+ *                   0..65535) -> d_table[k] = packed entry of h_order[k]
+ *   qmoe_remap      d_out[i] = d_rank_of[d_in[i]] (in place allowed) */
+int qmoe_histogram(const uint16_t* d_cw, int64_t n, uint32_t* d_counts, void* stream);
+int qmoe_codebook_table(qmoe_dict_t dict, const uint16_t* h_order, uint32_t* d_table);
+int qmoe_remap(const uint16_t* d_in, int64_t n, const uint16_t* d_rank_of, uint16_t* d_out,
+               void* stream);
 
 /* Paper Listing 1 kept as the "paper design on B200"
  * baseline: warp per row, lanes 0..27 extract, decode words read through the
@@ -197,8 +218,8 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
  * d_expert_count (int32[E]) and d_order (int32[T]) are outputs too. */
 int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats,
                   int32_t rows_wi, int32_t rows_wo, int32_t rows_per_unit_wi,
-                  int32_t rows_per_unit_wo, int32_t tokens_per_unit, int32_t max_units,
-                  qmoe_unit* d_units_wi, qmoe_unit* d_units_wo, int32_t* d_n_units,
+                  int32_t rows_per_unit_wo, int32_t tokens_per_unit, int32_t max_work,
+                  qmoe_work* d_work_wi, qmoe_work* d_work_wo, int32_t* d_n_work,
                   int32_t* d_expert_count, int32_t* d_order, void* stream);
 
 #ifdef __cplusplus

@@ -41,15 +41,16 @@ class QmoeMatrix(ctypes.Structure):
                 ("pad_", i32)]
 
 
-class QmoeUnit(ctypes.Structure):
-    _fields_ = [("mat", i32), ("row0", i32), ("row1", i32), ("ntok", i32), ("tok", i32 * NT_MAX), ("cw0", i32),
-                ("cw1", i32)]
+class QmoeWork(ctypes.Structure):
+    _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("cols", i32), ("row0", i32), ("row1", i32),
+                ("ntok", i32), ("cw0", i32), ("cw1", i32), ("tok", i32 * NT_MAX)]
 
 
 QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16 = 0, 1
 
 
-UNIT_BYTES = ctypes.sizeof(QmoeUnit)
+WORK_BYTES = ctypes.sizeof(QmoeWork)
+NT_STREAM = 2  # tokens per work unit on the streaming (sparse-table) path
 MATRIX_BYTES = ctypes.sizeof(QmoeMatrix)
 
 _SIGS = {
@@ -62,11 +63,14 @@ _SIGS = {
     "qmoe_dict_info": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int)]),
     "qmoe_validate_rows": (ctypes.c_int, [vp, vp, vp, i64, i64, vp, vp]),
-    "qmoe_decompress": (ctypes.c_int, [vp, vp, vp, i64, i64, vp, vp, vp]),
+    "qmoe_decompress": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, vp, vp]),
     "qmoe_fused_matvec": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, vp, vp, vp]),
     "qmoe_fused_matmat": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, i64, i64, vp, i64, vp, vp]),
     "qmoe_grouped_matvec": (ctypes.c_int, [vp, vp, vp, vp, i32, i32, i32, vp, ctypes.c_int, i64, vp,
                                            ctypes.c_int, i64, vp, vp]),
+    "qmoe_histogram": (ctypes.c_int, [vp, i64, vp, vp]),
+    "qmoe_codebook_table": (ctypes.c_int, [vp, vp, vp]),
+    "qmoe_remap": (ctypes.c_int, [vp, i64, vp, vp, vp]),
     "qmoe_paper_matvec": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, vp, vp, vp]),
     "qmoe_encode_count": (ctypes.c_int, [vp, vp, i64, i64, vp, vp]),
     "qmoe_encode_emit": (ctypes.c_int, [vp, vp, i64, i64, vp, vp, vp]),

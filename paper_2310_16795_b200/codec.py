@@ -86,6 +86,9 @@ class DeviceMatrix:
         self.dict_hash = int(dict_hash)
         self.bad_rows = int(bad_rows)
         self.first_bad = first_bad
+        # None: stream indexed in dictionary order; else a frequency codebook
+        # (codebook.Codebook) whose packed table the stream is indexed in
+        self.codebook = None
 
     @property
     def n_codewords(self) -> int:
@@ -192,7 +195,9 @@ def decompress_device(dm: DeviceMatrix, dic: Dictionary, stream=None):
     out = torch.empty((dm.rows, dm.cols), dtype=torch.uint8, device=dm.cw.device)
     bad = torch.tensor([0, INT32_MAX], dtype=torch.int32, device=dm.cw.device)
     h = dic.device_handle(dm.cw.device.index)
-    _lib.check(_lib.lib.qmoe_decompress(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), dm.rows, dm.cols, _lib.ptr(out),
+    table = dm.codebook.table if dm.codebook is not None else None
+    _lib.check(_lib.lib.qmoe_decompress(h, _lib.ptr(table), _lib.ptr(dm.cw), _lib.ptr(dm.row_off), dm.rows, dm.cols,
+                                        _lib.ptr(out),
                                         _lib.ptr(bad), _lib.stream_ptr(stream)))
     return out, bad
 
@@ -225,6 +230,8 @@ def _x_dtype_code(x) -> int:
 def fused_matvec_device(dm: DeviceMatrix, dic: Dictionary, x, y, stream=None, bad=None) -> None:
     """y (CUDA f32, rows) += bf16(M @ x) for x a CUDA f32/bf16 (cols,) tensor,
     or x (ntok, cols) / y (ntok, rows) for an inner token loop."""
+    if dm.codebook is not None:
+        raise ValueError("matrix is re-indexed by a layer codebook; use the grouped/MoE path")
     h = dic.device_handle(dm.cw.device.index)
     sp = _lib.stream_ptr(stream)
     xt = _lib.QMOE_X_BF16 if _x_dtype_code(x) == _lib.QMOE_X_BF16 else _lib.QMOE_X_F32

@@ -177,6 +177,27 @@ int derive_tables(const uint32_t* words, uint32_t* sparse_tab, uint8_t* len_tab,
   return QMOE_OK;
 }
 
+int derive_matvec_tables(const uint32_t* sparse_tab, uint32_t* mtab) {
+  for (int v = 0; v < 2; ++v) {
+    const uint32_t esz = v == 0 ? 4u : 2u;
+    uint32_t* t = mtab + size_t(v) * (QMOE_DICT_SIZE + 1);
+    for (int i = 0; i < QMOE_DICT_SIZE; ++i) {
+      const uint32_t e = sparse_tab[i];
+      uint32_t m = e & 31u;
+      for (int j = 0; j < 3; ++j) {
+        const uint32_t b = (e >> (8 * (j + 1))) & 0xFFu;
+        if (!b) continue;
+        m |= ((b >> 2) * esz) << (5 + 7 * j);
+        m |= 1u << (26 + j);
+        if (b & 2u) m |= 1u << (29 + j);
+      }
+      t[i] = m;
+    }
+    t[QMOE_DICT_SIZE] = 0;
+  }
+  return QMOE_OK;
+}
+
 }  // namespace qmoe
 
 extern "C" {

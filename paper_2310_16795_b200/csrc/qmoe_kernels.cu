@@ -45,6 +45,7 @@ __global__ void validate_rows_kernel(const uint8_t* __restrict__ len_tab, const 
 template <int K>
 __device__ __forceinline__ void dseg_sparse(const uint16_t* __restrict__ cwp, int cnt, int lane,
                                             const SparseTab& tab, uint8_t* out, int64_t cols, int& base) {
+  // matvec-format entries (esz 4 variant): field / 4 = position in the entry
   const int my0 = lane * K;
   uint32_t t[K];
   int sum = 0;
@@ -67,10 +68,9 @@ __device__ __forceinline__ void dseg_sparse(const uint16_t* __restrict__ cwp, in
   for (int k = 0; k < K; ++k) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const uint32_t b = (t[k] >> (8 * j + 8)) & 0xFFu;
-      if (b) {
-        const int c = off + int(b >> 2);
-        if (c < cols) out[c] = (b & 1u) ? 1 : 2;
+      if ((t[k] >> (26 + j)) & 1u) {
+        const int c = off + int(((t[k] >> (5 + 7 * j)) & 0x7Fu) >> 2);
+        if (c < cols) out[c] = ((t[k] >> (29 + j)) & 1u) ? 2 : 1;
       }
     }
     off += int(t[k] & 31u);
@@ -349,7 +349,7 @@ __global__ void rtn_kernel(const float* __restrict__ w, int64_t rows, int64_t co
 __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restrict__ assign, int T, int E,
                                                         const qmoe_matrix* __restrict__ mats, int rows_wi,
                                                         int rows_wo, int rpu_wi, int rpu_wo, int ntu, int max_units,
-                                                        qmoe_unit* units_wi, qmoe_unit* units_wo, int32_t* n_units,
+                                                        qmoe_work* units_wi, qmoe_work* units_wo, int32_t* n_units,
                                                         int32_t* cnt_out, int32_t* order) {
   extern __shared__ int32_t sh[];
   int32_t* cnt = sh;            // E
@@ -417,16 +417,19 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     }
     const int e = lo;
     const int ch = chunk - choff[e];
-    qmoe_unit U;
+    qmoe_work U;
     U.ntok = min(ntu, cnt[e] - ch * ntu);
     for (int q = 0; q < QMOE_NT_MAX; ++q) U.tok[q] = order[start[e] + ch * ntu + min(q, U.ntok - 1)];
-    U.mat = 2 * e + (is_wi ? 0 : 1);
+    const qmoe_matrix M = mats[2 * e + (is_wi ? 0 : 1)];
     const int rows = is_wi ? rows_wi : rows_wo, rpu = is_wi ? rpu_wi : rpu_wo;
+    U.cw = M.cw;
+    U.row_off = M.row_off;
+    U.row_minmax = M.row_minmax;
+    U.cols = M.cols;
     U.row0 = blk * rpu;
     U.row1 = min(rows, U.row0 + rpu);
-    const int32_t* ro = mats[U.mat].row_off;
-    U.cw0 = ro[U.row0];
-    U.cw1 = ro[U.row1];
+    U.cw0 = M.row_off[U.row0];
+    U.cw1 = M.row_off[U.row1];
     (is_wi ? units_wi : units_wo)[j] = U;
   }
   if (threadIdx.x == 0) {
@@ -434,6 +437,18 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     n_units[1] = min(nchunks * nblk_wo, max_units);
     n_units[2] = (nchunks * nblk_wi > max_units || nchunks * nblk_wo > max_units) ? 1 : 0;  // overflow flag
   }
+}
+
+// ================================================================ codebook
+// Frequency codebook (kernel-private re-indexing, include/qmoe.h).
+__global__ void histogram_kernel(const uint16_t* __restrict__ cw, int64_t n, uint32_t* counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(counts + __ldg(cw + i), 1u);
+}
+__global__ void remap_kernel(const uint16_t* __restrict__ in, int64_t n, const uint16_t* __restrict__ rank_of,
+                             uint16_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __ldg(rank_of + in[i]);
 }
 
 bool bad_dict(const qmoe_dict* d) { return d == nullptr || d->d_stab == nullptr; }
@@ -452,6 +467,8 @@ int qmoe_dict_create(const uint32_t* h_words, uint64_t hash64, int device, qmoe_
   int max_nz = 0;
   int rc = qmoe::derive_tables(h_words, stab.data(), len.data(), &max_nz);
   if (rc) return rc;
+  std::vector<uint32_t> mtab(2 * (size_t)(QMOE_DICT_SIZE + 1));
+  qmoe::derive_matvec_tables(stab.data(), mtab.data());
   rc = qmoe::build_trie(h_words, next.data(), ent.data());
   if (rc) return rc;
   CK(cudaSetDevice(device), "cudaSetDevice");
@@ -466,6 +483,8 @@ int qmoe_dict_create(const uint32_t* h_words, uint64_t hash64, int device, qmoe_
   if ((e = cudaMalloc(&d->d_words, QMOE_DICT_SIZE * 8)) != cudaSuccess ||
       (e = cudaMalloc(&d->d_stab, QMOE_DICT_SIZE * 4)) != cudaSuccess ||
       (e = cudaMalloc(&d->d_len, QMOE_DICT_SIZE)) != cudaSuccess ||
+      (e = cudaMalloc(&d->d_mtab, mtab.size() * 4)) != cudaSuccess ||
+      (e = cudaMemcpy(d->d_mtab, mtab.data(), mtab.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMalloc(&d->d_next, next.size() * 4)) != cudaSuccess ||
       (e = cudaMemcpy(d->d_words, h_words, QMOE_DICT_SIZE * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(d->d_stab, stab.data(), QMOE_DICT_SIZE * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -474,6 +493,7 @@ int qmoe_dict_create(const uint32_t* h_words, uint64_t hash64, int device, qmoe_
     qmoe_dict_destroy(d);
     return cuda_fail(e, "dictionary upload");
   }
+  d->h_mtab = std::move(mtab);
   *out = d;
   return QMOE_OK;
 }
@@ -483,6 +503,7 @@ int qmoe_dict_destroy(qmoe_dict_t d) {
   cudaFree(d->d_words);
   cudaFree(d->d_stab);
   cudaFree(d->d_len);
+  cudaFree(d->d_mtab);
   cudaFree(d->d_next);
   delete d;
   return QMOE_OK;
@@ -506,10 +527,11 @@ int qmoe_validate_rows(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row
   return QMOE_OK;
 }
 
-int qmoe_decompress(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_off, int64_t rows, int64_t cols,
-                    uint8_t* d_out, int32_t* d_bad, void* stream) {
+int qmoe_decompress(qmoe_dict_t d, const uint32_t* d_table, const uint16_t* d_cw, const int32_t* d_row_off,
+                    int64_t rows, int64_t cols, uint8_t* d_out, int32_t* d_bad, void* stream) {
   if (bad_dict(d) || rows < 0 || cols < 0 || cols % 2 || !d_bad) return qmoe::fail(QMOE_EINVAL, "bad argument");
   if (rows == 0) return QMOE_OK;
+  if (d_table && !d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
   cudaStream_t st = S(stream);
   if (cols) CK(cudaMemsetAsync(d_out, 0, (size_t)rows * cols, st), "memset");
   // Decompress is write-bound (rows*cols output bytes per ~2 bits read): a
@@ -519,8 +541,8 @@ int qmoe_decompress(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_of
   const size_t smem = (size_t)H * 4;
   if (d->sparse_ok) {
     CK(cudaFuncSetAttribute(decompress_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    decompress_kernel<true><<<(int)blocks, 512, smem, st>>>(d->d_stab, d->d_words, H, d_cw, d_row_off, rows, cols,
-                                                            d_out, d_bad);
+    decompress_kernel<true><<<(int)blocks, 512, smem, st>>>(d_table ? d_table : d->d_mtab, d->d_words, H, d_cw,
+                                                            d_row_off, rows, cols, d_out, d_bad);
   } else {
     decompress_kernel<false><<<(int)blocks, 512, 0, st>>>(d->d_stab, d->d_words, 0, d_cw, d_row_off, rows, cols,
                                                           d_out, d_bad);
@@ -584,7 +606,7 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
 
 int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats, int32_t rows_wi,
                   int32_t rows_wo, int32_t rpu_wi, int32_t rpu_wo, int32_t ntu, int32_t max_units,
-                  qmoe_unit* d_units_wi, qmoe_unit* d_units_wo, int32_t* d_n_units, int32_t* d_expert_count,
+                  qmoe_work* d_units_wi, qmoe_work* d_units_wo, int32_t* d_n_units, int32_t* d_expert_count,
                   int32_t* d_order, void* stream) {
   if (T < 0 || E < 1 || !d_mats || rows_wi < 1 || rows_wo < 1 || rpu_wi < 1 || rpu_wo < 1 || max_units < 0 ||
       ntu < 1 || ntu > QMOE_NT_MAX)
@@ -596,6 +618,40 @@ int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matr
                                                  max_units, d_units_wi, d_units_wo, d_n_units, d_expert_count,
                                                  d_order);
   CK(cudaGetLastError(), "moe_plan_kernel");
+  return QMOE_OK;
+}
+
+int qmoe_histogram(const uint16_t* d_cw, int64_t n, uint32_t* d_counts, void* stream) {
+  if (n < 0 || !d_counts) return qmoe::fail(QMOE_EINVAL, "bad argument");
+  if (n == 0) return QMOE_OK;
+  histogram_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, S(stream)>>>(d_cw, n, d_counts);
+  CK(cudaGetLastError(), "histogram_kernel");
+  return QMOE_OK;
+}
+
+int qmoe_codebook_table(qmoe_dict_t d, const uint16_t* h_order, uint32_t* d_table) {
+  if (bad_dict(d) || !h_order || !d_table) return qmoe::fail(QMOE_EINVAL, "bad argument");
+  if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
+  std::vector<uint8_t> seen(QMOE_DICT_SIZE, 0);
+  const size_t V = QMOE_DICT_SIZE + 1;
+  std::vector<uint32_t> t(2 * V);
+  for (int k = 0; k < QMOE_DICT_SIZE; ++k) {
+    const uint16_t c = h_order[k];
+    if (seen[c]++) return qmoe::fail(QMOE_EINVAL, "order is not a permutation of the 65536 codewords");
+    t[k] = d->h_mtab[c];
+    t[V + k] = d->h_mtab[V + c];
+  }
+  t[V - 1] = 0;
+  t[2 * V - 1] = 0;
+  CK(cudaMemcpy(d_table, t.data(), t.size() * 4, cudaMemcpyHostToDevice), "codebook upload");
+  return QMOE_OK;
+}
+
+int qmoe_remap(const uint16_t* d_in, int64_t n, const uint16_t* d_rank_of, uint16_t* d_out, void* stream) {
+  if (n < 0 || !d_rank_of) return qmoe::fail(QMOE_EINVAL, "bad argument");
+  if (n == 0) return QMOE_OK;
+  remap_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4736), 256, 0, S(stream)>>>(d_in, n, d_rank_of, d_out);
+  CK(cudaGetLastError(), "remap_kernel");
   return QMOE_OK;
 }
 

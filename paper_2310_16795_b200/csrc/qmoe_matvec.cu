@@ -1,18 +1,24 @@
 // Fused dictionary-decode + matvec (codec.py:196-244 semantics) for sm_100a.
 //
 // stream_matvec_kernel — the product path for dictionaries whose entries hold
-// <= 3 non-zero values (the default p0 = 0.885 dictionary):
-//   * persistent: one CTA per SM, a contiguous slice of work units per CTA;
-//   * the hot prefix of the packed entry table (qmoe_internal.h) is staged in
-//     shared memory once per launch; cold entries come through L1/L2;
-//   * each unit's codeword range, row offsets and row scales are streamed into
-//     double-buffered shared memory with cp.async.bulk (TMA bulk copies),
-//     mbarrier-tracked, one unit ahead of the consumers; the x rows of the next
-//     unit are streamed the same way when its tokens differ;
-//   * G lanes per row (G = 8/16/32 from the unit's mean codewords per row),
-//     each lane decoding K consecutive codewords: one sub-warp scan of entry
-//     lengths gives every lane its column offset, then each non-zero slot adds
-//     x[col] to S1 (code 1) or S2 (code 2); y = bf16_rne(min*S1 + max*S2).
+// <= 3 non-zero values (the default p0 = 0.885 dictionary). Persistent, one
+// CTA per SM, warp-specialised:
+//   * warp 0 = producer. Its 32 lanes hold the next 32 work records in
+//     registers (prefetched one batch ahead). Lane 0 stages, per work unit,
+//     the unit's codeword range, row offsets, row scales and (when the tokens
+//     change) the x rows into a STAGES-deep ring of shared-memory slots with
+//     cp.async.bulk, completing a `full` mbarrier; it reuses a slot once all
+//     consumer warps arrived on its `empty` mbarrier.
+//   * warps 1..16 = consumers. G lanes per row (G = 8/16/32 from the unit's
+//     mean codewords per row); each lane decodes K consecutive codewords:
+//     packed-entry lookup (hot prefix of the entry table in shared memory,
+//     the rest through the read-only path), one sub-warp scan of entry lengths
+//     for the column offsets, then <= 3 predicated non-zero slots per entry:
+//     acc += level(code) * x[col] in fp32, y = bf16_rne(sum) (codec.py:243).
+//   * the entry table prefix is filled by one bulk copy at kernel start.
+// Entry format "matvec" (built in qmoe_kernels.cu, esz = bytes per staged x):
+//   bits 0-4 len = 2n | bits 5-11, 12-18, 19-25: position * esz of non-zero
+//   slot 0..2 | bits 26-28 slot used | bits 29-31 slot is code 2 (row max).
 //
 // general_matvec_kernel — any dictionary (e.g. p0 = 0.7, up to 6 non-zeros per
 // entry): expands the two decode words value by value (dictionary.py:115-120).
@@ -25,83 +31,149 @@ using namespace qmoe_dev;
 
 namespace {
 
-constexpr int THREADS = 512;
-constexpr int KSTREAM = 8;          // codewords per lane per pass
-constexpr int CW_CAP = 8192;        // codewords per staged unit buffer
-constexpr int ROW_CAP = 512;        // rows per staged unit
-constexpr int UCHUNK = 64;          // unit records staged per refill
+constexpr int NCONS = 15;                  // consumer warps (16 warps total: 4 per SMSP)
+constexpr int THREADS = (NCONS + 1) * 32;  // + one producer warp
+constexpr int STAGES = 3;
+constexpr int KS = 8;                      // codewords per lane per pass
+constexpr int CW_CAP = 4096;               // codewords per staged unit
+constexpr int ROW_CAP = 256;               // rows per staged unit
+constexpr uint32_t COLD_ZERO = 65536;      // global tables carry a zero entry here
+constexpr int NT_STREAM = 2;               // tokens per unit on the streaming path
 
 // ----------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(saddr(bar)),
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   saddr(dst)),
-               "l"(src), "r"(bytes), "r"(saddr(bar))
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// ----------------------------------------------------------------- unit records
-struct UnitRec {
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) { return (int)lds32(a); }
+
+// codeword of slot (predicated; COLD_ZERO when past the end of the row)
+__device__ __forceinline__ uint32_t load_cw(uint32_t a, bool valid) {
+  uint32_t v;
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .u16 h;\n setp.ne.u32 p, %2, 0;\n mov.u32 %0, %3;\n"
+      " @p ld.shared.u16 h, [%1];\n @p cvt.u32.u16 %0, h;\n}"
+      : "=r"(v)
+      : "r"(a), "r"((uint32_t)valid), "n"(COLD_ZERO)
+      : "memory");
+  return v;
+}
+
+// packed entry: hot prefix from shared memory, the rest (and the zero
+// sentinel at COLD_ZERO) through the non-coherent read-only path
+__device__ __forceinline__ uint32_t lookup(uint32_t c, uint32_t H, uint32_t tab_s, const uint32_t* gtab) {
+  uint32_t e;
+  asm volatile(
+      "{\n .reg .pred ph;\n .reg .u32 a;\n .reg .u64 g;\n"
+      " setp.lt.u32 ph, %1, %2;\n"
+      " mad.lo.u32 a, %1, 4, %3;\n"
+      " mad.wide.u32 g, %1, 4, %4;\n"
+      " @ph ld.shared.u32 %0, [a];\n"
+      " @!ph ld.global.nc.u32 %0, [g];\n}"
+      : "=r"(e)
+      : "r"(c), "r"(H), "r"(tab_s), "l"(gtab)
+      : "memory");
+  return e;
+}
+
+// one non-zero slot: if used, acc += level * x[xoff + field]
+template <int ESZ>
+__device__ __forceinline__ void slot(uint32_t e, int j, uint32_t xoff, float lmin, float lmax, float& acc) {
+  const uint32_t used = (e >> (26 + j)) & 1u;
+  const uint32_t field = (e >> (5 + 7 * j)) & 0x7Fu;
+  const float w = ((e >> (29 + j)) & 1u) ? lmax : lmin;
+  if (ESZ == 4) {
+    float v;
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n mov.f32 %0, 0f00000000;\n"
+        " @p ld.shared.f32 %0, [%1];\n}"
+        : "=f"(v)
+        : "r"(xoff + field), "r"(used)
+        : "memory");
+    acc = fmaf(w, v, acc);
+  } else {
+    uint32_t h;
+    asm volatile(
+        "{\n .reg .pred p;\n .reg .u16 s;\n setp.ne.u32 p, %2, 0;\n mov.u32 %0, 0;\n"
+        " @p ld.shared.u16 s, [%1];\n @p cvt.u32.u16 %0, s;\n}"
+        : "=r"(h)
+        : "r"(xoff + field), "r"(used)
+        : "memory");
+    acc = fmaf(w, __uint_as_float(h << 16), acc);
+  }
+}
+
+// ----------------------------------------------------------------- records
+struct Rec {  // == qmoe_work (64 bytes)
   const uint16_t* cw;
   const int32_t* ro;
   const uint32_t* mm;
   int32_t cols, row0, row1, ntok, cw0, cw1;
   int32_t tok[QMOE_NT_MAX];
 };
+static_assert(sizeof(Rec) == sizeof(qmoe_work), "record layout");
+
+// per-slot staging metadata written by the producer before the full arrive
+struct SlotMeta {
+  Rec r;
+  uint32_t cw_s, ro_s, mm_s, x_s;  // shared addresses of the staged ranges
+  int32_t direct;                  // 1: unit exceeds the slot, read global
+  int32_t pad[3];
+};
 
 struct StreamParams {
-  const uint32_t* gtab;
-  int H;
-  const qmoe_matrix* mats;   // explicit mode
-  const qmoe_unit* units;    // explicit mode (nullptr => implicit single-matrix units)
-  const int32_t* n_units;
-  int max_units;
-  qmoe_matrix single;        // implicit mode
+  const uint32_t* gtab;       // matvec-format table, 65537 entries (zero sentinel last)
+  int H;                      // entries staged in shared memory
+  const qmoe_work* work;      // explicit work list (or nullptr: implicit single matrix)
+  const int32_t* n_work;
+  int max_work;
+  qmoe_matrix single;         // implicit mode
   int rows_per_unit;
   int64_t ntok_single;
-  int ntu_single;            // tokens per implicit unit
+  int ntu_single;
   const void* x;
-  int x_bf16;
   int64_t ldx;
   void* y;
   int y_mode;
   int64_t ldy;
   int32_t* bad;
-  int xcap;                  // elements per token slot of an x buffer (>= cols + 32, multiple of 8)
-  int ntmax;                 // token slots per x buffer
+  int xcap;                   // elements per token slot of an x buffer
+  int ntmax;                  // token slots per x buffer
 };
 
-__device__ __forceinline__ void make_rec(const StreamParams& P, int u, UnitRec& R) {
-  if (P.units) {
-    const qmoe_unit U = P.units[u];
-    const qmoe_matrix M = P.mats[U.mat];
-    R.cw = M.cw;
-    R.ro = M.row_off;
-    R.mm = M.row_minmax;
-    R.cols = M.cols;
-    R.row0 = U.row0;
-    R.row1 = U.row1;
-    R.ntok = U.ntok;
-    R.cw0 = U.cw0;
-    R.cw1 = U.cw1;
+__device__ __forceinline__ void make_rec(const StreamParams& P, int u, Rec& R) {
+  if (P.work) {
+    const uint4* s = reinterpret_cast<const uint4*>(P.work + u);
+    uint4* d = reinterpret_cast<uint4*>(&R);
 #pragma unroll
-    for (int q = 0; q < QMOE_NT_MAX; ++q) R.tok[q] = U.tok[q];
+    for (int i = 0; i < 4; ++i) d[i] = __ldg(s + i);
   } else {
     const int nblk = (P.single.rows + P.rows_per_unit - 1) / P.rows_per_unit;
     const int chunk = u / nblk, blk = u % nblk;
@@ -120,46 +192,43 @@ __device__ __forceinline__ void make_rec(const StreamParams& P, int u, UnitRec& 
   }
 }
 
-__device__ __forceinline__ bool same_x(const UnitRec& a, const UnitRec& b) {
+__device__ __forceinline__ Rec shfl_rec(const Rec& R, int src) {
+  Rec o;
+  const int* a = reinterpret_cast<const int*>(&R);
+  int* b = reinterpret_cast<int*>(&o);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) b[i] = __shfl_sync(FULL_MASK, a[i], src);
+  return o;
+}
+
+__device__ __forceinline__ bool same_x(const Rec& a, const Rec& b) {
   bool s = a.cols == b.cols && a.ntok == b.ntok;
 #pragma unroll
   for (int q = 0; q < QMOE_NT_MAX; ++q) s = s && (q >= a.ntok || a.tok[q] == b.tok[q]);
   return s;
 }
 
-// where a staged range landed: element offset of `begin` inside the buffer
-struct Staged {
-  int dcw, dro, dmm, dx[QMOE_NT_MAX];
-  int xbuf;
-  int direct;  // 1 => unit too large for the buffers: read cw/ro/mm from global
-};
+__device__ __forceinline__ uint32_t span(const void* begin, size_t nbytes, uint32_t& delta, uintptr_t& a0) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(begin);
+  a0 = a & ~uintptr_t(15);
+  delta = (uint32_t)(a - a0);
+  return (uint32_t)(((a + nbytes + 15) & ~uintptr_t(15)) - a0);
+}
 
-// ----------------------------------------------------------------- x access
-template <typename XT>
-__device__ __forceinline__ float xval(const XT* p);
-template <>
-__device__ __forceinline__ float xval<float>(const float* p) { return *p; }
-template <>
-__device__ __forceinline__ float xval<uint16_t>(const uint16_t* p) { return __uint_as_float(uint32_t(*p) << 16); }
-
-// ----------------------------------------------------------------- decode segment
+// ----------------------------------------------------------------- consumer
 // G lanes share one row; lane `gl` owns codewords [gl*K, gl*K + K) of this pass.
-template <int K, int NT, typename XT>
-__device__ __forceinline__ void seg(const uint16_t* cwp, int cnt, int gl, int G, const uint32_t* tab_s, int H,
-                                    const uint32_t* __restrict__ gtab, const XT* xs, int xcap, int& base,
-                                    float (&a1)[NT], float (&a2)[NT]) {
+template <int K, int NT, int ESZ>
+__device__ __noinline__ void seg(uint32_t cw_a, int cnt, int gl, int G, uint32_t tab_s, uint32_t H,
+                                   const uint32_t* gtab, uint32_t xbase, uint32_t xslot, int& base, float lmin,
+                                   float lmax, float (&acc)[NT]) {
   const int my0 = gl * K;
   uint32_t t[K];
   int sum = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    uint32_t e = 0;
-    if (my0 + k < cnt) {
-      const uint32_t c = cwp[my0 + k];
-      e = c < (uint32_t)H ? tab_s[c] : __ldg(gtab + c);
-    }
-    t[k] = e;
-    sum += int(e & 31u);
+    const uint32_t c = load_cw(cw_a + 2u * (my0 + k), my0 + k < cnt);
+    t[k] = lookup(c, H, tab_s, gtab);
+    sum += int(t[k] & 31u);
   }
   int incl = sum;
 #pragma unroll
@@ -168,75 +237,69 @@ __device__ __forceinline__ void seg(const uint16_t* cwp, int cnt, int gl, int G,
     const int v = __shfl_up_sync(FULL_MASK, incl, d, G);
     if (gl >= d) incl += v;
   }
-  int off = base + incl - sum;
+  uint32_t xoff = xbase + (uint32_t)(base + incl - sum) * ESZ;
   base += __shfl_sync(FULL_MASK, incl, G - 1, G);
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const uint32_t e = t[k];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const uint32_t b = (e >> (8 * j + 8)) & 0xFFu;
-      if (b) {
-        const int c = off + int(b >> 2);
-        float xv[NT];
-#pragma unroll
-        for (int q = 0; q < NT; ++q) xv[q] = xval<XT>(xs + q * xcap + c);
-        if (b & 1u) {
-#pragma unroll
-          for (int q = 0; q < NT; ++q) a1[q] += xv[q];
-        } else {
-#pragma unroll
-          for (int q = 0; q < NT; ++q) a2[q] += xv[q];
-        }
-      }
+    for (int q = 0; q < NT; ++q) {
+      slot<ESZ>(e, 0, xoff + q * xslot, lmin, lmax, acc[q]);
+      slot<ESZ>(e, 1, xoff + q * xslot, lmin, lmax, acc[q]);
+      slot<ESZ>(e, 2, xoff + q * xslot, lmin, lmax, acc[q]);
     }
-    off += int(e & 31u);
+    xoff += (e & 31u) * ESZ;
   }
 }
 
-template <int NT, typename XT>
-__device__ __forceinline__ void run_rows(const StreamParams& P, const UnitRec& R, const uint16_t* cwp,
-                                         const int32_t* rop, const uint32_t* mmp, const XT* xs, const uint32_t* tab_s) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+template <int NT, int ESZ>
+__device__ __forceinline__ void run_unit(const StreamParams& P, const SlotMeta& M, uint32_t tab_s, int cwarp,
+                                         int u) {
+  const Rec& R = M.r;
+  const int lane = threadIdx.x & 31;
   const int nrows = R.row1 - R.row0;
   const int avg = nrows > 0 ? (R.cw1 - R.cw0) / nrows : 0;
   const int G = avg <= 48 ? 8 : (avg <= 96 ? 16 : 32);
   const int RG = 32 / G;
   const int g = lane / G, gl = lane % G;
-  for (int i0 = warp * RG; i0 < nrows; i0 += nw * RG) {
-    const int i = i0 + g;
+  const int ngroups = (nrows + RG - 1) / RG;
+  const uint32_t xslot = (uint32_t)P.xcap * ESZ;
+  // rotate the group -> warp assignment per unit so imbalance averages out
+  int gi0 = cwarp - (u % NCONS);
+  if (gi0 < 0) gi0 += NCONS;
+  for (int gi = gi0; gi < ngroups; gi += NCONS) {
+    const int i = gi * RG + g;
     const bool valid = i < nrows;
-    const int s = valid ? rop[i] - R.cw0 : 0;
-    const int n = valid ? rop[i + 1] - R.cw0 - s : 0;
+    int s = 0, n = 0;
+    uint32_t mm = 0;
+    if (valid) {
+      s = lds_s32(M.ro_s + 4u * i) - R.cw0;
+      n = lds_s32(M.ro_s + 4u * (i + 1)) - R.cw0 - s;
+      mm = lds32(M.mm_s + 4u * i);
+    }
+    const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
     const int maxn = __reduce_max_sync(FULL_MASK, n);
-    float a1[NT], a2[NT];
+    float acc[NT];
 #pragma unroll
-    for (int q = 0; q < NT; ++q) a1[q] = a2[q] = 0.f;
+    for (int q = 0; q < NT; ++q) acc[q] = 0.f;
     int base = 0;
-    for (int p = 0; p < maxn; p += G * KSTREAM) {
-      const int K = (min(maxn - p, G * KSTREAM) + G - 1) / G;
-      const uint16_t* c = cwp + s + p;
+    for (int p = 0; p < maxn; p += G * KS) {
+      const int K = (min(maxn - p, G * KS) + G - 1) / G;
+      const uint32_t cw_a = M.cw_s + 2u * (uint32_t)(s + p);
       const int cnt = n - p;
       switch (K) {
 #define QMOE_K(KK) \
-  case KK: seg<KK, NT, XT>(c, cnt, gl, G, tab_s, P.H, P.gtab, xs, P.xcap, base, a1, a2); break;
+  case KK: seg<KK, NT, ESZ>(cw_a, cnt, gl, G, tab_s, (uint32_t)P.H, P.gtab, M.x_s, xslot, base, lmin, lmax, acc); break;
         QMOE_K(1) QMOE_K(2) QMOE_K(3) QMOE_K(4) QMOE_K(5) QMOE_K(6) QMOE_K(7) QMOE_K(8)
 #undef QMOE_K
         default: break;
       }
     }
-    // sub-warp reductions (all lanes participate)
-    float s1[NT], s2[NT];
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      s1[q] = a1[q];
-      s2[q] = a2[q];
 #pragma unroll
-      for (int d = 16; d >= 1; d >>= 1) {
-        if (d >= G) continue;
-        s1[q] += __shfl_xor_sync(FULL_MASK, s1[q], d);
-        s2[q] += __shfl_xor_sync(FULL_MASK, s2[q], d);
-      }
+      for (int d = 16; d >= 1; d >>= 1)
+        if (d < G) acc[q] += __shfl_xor_sync(FULL_MASK, acc[q], d);
     }
     if (!valid || gl != 0) continue;
     const int r = R.row0 + i;
@@ -247,12 +310,10 @@ __device__ __forceinline__ void run_rows(const StreamParams& P, const UnitRec& R
       }
       continue;
     }
-    const uint32_t mm = mmp[i];
-    const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (q >= R.ntok) break;
-      const float v = bf16_round_dev(fmaf(lmin, s1[q], lmax * s2[q]));
+      const float v = bf16_round_dev(acc[q]);
       if (P.y_mode == QMOE_Y_RELU_BF16) {
         uint16_t* yp = reinterpret_cast<uint16_t*>(P.y) + (int64_t)R.tok[q] * P.ldy + r;
         *yp = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
@@ -264,140 +325,234 @@ __device__ __forceinline__ void run_rows(const StreamParams& P, const UnitRec& R
   }
 }
 
-template <typename XT>
+// Slow path for units larger than a slot: everything read from global.
+template <int ESZ>
+__device__ void run_unit_direct(const StreamParams& P, const SlotMeta& M, int cwarp) {
+  const Rec& R = M.r;
+  const int lane = threadIdx.x & 31;
+  for (int i = cwarp; i < R.row1 - R.row0; i += NCONS) {
+    const int r = R.row0 + i;
+    const int s = __ldg(R.ro + r), e = __ldg(R.ro + r + 1);
+    const uint32_t mm = __ldg(R.mm + r);
+    const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
+    float acc[QMOE_NT_MAX] = {0.f, 0.f, 0.f, 0.f};
+    int base = 0;
+    for (int p0 = s; p0 < e; p0 += 32) {
+      const uint32_t c = p0 + lane < e ? (uint32_t)__ldg(R.cw + p0 + lane) : COLD_ZERO;
+      const uint32_t t = __ldg(P.gtab + c);
+      const int len = int(t & 31u);
+      int incl = len;
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(FULL_MASK, incl, d);
+        if (lane >= d) incl += v;
+      }
+      const int off = base + incl - len;
+      base += __shfl_sync(FULL_MASK, incl, 31);
+      for (int j = 0; j < 3; ++j) {
+        if (!((t >> (26 + j)) & 1u)) continue;
+        const int col = off + int(((t >> (5 + 7 * j)) & 0x7Fu) / ESZ);
+        const float w = ((t >> (29 + j)) & 1u) ? lmax : lmin;
+        for (int q = 0; q < R.ntok; ++q) {
+          const int64_t xi = (int64_t)R.tok[q] * P.ldx + col;
+          const float xv = ESZ == 2 ? __uint_as_float(uint32_t(__ldg(reinterpret_cast<const uint16_t*>(P.x) + xi)) << 16)
+                                    : __ldg(reinterpret_cast<const float*>(P.x) + xi);
+          acc[q] = fmaf(w, xv, acc[q]);
+        }
+      }
+    }
+    for (int q = 0; q < QMOE_NT_MAX; ++q) acc[q] = warp_sum(acc[q]);
+    if (lane != 0) continue;
+    if (base != R.cols) {
+      if (P.bad) {
+        atomicAdd(P.bad, 1);
+        atomicMin(P.bad + 1, r);
+      }
+      continue;
+    }
+    for (int q = 0; q < R.ntok; ++q) {
+      const float v = bf16_round_dev(acc[q]);
+      if (P.y_mode == QMOE_Y_RELU_BF16)
+        reinterpret_cast<uint16_t*>(P.y)[(int64_t)R.tok[q] * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+      else {
+        float* yp = reinterpret_cast<float*>(P.y) + (int64_t)R.tok[q] * P.ldy + r;
+        *yp = *yp + v;
+      }
+    }
+  }
+}
+
+struct Carve {
+  uint32_t tab_s, bar_full, bar_empty, bar_tab, cwbuf, robuf, mmbuf, xbuf, xbytes;
+  SlotMeta* meta;
+  Rec* ring;  // producer's record ring [RING]
+};
+constexpr int RING = 64;
+
+// Producer warp: keeps the work records of the next 32 units in flight in
+// registers, the current 64 in a shared-memory ring, and stages one unit per
+// iteration into the ring of STAGES slots (lane 0 issues the bulk copies).
+template <int ESZ>
+__device__ __noinline__ void producer(const StreamParams& P, const Carve& C, int u0, int u1) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    mbar_arrive_expect_tx(C.bar_tab, (uint32_t)P.H * 4);
+    if (P.H > 0) bulk_g2s(C.tab_s, P.gtab, (uint32_t)P.H * 4, C.bar_tab);
+  }
+  Rec nxt;
+  for (int v = u0 + lane; v < min(u1, u0 + RING); v += 32) {
+    Rec r;
+    make_rec(P, v, r);
+    C.ring[(v - u0) % RING] = r;
+  }
+  if (u0 + RING + lane < u1) make_rec(P, u0 + RING + lane, nxt);
+  __syncwarp();
+  int cur_xb = 1;
+  int last_x_unit[2] = {-1, -1};
+  int consumed = -1;  // highest relative unit known consumed
+  for (int u = u0; u < u1; ++u) {
+    const int rel = u - u0;
+    if (lane == 0) {
+      const Rec& R = C.ring[rel % RING];
+      const int s = rel % STAGES;
+      if (rel >= STAGES) {
+        while (consumed < rel - STAGES) {
+          ++consumed;
+          mbar_wait(C.bar_empty + 8 * (consumed % STAGES), (uint32_t)((consumed / STAGES) & 1));
+        }
+      }
+      SlotMeta& M = C.meta[s];
+      const int nrows = R.row1 - R.row0;
+      const int ncw = R.cw1 - R.cw0;
+      M.r = R;
+      M.direct = (ncw > CW_CAP || nrows > ROW_CAP) ? 1 : 0;
+      const bool reuse = rel > 0 && same_x(C.ring[(rel - 1) % RING], R);
+      int xb = cur_xb;
+      if (!reuse) {
+        xb = cur_xb ^ 1;
+        const int v = last_x_unit[xb];
+        while (v >= 0 && consumed < v) {
+          ++consumed;
+          mbar_wait(C.bar_empty + 8 * (consumed % STAGES), (uint32_t)((consumed / STAGES) & 1));
+        }
+      }
+      last_x_unit[xb] = rel;
+      cur_xb = xb;
+      M.x_s = C.xbuf + (uint32_t)xb * C.xbytes;
+      const uint32_t full = C.bar_full + 8 * s;
+      const uint32_t cw_dst = C.cwbuf + s * (CW_CAP * 2 + 64);
+      const uint32_t ro_dst = C.robuf + s * (ROW_CAP * 4 + 64);
+      const uint32_t mm_dst = C.mmbuf + s * (ROW_CAP * 4 + 64);
+      uintptr_t acw = 0, aro = 0, amm = 0;
+      uint32_t bcw = 0, bro = 0, bmm = 0, dcw = 0, dro = 0, dmm = 0, total = 0;
+      if (!M.direct) {
+        bcw = span(R.cw + R.cw0, (size_t)ncw * 2, dcw, acw);
+        bro = span(R.ro + R.row0, (size_t)(nrows + 1) * 4, dro, aro);
+        bmm = span(R.mm + R.row0, (size_t)nrows * 4, dmm, amm);
+        total = bcw + bro + bmm;
+      }
+      const size_t xrow = (size_t)R.cols * ESZ;
+      const uint32_t xrow16 = (uint32_t)((xrow + 15) & ~size_t(15));  // x rows are 16-byte aligned
+      if (!reuse) total += xrow16 * (uint32_t)R.ntok;
+      M.cw_s = cw_dst + dcw;
+      M.ro_s = ro_dst + dro;
+      M.mm_s = mm_dst + dmm;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(full, total);  // releases M.* to the consumers
+      if (bcw) bulk_g2s(cw_dst, reinterpret_cast<const void*>(acw), bcw, full);
+      if (bro) bulk_g2s(ro_dst, reinterpret_cast<const void*>(aro), bro, full);
+      if (bmm) bulk_g2s(mm_dst, reinterpret_cast<const void*>(amm), bmm, full);
+      if (!reuse) {
+        for (int q = 0; q < R.ntok; ++q)
+          bulk_g2s(M.x_s + (uint32_t)q * P.xcap * ESZ,
+                   reinterpret_cast<const uint8_t*>(P.x) + (int64_t)R.tok[q] * P.ldx * ESZ, xrow16, full);
+      }
+    }
+    // refill: after the last unit of a 32-batch, park the prefetched records
+    // (units rel+33 .. rel+64 relative... i.e. the batch two ahead) in the
+    // half of the ring that just drained, and prefetch the next batch
+    if ((rel & 31) == 31) {
+      __syncwarp();
+      const int v = u + 1 + (RING - 32) + lane;  // units [u+33, u+65) relative to the ring's next half
+      if (v < u1) C.ring[(v - u0) % RING] = nxt;
+      __syncwarp();
+      if (v + 32 < u1) make_rec(P, v + 32, nxt);
+    }
+    __syncwarp();
+  }
+}
+
+template <int ESZ>
 __global__ void __launch_bounds__(THREADS, 1) stream_matvec_kernel(StreamParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* tab_s = reinterpret_cast<uint32_t*>(smem);
+  Carve C;
+  C.tab_s = saddr(smem);
   uint8_t* p = smem + (size_t)P.H * 4;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(p);          // [2]
+  C.bar_full = saddr(p);  // STAGES x 8
+  C.bar_empty = C.bar_full + 8 * STAGES;
+  C.bar_tab = C.bar_empty + 8 * STAGES;
   p += 128;
-  UnitRec* urec = reinterpret_cast<UnitRec*>(p);           // [UCHUNK]
-  p += ((sizeof(UnitRec) * UCHUNK + 127) / 128) * 128;
-  Staged* stg = reinterpret_cast<Staged*>(p);              // [2]
-  p += 256;
-  uint16_t* cwbuf = reinterpret_cast<uint16_t*>(p);        // [2][CW_CAP + 16]
-  p += 2 * (CW_CAP + 16) * 2;
-  int32_t* robuf = reinterpret_cast<int32_t*>(p);          // [2][ROW_CAP + 8]
-  p += 2 * (ROW_CAP + 8) * 4;
-  uint32_t* mmbuf = reinterpret_cast<uint32_t*>(p);        // [2][ROW_CAP + 8]
-  p += 2 * (ROW_CAP + 8) * 4;
-  XT* xbuf = reinterpret_cast<XT*>(p);                     // [2][ntmax][xcap]
-  const int xslot = P.ntmax * P.xcap;
+  C.meta = reinterpret_cast<SlotMeta*>(p);
+  p += ((sizeof(SlotMeta) * STAGES + 127) / 128) * 128;
+  C.ring = reinterpret_cast<Rec*>(p);
+  p += sizeof(Rec) * RING;
+  C.cwbuf = saddr(p);
+  p += STAGES * (CW_CAP * 2 + 64);
+  C.robuf = saddr(p);
+  p += STAGES * (ROW_CAP * 4 + 64);
+  C.mmbuf = saddr(p);
+  p += STAGES * (ROW_CAP * 4 + 64);
+  C.xbuf = saddr(p);  // [2][ntmax][xcap]
+  C.xbytes = (uint32_t)P.ntmax * P.xcap * ESZ;
 
-  // ---- table fill (all threads), barrier init, first unit records
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
-    uint4* dst = reinterpret_cast<uint4*>(tab_s);
-    for (int i = threadIdx.x; i < P.H / 4; i += blockDim.x) dst[i] = __ldg(src + i);
-  }
   int n;
-  if (P.units) n = min(*P.n_units, P.max_units);
+  if (P.work) n = min(*P.n_work, P.max_work);
   else {
     const int nblk = (P.single.rows + P.rows_per_unit - 1) / P.rows_per_unit;
     n = nblk * (int)((P.ntok_single + P.ntu_single - 1) / P.ntu_single);
   }
   const int u0 = (int)((int64_t)n * blockIdx.x / gridDim.x);
   const int u1 = (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
+  if (u0 >= u1) return;  // whole CTA exits before any barrier use
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(C.bar_full + 8 * s, 1);
+      mbar_init(C.bar_empty + 8 * s, NCONS);
+    }
+    mbar_init(C.bar_tab, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int v = u0 + (int)threadIdx.x; v < min(u1, u0 + UCHUNK); v += blockDim.x) make_rec(P, v, urec[v % UCHUNK]);
   __syncthreads();
-  if (u0 >= u1) return;
 
-  const size_t esz = sizeof(XT);
-  // producer: stage unit u into slot s (thread 0 only)
-  // producer: stage unit u into slot s (thread 0 only). Offsets are published
-  // in stg[s] BEFORE the mbarrier arrive, whose release orders them for the
-  // consumers' acquire-wait; then the bulk copies complete the transaction.
-  auto span = [](const void* begin, size_t nbytes, int esz_, int& delta, uintptr_t& a0) -> uint32_t {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(begin);
-    a0 = a & ~uintptr_t(15);
-    delta = (int)((a - a0) / esz_);
-    return (uint32_t)(((a + nbytes + 15) & ~uintptr_t(15)) - a0);
-  };
-  auto issue = [&](int u, int s, const UnitRec* prev, int prev_xbuf) {
-    const UnitRec& R = urec[u % UCHUNK];
-    Staged& S = stg[s];
-    const int nrows = R.row1 - R.row0;
-    S.direct = (R.cw1 - R.cw0 > CW_CAP || nrows > ROW_CAP) ? 1 : 0;
-    const bool reuse = prev && same_x(*prev, R);
-    S.xbuf = reuse ? prev_xbuf : (prev ? prev_xbuf ^ 1 : 0);
-    uintptr_t acw = 0, aro = 0, amm = 0, ax[QMOE_NT_MAX] = {0, 0, 0, 0};
-    uint32_t bcw = 0, bro = 0, bmm = 0, bx[QMOE_NT_MAX] = {0, 0, 0, 0};
-    if (!S.direct) {
-      bcw = span(R.cw + R.cw0, (size_t)(R.cw1 - R.cw0) * 2, 2, S.dcw, acw);
-      bro = span(R.ro + R.row0, (size_t)(nrows + 1) * 4, 4, S.dro, aro);
-      bmm = span(R.mm + R.row0, (size_t)nrows * 4, 4, S.dmm, amm);
+  if (warp == 0) {
+    producer<ESZ>(P, C, u0, u1);
+  } else {
+    const int cwarp = warp - 1;
+    mbar_wait(C.bar_tab, 0);
+    for (int u = u0; u < u1; ++u) {
+      const int rel = u - u0;
+      const int s = rel % STAGES;
+      mbar_wait(C.bar_full + 8 * s, (uint32_t)((rel / STAGES) & 1));
+      const SlotMeta& M = C.meta[s];
+      if (M.direct) run_unit_direct<ESZ>(P, M, cwarp);
+      else if (M.r.ntok == 1) run_unit<1, ESZ>(P, M, C.tab_s, cwarp, u);
+      else run_unit<2, ESZ>(P, M, C.tab_s, cwarp, u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(C.bar_empty + 8 * s);
     }
-    if (!reuse) {
-      for (int q = 0; q < R.ntok; ++q)
-        bx[q] = span(reinterpret_cast<const uint8_t*>(P.x) + (int64_t)R.tok[q] * P.ldx * (int64_t)esz,
-                     (size_t)R.cols * esz, (int)esz, S.dx[q], ax[q]);
-    }
-    uint32_t total = bcw + bro + bmm;
-    for (int q = 0; q < QMOE_NT_MAX; ++q) total += bx[q];
-    fence_proxy_async();
-    mbar_arrive_expect_tx(&bar[s], total);
-    if (bcw) bulk_g2s(cwbuf + s * (CW_CAP + 16), reinterpret_cast<const void*>(acw), bcw, &bar[s]);
-    if (bro) bulk_g2s(robuf + s * (ROW_CAP + 8), reinterpret_cast<const void*>(aro), bro, &bar[s]);
-    if (bmm) bulk_g2s(mmbuf + s * (ROW_CAP + 8), reinterpret_cast<const void*>(amm), bmm, &bar[s]);
-    for (int q = 0; q < QMOE_NT_MAX; ++q)
-      if (bx[q]) bulk_g2s(xbuf + (size_t)S.xbuf * xslot + (size_t)q * P.xcap, reinterpret_cast<const void*>(ax[q]), bx[q], &bar[s]);
-  };
-
-  if (threadIdx.x == 0) issue(u0, 0, nullptr, 1);
-  // unit records live in a ring of UCHUNK slots (unit u -> slot u % UCHUNK);
-  // units [u0, loaded) are present. A refill never overwrites unit u's slot.
-  int loaded = min(u1, u0 + UCHUNK);
-  for (int u = u0; u < u1; ++u) {
-    const int s = (u - u0) & 1;
-    const uint32_t parity = ((u - u0) >> 1) & 1;
-    __syncthreads();  // everyone finished unit u-1: its slot and (if unused now) x buffer are free
-    if (u + 1 < u1 && u + 1 >= loaded) {
-      const int hi = min(u1, u + UCHUNK);
-      for (int v = loaded + (int)threadIdx.x; v < hi; v += blockDim.x) make_rec(P, v, urec[v % UCHUNK]);
-      loaded = hi;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0 && u + 1 < u1) issue(u + 1, s ^ 1, &urec[u % UCHUNK], stg[s].xbuf);
-    mbar_wait(&bar[s], parity);
-    const UnitRec& R = urec[u % UCHUNK];
-    const Staged S = stg[s];
-    const uint16_t* cwp;
-    const int32_t* rop;
-    const uint32_t* mmp;
-    if (S.direct) {
-      cwp = R.cw + R.cw0;
-      rop = R.ro + R.row0;
-      mmp = R.mm + R.row0;
-    } else {
-      cwp = cwbuf + s * (CW_CAP + 16) + S.dcw;
-      rop = robuf + s * (ROW_CAP + 8) + S.dro;
-      mmp = mmbuf + s * (ROW_CAP + 8) + S.dmm;
-    }
-    // x rows are 16-byte aligned (checked host-side), so every token slot
-    // starts at delta 0 and token q sits at xs0 + q * xcap.
-    const XT* xs0 = xbuf + (size_t)S.xbuf * xslot + S.dx[0];
-    if (R.ntok == 1) run_rows<1, XT>(P, R, cwp, rop, mmp, xs0, tab_s);
-    else if (R.ntok == 2) run_rows<2, XT>(P, R, cwp, rop, mmp, xs0, tab_s);
-    else run_rows<4, XT>(P, R, cwp, rop, mmp, xs0, tab_s);
   }
 }
 
 // ----------------------------------------------------------------- general path
 // Any dictionary: decode words read through the cache, value-by-value walk.
-// Warp per row; simple and exact (not the tuned path).
+// Warp per row over a flat work list; exact, not the tuned path.
 struct GeneralParams {
   const uint32_t* words;
-  const qmoe_matrix* mats;
-  const qmoe_unit* units;
-  const int32_t* n_units;
-  int max_units;
+  const qmoe_work* work;
+  const int32_t* n_work;
+  int max_work;
   qmoe_matrix single;
-  int rows_per_unit;
   int64_t ntok_single;
   const void* x;
   int x_bf16;
@@ -410,37 +565,44 @@ struct GeneralParams {
 
 __global__ void __launch_bounds__(256) general_matvec_kernel(GeneralParams P) {
   const int lane = threadIdx.x & 31;
-  int n;
-  if (P.units) n = min(*P.n_units, P.max_units);
-  else n = ((P.single.rows + P.rows_per_unit - 1) / P.rows_per_unit) * (int)P.ntok_single;
+  const int n = P.work ? min(*P.n_work, P.max_work) : (int)P.ntok_single;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  // work item = (unit, row) flattened; warps stride over it
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   for (int u = 0; u < n; ++u) {
-    qmoe_matrix M;
-    int row0, row1, ntok, tok[QMOE_NT_MAX];
-    if (P.units) {
-      const qmoe_unit U = P.units[u];
-      M = P.mats[U.mat];
-      row0 = U.row0;
-      row1 = U.row1;
-      ntok = U.ntok;
-      for (int q = 0; q < QMOE_NT_MAX; ++q) tok[q] = U.tok[q];
+    const uint16_t* cw;
+    const int32_t* ro;
+    const uint32_t* mmv;
+    int cols, row0, row1, ntok, tok[QMOE_NT_MAX];
+    if (P.work) {
+      const qmoe_work W = P.work[u];
+      cw = W.cw;
+      ro = W.row_off;
+      mmv = W.row_minmax;
+      cols = W.cols;
+      row0 = W.row0;
+      row1 = W.row1;
+      ntok = W.ntok;
+      for (int q = 0; q < QMOE_NT_MAX; ++q) tok[q] = W.tok[q];
     } else {
-      const int nblk = (P.single.rows + P.rows_per_unit - 1) / P.rows_per_unit;
-      M = P.single;
-      row0 = (u % nblk) * P.rows_per_unit;
-      row1 = min(M.rows, row0 + P.rows_per_unit);
+      cw = P.single.cw;
+      ro = P.single.row_off;
+      mmv = P.single.row_minmax;
+      cols = P.single.cols;
+      row0 = 0;
+      row1 = P.single.rows;
       ntok = 1;
-      tok[0] = u / nblk;
+      tok[0] = u;
     }
-    for (int r = row0 + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < row1; r += nw) {
-      const int s = __ldg(M.row_off + r), e = __ldg(M.row_off + r + 1);
-      float a1[QMOE_NT_MAX] = {0, 0, 0, 0}, a2[QMOE_NT_MAX] = {0, 0, 0, 0};
+    for (int r = row0 + w0; r < row1; r += nw) {
+      const int s = __ldg(ro + r), e = __ldg(ro + r + 1);
+      float acc[QMOE_NT_MAX] = {0, 0, 0, 0};
+      const uint32_t mm = __ldg(mmv + r);
+      const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
       int base = 0;
       for (int p0 = s; p0 < e; p0 += 32) {
         const int i = p0 + lane;
         uint2 w = make_uint2(0u, 0u);
-        if (i < e) w = __ldg(reinterpret_cast<const uint2*>(P.words) + __ldg(M.cw + i));
+        if (i < e) w = __ldg(reinterpret_cast<const uint2*>(P.words) + __ldg(cw + i));
         const int len = 2 * int(w.x & 15u);
         int incl = len;
         for (int d = 1; d < 32; d <<= 1) {
@@ -451,32 +613,27 @@ __global__ void __launch_bounds__(256) general_matvec_kernel(GeneralParams P) {
         base += __shfl_sync(FULL_MASK, incl, 31);
         for (int v = 0; v < len; ++v) {
           const uint32_t code = ((v < 14 ? w.x : w.y) >> (4 + 2 * (v % 14))) & 3u;
-          if (!code || off + v >= M.cols) continue;
+          if (!code || off + v >= cols) continue;
+          const float lv = code == 1u ? lmin : lmax;
           for (int q = 0; q < ntok; ++q) {
             const int64_t xi = (int64_t)tok[q] * P.ldx + off + v;
             const float xv = P.x_bf16 ? __uint_as_float(uint32_t(__ldg(reinterpret_cast<const uint16_t*>(P.x) + xi)) << 16)
                                       : __ldg(reinterpret_cast<const float*>(P.x) + xi);
-            if (code == 1u) a1[q] += xv;
-            else a2[q] += xv;
+            acc[q] = fmaf(lv, xv, acc[q]);
           }
         }
       }
-      for (int q = 0; q < QMOE_NT_MAX; ++q) {
-        a1[q] = warp_sum(a1[q]);
-        a2[q] = warp_sum(a2[q]);
-      }
+      for (int q = 0; q < QMOE_NT_MAX; ++q) acc[q] = warp_sum(acc[q]);
       if (lane != 0) continue;
-      if (base != M.cols) {
+      if (base != cols) {
         if (P.bad) {
           atomicAdd(P.bad, 1);
           atomicMin(P.bad + 1, r);
         }
         continue;
       }
-      const uint32_t mm = __ldg(M.row_minmax + r);
-      const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
       for (int q = 0; q < ntok; ++q) {
-        const float v = bf16_round_dev(fmaf(lmin, a1[q], lmax * a2[q]));
+        const float v = bf16_round_dev(acc[q]);
         if (P.y_mode == QMOE_Y_RELU_BF16) {
           reinterpret_cast<uint16_t*>(P.y)[(int64_t)tok[q] * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
         } else {
@@ -490,8 +647,8 @@ __global__ void __launch_bounds__(256) general_matvec_kernel(GeneralParams P) {
 
 // ----------------------------------------------------------------- host side
 size_t fixed_smem() {
-  return 128 + ((sizeof(UnitRec) * UCHUNK + 127) / 128) * 128 + 256 + 2 * (CW_CAP + 16) * 2 +
-         2 * 2 * (ROW_CAP + 8) * 4;
+  return 128 + ((sizeof(SlotMeta) * STAGES + 127) / 128) * 128 + sizeof(Rec) * RING + STAGES * (CW_CAP * 2 + 64) +
+         2 * STAGES * (ROW_CAP * 4 + 64);
 }
 
 int hot_override() {
@@ -503,9 +660,10 @@ int hot_override() {
   return v;
 }
 
-int launch_stream(const qmoe_dict* d, StreamParams& P, int max_cols, int ntmax, int grid, int hot_want,
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int launch_stream(const qmoe_dict* d, StreamParams& P, int esz, int max_cols, int ntmax, int grid, int hot_want,
                   cudaStream_t st) {
-  const size_t esz = P.x_bf16 ? 2 : 4;
   P.ntmax = ntmax;
   P.xcap = ((max_cols + 32 + 15) / 16) * 16;
   const size_t xbytes = 2 * (size_t)ntmax * P.xcap * esz;
@@ -515,23 +673,25 @@ int launch_stream(const qmoe_dict* d, StreamParams& P, int max_cols, int ntmax, 
   int H = (int)((d->max_smem_optin - fixed) / 4);
   if (hot_override() >= 0) hot_want = hot_override();
   H = std::min(H, std::min(hot_want, QMOE_DICT_SIZE));
-  H &= ~1023;
+  H &= ~255;
   P.H = H;
   const size_t smem = (size_t)H * 4 + fixed;
-  if (P.x_bf16) {
-    CK(cudaFuncSetAttribute(stream_matvec_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-       "attr");
-    stream_matvec_kernel<uint16_t><<<grid, THREADS, smem, st>>>(P);
+  if (esz == 2) {
+    CK(cudaFuncSetAttribute(stream_matvec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    stream_matvec_kernel<2><<<grid, THREADS, smem, st>>>(P);
   } else {
-    CK(cudaFuncSetAttribute(stream_matvec_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-       "attr");
-    stream_matvec_kernel<float><<<grid, THREADS, smem, st>>>(P);
+    CK(cudaFuncSetAttribute(stream_matvec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    stream_matvec_kernel<4><<<grid, THREADS, smem, st>>>(P);
   }
   CK(cudaGetLastError(), "stream_matvec_kernel launch");
   return QMOE_OK;
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+const uint32_t* pick_table(const qmoe_dict* d, const uint32_t* user, int esz) {
+  // codebooks hold both variants back to back: [esz 4 | esz 2], 65537 entries each
+  if (user) return esz == 4 ? user : user + (QMOE_DICT_SIZE + 1);
+  return esz == 4 ? d->d_mtab : d->d_mtab + (QMOE_DICT_SIZE + 1);
+}
 
 }  // namespace
 
@@ -545,25 +705,23 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
     return qmoe::fail(QMOE_EINVAL, "bad argument");
   if (rows > INT32_MAX / 2 || cols > INT32_MAX / 2) return qmoe::fail(QMOE_EINVAL, "matrix too large");
   if (rows == 0 || ntok == 0 || cols == 0) return QMOE_OK;
-  const size_t esz = x_dtype == QMOE_X_BF16 ? 2 : 4;
+  const int esz = x_dtype == QMOE_X_BF16 ? 2 : 4;
   if (!aligned16(d_cw) || !aligned16(d_row_off) || !aligned16(d_mm) || !aligned16(d_x) || (ldx * esz) % 16)
     return qmoe::fail(QMOE_EINVAL, "device arrays must be 16-byte aligned (and x rows 16-byte strided)");
-  // Rows per unit from a typical ~24 values per codeword (no host sync; a
-  // unit that outgrows the staging buffers is read directly from global).
-  const int32_t n_cw = (int32_t)std::min<int64_t>(INT32_MAX, rows * cols / 24 + rows);
-  const double per_row = std::max(1.0, (double)cols / 24.0);
-  int rpu = (int)std::max(1.0, std::min(4096.0 / per_row, (double)ROW_CAP));
-  const int ntu = (int)std::min<int64_t>(ntok, QMOE_NT_MAX);
   if (d->sparse_ok) {
+    // rows per unit from a typical ~24 values per codeword (no host sync; a
+    // unit that outgrows a slot is read directly from global)
+    const double per_row = std::max(1.0, (double)cols / 24.0);
+    const int rpu = (int)std::max(1.0, std::min(0.75 * CW_CAP / per_row, (double)ROW_CAP));
+    const int ntu = (int)std::min<int64_t>(ntok, NT_STREAM);
     StreamParams P{};
-    P.gtab = d->d_stab;
-    P.units = nullptr;
-    P.single = qmoe_matrix{d_cw, d_row_off, d_mm, (int32_t)rows, (int32_t)cols, n_cw, 0};
+    P.gtab = pick_table(d, nullptr, esz);
+    P.work = nullptr;
+    P.single = qmoe_matrix{d_cw, d_row_off, d_mm, (int32_t)rows, (int32_t)cols, 0, 0};
     P.rows_per_unit = rpu;
     P.ntok_single = ntok;
     P.ntu_single = ntu;
     P.x = d_x;
-    P.x_bf16 = x_dtype == QMOE_X_BF16;
     P.ldx = ldx;
     P.y = d_y;
     P.y_mode = QMOE_Y_ACCUM_F32;
@@ -573,13 +731,13 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
     const int64_t units = nblk * ((ntok + ntu - 1) / ntu);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, d->num_sms));
     // small launches stage a smaller hot table (the fill is per CTA)
-    const int want = (int)std::min<int64_t>(QMOE_DICT_SIZE, std::max<int64_t>(8192, (int64_t)n_cw / grid * 4));
-    return launch_stream(d, P, (int)cols, ntu, grid, want, S(stream));
+    const int64_t est_cw = rows * cols / 24 + rows;
+    const int want = (int)std::min<int64_t>(QMOE_DICT_SIZE, std::max<int64_t>(4096, est_cw / grid * 2));
+    return launch_stream(d, P, esz, (int)cols, ntu, grid, want, S(stream));
   }
   GeneralParams G{};
   G.words = d->d_words;
-  G.single = qmoe_matrix{d_cw, d_row_off, d_mm, (int32_t)rows, (int32_t)cols, n_cw, 0};
-  G.rows_per_unit = (int)rows;
+  G.single = qmoe_matrix{d_cw, d_row_off, d_mm, (int32_t)rows, (int32_t)cols, 0, 0};
   G.ntok_single = ntok;
   G.x = d_x;
   G.x_bf16 = x_dtype == QMOE_X_BF16;
@@ -607,38 +765,37 @@ int qmoe_fused_matmat(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_
   return fused_common(d, d_cw, d_row_off, d_mm, rows, cols, d_x, x_dtype, ntok, ldx, d_y, ldy, d_bad, stream);
 }
 
-int qmoe_grouped_matvec(qmoe_dict_t d, const qmoe_matrix* d_mats, const qmoe_unit* d_units, const int32_t* d_n_units,
-                        int32_t max_units, int32_t max_cols, int32_t max_ntok, const void* d_x, int x_dtype,
+int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work* d_work, const int32_t* d_n_work,
+                        int32_t max_work, int32_t max_cols, int32_t max_ntok, const void* d_x, int x_dtype,
                         int64_t ldx, void* d_y, int y_mode, int64_t ldy, int32_t* d_bad, void* stream) {
-  if (!d || !d->d_stab || !d_mats || !d_units || !d_n_units || max_units < 0 || max_cols <= 0 || max_ntok < 1 ||
+  if (!d || !d->d_stab || !d_work || !d_n_work || max_work < 0 || max_cols <= 0 || max_ntok < 1 ||
       max_ntok > QMOE_NT_MAX || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16) ||
       (y_mode != QMOE_Y_ACCUM_F32 && y_mode != QMOE_Y_RELU_BF16))
     return qmoe::fail(QMOE_EINVAL, "bad argument");
-  const size_t esz = x_dtype == QMOE_X_BF16 ? 2 : 4;
+  const int esz = x_dtype == QMOE_X_BF16 ? 2 : 4;
   if (!aligned16(d_x) || (ldx * esz) % 16) return qmoe::fail(QMOE_EINVAL, "x rows must be 16-byte aligned");
-  if (max_units == 0) return QMOE_OK;
+  if (max_work == 0) return QMOE_OK;
   if (d->sparse_ok) {
+    if (max_ntok > NT_STREAM) return qmoe::fail(QMOE_EUNSUPPORTED, "streaming path takes <= 2 tokens per unit");
     StreamParams P{};
-    P.gtab = d->d_stab;
-    P.mats = d_mats;
-    P.units = d_units;
-    P.n_units = d_n_units;
-    P.max_units = max_units;
+    P.gtab = pick_table(d, d_table, esz);
+    P.work = d_work;
+    P.n_work = d_n_work;
+    P.max_work = max_work;
     P.x = d_x;
-    P.x_bf16 = x_dtype == QMOE_X_BF16;
     P.ldx = ldx;
     P.y = d_y;
     P.y_mode = y_mode;
     P.ldy = ldy;
     P.bad = d_bad;
-    return launch_stream(d, P, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
+    return launch_stream(d, P, esz, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
   }
+  if (d_table) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
   GeneralParams G{};
   G.words = d->d_words;
-  G.mats = d_mats;
-  G.units = d_units;
-  G.n_units = d_n_units;
-  G.max_units = max_units;
+  G.work = d_work;
+  G.n_work = d_n_work;
+  G.max_work = max_work;
   G.x = d_x;
   G.x_bf16 = x_dtype == QMOE_X_BF16;
   G.ldx = ldx;

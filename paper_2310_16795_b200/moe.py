@@ -42,7 +42,7 @@ class CompressedMoELayer:
     all DeviceMatrix on one device."""
 
     def __init__(self, wi: list[DeviceMatrix], wo: list[DeviceMatrix], dic: Dictionary, max_tokens: int = 64,
-                 target_cw_per_unit: int = 4096, tokens_per_unit: int = 2):
+                 target_cw_per_unit: int = 3072, tokens_per_unit: int = 2, codebook: bool = True):
         import torch
 
         if len(wi) != len(wo) or not wi:
@@ -57,13 +57,24 @@ class CompressedMoELayer:
         self.wi, self.wo, self.dic = wi, wo, dic
         self.device = wi[0].cw.device
         self.handle = dic.device_handle(self.device.index)
+        # layer-level frequency codebook (kernel-private stream re-indexing)
+        self.codebook = None
+        if codebook and dic.device_info(self.device.index)["sparse_path"]:
+            from .codebook import Codebook
+
+            mats = list(wi) + list(wo)
+            if all(m.codebook is None for m in mats):
+                self.codebook = Codebook(dic, mats)
+                self.codebook.apply(mats)
+            elif len({id(m.codebook) for m in mats}) == 1:
+                self.codebook = mats[0].codebook
         descs = (_lib.QmoeMatrix * (2 * self.E))()
         for e in range(self.E):
             descs[2 * e] = _lib.QmoeMatrix(*wi[e].descriptor())
             descs[2 * e + 1] = _lib.QmoeMatrix(*wo[e].descriptor())
         raw = np.frombuffer(bytes(descs), dtype=np.uint8)
         self.mats = torch.from_numpy(raw.copy()).to(self.device)
-        self.tokens_per_unit = int(tokens_per_unit)
+        self.tokens_per_unit = min(int(tokens_per_unit), _lib.NT_STREAM)
         self.rpu_wi = _rows_per_unit(wi, target_cw_per_unit)
         self.rpu_wo = _rows_per_unit(wo, target_cw_per_unit)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
@@ -77,8 +88,8 @@ class CompressedMoELayer:
         nblk = max((self.d_ff + self.rpu_wi - 1) // self.rpu_wi, (self.d_model + self.rpu_wo - 1) // self.rpu_wo)
         self.max_units = max(1, T * nblk)
         dev = self.device
-        self.units_wi = torch.empty(self.max_units * _lib.UNIT_BYTES, dtype=torch.uint8, device=dev)
-        self.units_wo = torch.empty(self.max_units * _lib.UNIT_BYTES, dtype=torch.uint8, device=dev)
+        self.units_wi = torch.empty(self.max_units * _lib.WORK_BYTES, dtype=torch.uint8, device=dev)
+        self.units_wo = torch.empty(self.max_units * _lib.WORK_BYTES, dtype=torch.uint8, device=dev)
         self.n_units = torch.zeros(4, dtype=torch.int32, device=dev)
         self.expert_count = torch.zeros(self.E, dtype=torch.int32, device=dev)
         self.order = torch.zeros(max(1, T), dtype=torch.int32, device=dev)
@@ -100,18 +111,21 @@ class CompressedMoELayer:
             self.tokens_per_unit, self.max_units, _lib.ptr(self.units_wi), _lib.ptr(self.units_wo),
             _lib.ptr(self.n_units), _lib.ptr(self.expert_count), _lib.ptr(self.order), _lib.stream_ptr(stream)))
 
+    def _table(self) -> int:
+        return self.codebook.table.data_ptr() if self.codebook is not None else 0
+
     def pass_wi(self, x, stream=None) -> None:
         import torch
 
         xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
         _lib.check(_lib.lib.qmoe_grouped_matvec(
-            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
+            self.handle, self._table(), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
             self.d_model, self.tokens_per_unit, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h),
             _lib.QMOE_Y_RELU_BF16, self.h.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def pass_wo(self, out, stream=None) -> None:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
-            self.handle, _lib.ptr(self.mats), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 4, self.max_units,
+            self.handle, self._table(), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 4, self.max_units,
             self.d_ff, self.tokens_per_unit, _lib.ptr(self.h), _lib.QMOE_X_BF16, self.h.stride(0), _lib.ptr(out),
             _lib.QMOE_Y_ACCUM_F32, out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 

@@ -98,3 +98,25 @@ def test_moe_step_is_graph_capturable(dic):
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_codebook_reindexing_is_exact(dic):
+    """Frequency codebook: streams rewritten to ranks decode to the same codes
+    and the packed table follows the permutation."""
+    from paper_2310_16795_b200.codebook import Codebook
+    from paper_2310_16795_b200.codec import decompress_device
+
+    mats = []
+    for k in range(3):
+        w = torch.randn(300, 1024, device="cuda") * 0.02
+        codes, mm = q.rtn_quantize_device(w)
+        mats.append((codes, q.encode_device(codes, mm, dic)))
+    cb = Codebook(dic, [m for _, m in mats])
+    before = [m.cw.clone() for _, m in mats]
+    cb.apply([m for _, m in mats])
+    assert cb.hit_rate(40960) >= cb.counts[:40960].sum() / cb.counts.sum()
+    for (codes, m), b in zip(mats, before):
+        assert not torch.equal(m.cw, b)
+        out, bad = decompress_device(m, dic)
+        assert int(bad[0]) == 0
+        assert torch.equal(out, codes)
