@@ -297,7 +297,6 @@ def main():
         evs[0].record(stream)
         lay.pass_wi(xd[b], stream)
         evs[1].record(stream)
-        outs[l].zero_()
         evs[2].record(stream)
         lay.pass_wo(outs[l], stream)
         evs[3].record(stream)

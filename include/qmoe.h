@@ -54,41 +54,52 @@ enum { QMOE_X_F32 = 0, QMOE_X_BF16 = 1 };
 typedef struct qmoe_dict* qmoe_dict_t;
 
 /* One compressed matrix resident on the device (grouped launches). */
-/* The three arrays must start 16-byte aligned (they are streamed into shared
- * memory with cp.async.bulk); n_cw = row_off[rows]. */
+/* The arrays must start 16-byte aligned and be readable up to the next
+ * 16-byte boundary past their end (they are streamed into shared memory with
+ * cp.async.bulk); n_cw = row_off[rows].
+ * ck / lg: optional row-segment checkpoints (qmoe_checkpoints): with G = 2^lg
+ * lanes per row, ck[r * (G-1) + j - 1] is the column at which segment j of row
+ * r starts (segment j = codewords [s + j*n/G, s + (j+1)*n/G) of the row's n).
+ * lg = 0, ck = NULL: one lane per row. */
 typedef struct qmoe_matrix {
   const uint16_t* cw;
   const int32_t* row_off;
   const uint32_t* row_minmax;
+  const uint16_t* ck;
   int32_t rows;
   int32_t cols;
   int32_t n_cw;
-  int32_t pad_;
+  int32_t lg;
 } qmoe_matrix;
 
-/* One grouped work unit (self-contained, 64 bytes): rows [row0, row1) of the
- * matrix whose arrays are cw / row_off / row_minmax (codewords [cw0, cw1) =
- * [row_off[row0], row_off[row1])), applied to `ntok` (<= QMOE_NT_MAX) tokens.
- * Token t reads x row tok[t] (x + tok[t] * ldx) and writes y row tok[t]
- * (y + tok[t] * ldy). Written by qmoe_moe_plan (or by the caller). */
+/* One grouped work unit (self-contained, 80 bytes): rows [row0, row1) of the
+ * matrix whose arrays are cw / row_off / row_minmax / ck (codewords [cw0, cw1)
+ * = [row_off[row0], row_off[row1])), applied to `ntok` (<= 2 on the streaming
+ * path) tokens. Token t reads x row tok[t] (x + tok[t] * ldx) and writes y row
+ * tok[t] (y + tok[t] * ldy). Written by qmoe_moe_plan (or by the caller). */
 typedef struct qmoe_work {
   const uint16_t* cw;
   const int32_t* row_off;
   const uint32_t* row_minmax;
+  const uint16_t* ck;
   int32_t cols;
   int32_t row0;
   int32_t row1;
   int32_t ntok;
   int32_t cw0;
   int32_t cw1;
+  int32_t lg;
+  int32_t pad_;
   int32_t tok[QMOE_NT_MAX];
 } qmoe_work;
 
 /* y modes of the grouped launch */
 enum {
   QMOE_Y_ACCUM_F32 = 0,     /* y (f32) += bf16(dot)                       (codec.py:243) */
-  QMOE_Y_RELU_BF16 = 1      /* y (bf16) = relu(bf16(dot)) — the FFN hidden h, written
+  QMOE_Y_RELU_BF16 = 1,     /* y (bf16) = relu(bf16(dot)) — the FFN hidden h, written
                                once from zero: equals relu(fused_matvec(wi, x, y=0)) */
+  QMOE_Y_STORE_F32 = 2      /* y (f32) = 0 + bf16(dot): accumulate into a zero y
+                               without reading it */
 };
 
 /* ------------------------------------------------------------------ host-only
@@ -174,6 +185,15 @@ int qmoe_histogram(const uint16_t* d_cw, int64_t n, uint32_t* d_counts, void* st
 int qmoe_codebook_table(qmoe_dict_t dict, const uint16_t* h_order, uint32_t* d_table);
 int qmoe_remap(const uint16_t* d_in, int64_t n, const uint16_t* d_rank_of, uint16_t* d_out,
                void* stream);
+
+/* Row-segment checkpoints for a matrix (kernel-private, derived once): for
+ * G = 2^lg (1 <= lg <= 3) segments per row, d_ck[r*(G-1) + j-1] = column where
+ * segment j of row r starts. d_table selects the entry order the stream is
+ * indexed in (NULL = dictionary). Rows that do not decode to cols values are
+ * counted in d_bad (int32[2], as qmoe_validate_rows). */
+int qmoe_checkpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d_cw,
+                     const int32_t* d_row_off, int64_t rows, int64_t cols, int lg, uint16_t* d_ck,
+                     int32_t* d_bad, void* stream);
 
 /* Paper Listing 1 kept as the "paper design on B200"
  * baseline: warp per row, lanes 0..27 extract, decode words read through the

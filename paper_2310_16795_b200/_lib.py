@@ -37,16 +37,17 @@ i32 = ctypes.c_int32
 
 
 class QmoeMatrix(ctypes.Structure):
-    _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("rows", i32), ("cols", i32), ("n_cw", i32),
-                ("pad_", i32)]
+    _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("ck", vp), ("rows", i32), ("cols", i32),
+                ("n_cw", i32), ("lg", i32)]
 
 
 class QmoeWork(ctypes.Structure):
-    _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("cols", i32), ("row0", i32), ("row1", i32),
-                ("ntok", i32), ("cw0", i32), ("cw1", i32), ("tok", i32 * NT_MAX)]
+    _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("ck", vp), ("cols", i32), ("row0", i32),
+                ("row1", i32), ("ntok", i32), ("cw0", i32), ("cw1", i32), ("lg", i32), ("pad_", i32),
+                ("tok", i32 * NT_MAX)]
 
 
-QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16 = 0, 1
+QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16, QMOE_Y_STORE_F32 = 0, 1, 2
 
 
 WORK_BYTES = ctypes.sizeof(QmoeWork)
@@ -71,6 +72,7 @@ _SIGS = {
     "qmoe_histogram": (ctypes.c_int, [vp, i64, vp, vp]),
     "qmoe_codebook_table": (ctypes.c_int, [vp, vp, vp]),
     "qmoe_remap": (ctypes.c_int, [vp, i64, vp, vp, vp]),
+    "qmoe_checkpoints": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, ctypes.c_int, vp, vp, vp]),
     "qmoe_paper_matvec": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, vp, vp, vp]),
     "qmoe_encode_count": (ctypes.c_int, [vp, vp, i64, i64, vp, vp]),
     "qmoe_encode_emit": (ctypes.c_int, [vp, vp, i64, i64, vp, vp, vp]),

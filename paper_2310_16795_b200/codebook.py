@@ -21,6 +21,8 @@ import numpy as np
 from . import _lib
 from .dictionary import DICT_SIZE, Dictionary
 
+MT_STRIDE = 65540  # entries per table variant (csrc/qmoe_internal.h)
+
 
 class Codebook:
     def __init__(self, dic: Dictionary, mats, device=None):
@@ -43,7 +45,7 @@ class Codebook:
         self.rank_of = np.empty(DICT_SIZE, np.uint16)
         self.rank_of[self.order] = np.arange(DICT_SIZE, dtype=np.uint16)
         self.counts = c
-        self.table = torch.empty(2 * (DICT_SIZE + 1), dtype=torch.int32, device=dev)
+        self.table = torch.empty(2 * MT_STRIDE, dtype=torch.int32, device=dev)
         _lib.check(_lib.lib.qmoe_codebook_table(h, _lib.ptr(self.order), _lib.ptr(self.table)))
         self._rank_dev = torch.from_numpy(self.rank_of.view(np.int16).copy()).to(dev)
 

@@ -89,6 +89,9 @@ class DeviceMatrix:
         # None: stream indexed in dictionary order; else a frequency codebook
         # (codebook.Codebook) whose packed table the stream is indexed in
         self.codebook = None
+        # row-segment checkpoints (G = 2^lg lanes per row), see build_checkpoints
+        self.ck = None
+        self.lg = 0
 
     @property
     def n_codewords(self) -> int:
@@ -122,8 +125,33 @@ class DeviceMatrix:
 
     def descriptor(self) -> tuple:
         """qmoe_matrix fields (include/qmoe.h)."""
-        return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(), self.rows, self.cols,
-                self.n_codewords, 0)
+        return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(),
+                self.ck.data_ptr() if self.ck is not None else 0, self.rows, self.cols, self.n_codewords, self.lg)
+
+    def mean_codewords_per_row(self) -> float:
+        return self.n_codewords / max(1, self.rows)
+
+    def build_checkpoints(self, dic: Dictionary, lg: int | None = None) -> None:
+        """Kernel-private row-segment checkpoints (qmoe_checkpoints): the column
+        at which each of the G = 2^lg segments of every row starts, so G lanes
+        walk one row independently. lg=None picks ~48 codewords per segment."""
+        torch = _torch()
+        if lg is None:
+            avg = self.mean_codewords_per_row()
+            lg = 0 if avg <= 48 else (1 if avg <= 96 else (2 if avg <= 192 else 3))
+        self.lg = int(lg)
+        if self.lg == 0 or self.rows == 0:
+            self.ck = None
+            return
+        G = 1 << self.lg
+        self.ck = _lib.padded_empty(self.rows * (G - 1), torch.int16, self.cw.device)
+        bad = torch.tensor([0, INT32_MAX], dtype=torch.int32, device=self.cw.device)
+        table = self.codebook.table if self.codebook is not None else None
+        _lib.check(_lib.lib.qmoe_checkpoints(dic.device_handle(self.cw.device.index), _lib.ptr(table),
+                                             _lib.ptr(self.cw), _lib.ptr(self.row_off), self.rows, self.cols,
+                                             self.lg, _lib.ptr(self.ck), _lib.ptr(bad), _lib.stream_ptr()))
+        if int(bad[0].item()):
+            raise CorruptionError("row decodes to the wrong number of values")
 
 
 def _row_len_error():

@@ -21,7 +21,7 @@ struct qmoe_dict {
   int max_smem_optin = 0;
   uint32_t* d_words = nullptr;   // (65536, 2) decode words
   uint32_t* d_stab = nullptr;    // sparse entry table (see qmoe_internal.h)
-  uint32_t* d_mtab = nullptr;    // matvec-format tables: [esz 4 | esz 2] x 65537 (zero sentinel last)
+  uint32_t* d_mtab = nullptr;    // matvec-format tables: [esz 4 | esz 2] x MT_STRIDE (zero entries from 65536)
   std::vector<uint32_t> h_mtab;  // host copy (codebook construction)
   uint8_t* d_len = nullptr;      // 2n per entry
   int32_t* d_next = nullptr;     // trie next_node (65537, 9)

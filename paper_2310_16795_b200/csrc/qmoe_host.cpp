@@ -180,7 +180,7 @@ int derive_tables(const uint32_t* words, uint32_t* sparse_tab, uint8_t* len_tab,
 int derive_matvec_tables(const uint32_t* sparse_tab, uint32_t* mtab) {
   for (int v = 0; v < 2; ++v) {
     const uint32_t esz = v == 0 ? 4u : 2u;
-    uint32_t* t = mtab + size_t(v) * (QMOE_DICT_SIZE + 1);
+    uint32_t* t = mtab + size_t(v) * MT_STRIDE;
     for (int i = 0; i < QMOE_DICT_SIZE; ++i) {
       const uint32_t e = sparse_tab[i];
       uint32_t m = e & 31u;
@@ -193,7 +193,7 @@ int derive_matvec_tables(const uint32_t* sparse_tab, uint32_t* mtab) {
       }
       t[i] = m;
     }
-    t[QMOE_DICT_SIZE] = 0;
+    for (int i = QMOE_DICT_SIZE; i < MT_STRIDE; ++i) t[i] = 0;
   }
   return QMOE_OK;
 }

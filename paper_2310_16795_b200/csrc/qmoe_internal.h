@@ -20,10 +20,13 @@ int build_trie(const uint32_t* words, int32_t* next_node, int32_t* entry_of_node
 int derive_tables(const uint32_t* words, uint32_t* sparse_tab, uint8_t* len_tab, int* max_nz);
 
 // Matvec-format tables (see qmoe_matvec.cu header), two variants back to back
-// for staged x of 4-byte and 2-byte elements, each 65537 entries with a zero
-// entry at index 65536 (the kernels' padding sentinel):
+// for staged x of 4-byte and 2-byte elements, each MT_STRIDE entries with zero
+// entries from index 65536 (the kernels' padding sentinel):
 //   bits 0-4 len = 2n | bits 5-11/12-18/19-25 position*esz of non-zero 0..2 |
 //   bits 26-28 used | bits 29-31 code 2. Valid when max_nz <= 3.
-int derive_matvec_tables(const uint32_t* sparse_tab, uint32_t* mtab /* 2 * 65537 */);
+// Variant stride: 65540 entries so the second variant starts 16-byte aligned
+// (it is the source of a cp.async.bulk copy).
+constexpr int MT_STRIDE = 65540;
+int derive_matvec_tables(const uint32_t* sparse_tab, uint32_t* mtab /* 2 * MT_STRIDE */);
 
 }  // namespace qmoe

@@ -425,6 +425,9 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     U.cw = M.cw;
     U.row_off = M.row_off;
     U.row_minmax = M.row_minmax;
+    U.ck = M.ck;
+    U.lg = M.lg;
+    U.pad_ = 0;
     U.cols = M.cols;
     U.row0 = blk * rpu;
     U.row1 = min(rows, U.row0 + rpu);
@@ -451,6 +454,37 @@ __global__ void remap_kernel(const uint16_t* __restrict__ in, int64_t n, const u
     out[i] = __ldg(rank_of + in[i]);
 }
 
+// ================================================================ checkpoints
+// Row-segment checkpoints (include/qmoe.h qmoe_checkpoints): thread per row
+// walks the row's codewords once, summing entry lengths, and records the
+// column at each segment start s + (j*n >> lg).
+__global__ void checkpoints_kernel(const uint32_t* __restrict__ tab, const uint16_t* __restrict__ cw,
+                                   const int32_t* __restrict__ row_off, int64_t rows, int64_t cols, int lg,
+                                   uint16_t* ck, int32_t* bad) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int G = 1 << lg;
+  const int s = __ldg(row_off + r), e = __ldg(row_off + r + 1), n = e - s;
+  int j = 1, next = G > 1 ? s + ((1 * n) >> lg) : e;
+  int off = 0;
+  for (int k = s; k < e; ++k) {
+    while (j < G && k == next) {
+      ck[r * (G - 1) + j - 1] = (uint16_t)min(off, 65535);
+      ++j;
+      next = s + ((j * n) >> lg);
+    }
+    off += int(__ldg(tab + __ldg(cw + k)) & 31u);
+  }
+  while (j < G) {  // empty tail segments
+    ck[r * (G - 1) + j - 1] = (uint16_t)min(off, 65535);
+    ++j;
+  }
+  if (off != cols && bad) {
+    atomicAdd(bad, 1);
+    atomicMin(bad + 1, (int)r);
+  }
+}
+
 bool bad_dict(const qmoe_dict* d) { return d == nullptr || d->d_stab == nullptr; }
 
 }  // namespace
@@ -467,7 +501,7 @@ int qmoe_dict_create(const uint32_t* h_words, uint64_t hash64, int device, qmoe_
   int max_nz = 0;
   int rc = qmoe::derive_tables(h_words, stab.data(), len.data(), &max_nz);
   if (rc) return rc;
-  std::vector<uint32_t> mtab(2 * (size_t)(QMOE_DICT_SIZE + 1));
+  std::vector<uint32_t> mtab(2 * (size_t)qmoe::MT_STRIDE);
   qmoe::derive_matvec_tables(stab.data(), mtab.data());
   rc = qmoe::build_trie(h_words, next.data(), ent.data());
   if (rc) return rc;
@@ -633,16 +667,14 @@ int qmoe_codebook_table(qmoe_dict_t d, const uint16_t* h_order, uint32_t* d_tabl
   if (bad_dict(d) || !h_order || !d_table) return qmoe::fail(QMOE_EINVAL, "bad argument");
   if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
   std::vector<uint8_t> seen(QMOE_DICT_SIZE, 0);
-  const size_t V = QMOE_DICT_SIZE + 1;
-  std::vector<uint32_t> t(2 * V);
+  const size_t V = qmoe::MT_STRIDE;
+  std::vector<uint32_t> t(2 * V, 0u);
   for (int k = 0; k < QMOE_DICT_SIZE; ++k) {
     const uint16_t c = h_order[k];
     if (seen[c]++) return qmoe::fail(QMOE_EINVAL, "order is not a permutation of the 65536 codewords");
     t[k] = d->h_mtab[c];
     t[V + k] = d->h_mtab[V + c];
   }
-  t[V - 1] = 0;
-  t[2 * V - 1] = 0;
   CK(cudaMemcpy(d_table, t.data(), t.size() * 4, cudaMemcpyHostToDevice), "codebook upload");
   return QMOE_OK;
 }
@@ -652,6 +684,18 @@ int qmoe_remap(const uint16_t* d_in, int64_t n, const uint16_t* d_rank_of, uint1
   if (n == 0) return QMOE_OK;
   remap_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4736), 256, 0, S(stream)>>>(d_in, n, d_rank_of, d_out);
   CK(cudaGetLastError(), "remap_kernel");
+  return QMOE_OK;
+}
+
+int qmoe_checkpoints(qmoe_dict_t d, const uint32_t* d_table, const uint16_t* d_cw, const int32_t* d_row_off,
+                     int64_t rows, int64_t cols, int lg, uint16_t* d_ck, int32_t* d_bad, void* stream) {
+  if (bad_dict(d) || rows < 0 || cols < 0 || cols > 65535 || lg < 1 || lg > 3 || !d_ck)
+    return qmoe::fail(QMOE_EINVAL, "bad argument (1 <= lg <= 3, cols <= 65535)");
+  if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "checkpoints need a <=3-non-zero dictionary");
+  if (rows == 0) return QMOE_OK;
+  checkpoints_kernel<<<(int)((rows + 127) / 128), 128, 0, S(stream)>>>(d_table ? d_table : d->d_mtab, d_cw,
+                                                                        d_row_off, rows, cols, lg, d_ck, d_bad);
+  CK(cudaGetLastError(), "checkpoints_kernel");
   return QMOE_OK;
 }
 

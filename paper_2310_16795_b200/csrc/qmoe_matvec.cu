@@ -3,20 +3,26 @@
 // stream_matvec_kernel — the product path for dictionaries whose entries hold
 // <= 3 non-zero values (the default p0 = 0.885 dictionary). Persistent, one
 // CTA per SM, warp-specialised:
-//   * warp 0 = producer. Its 32 lanes hold the next 32 work records in
-//     registers (prefetched one batch ahead). Lane 0 stages, per work unit,
-//     the unit's codeword range, row offsets, row scales and (when the tokens
-//     change) the x rows into a STAGES-deep ring of shared-memory slots with
-//     cp.async.bulk, completing a `full` mbarrier; it reuses a slot once all
-//     consumer warps arrived on its `empty` mbarrier.
-//   * warps 1..16 = consumers. G lanes per row (G = 8/16/32 from the unit's
-//     mean codewords per row); each lane decodes K consecutive codewords:
-//     packed-entry lookup (hot prefix of the entry table in shared memory,
-//     the rest through the read-only path), one sub-warp scan of entry lengths
-//     for the column offsets, then <= 3 predicated non-zero slots per entry:
-//     acc += level(code) * x[col] in fp32, y = bf16_rne(sum) (codec.py:243).
+//   * warp 0 = producer. It keeps the work records of the next units in a
+//     shared-memory ring (refilled one 32-record batch ahead from registers)
+//     and lane 0 stages, per work unit, the unit's codeword range, row
+//     offsets, row scales, row checkpoints and (when the tokens change) the x
+//     rows into a STAGES-deep ring of shared-memory slots with cp.async.bulk,
+//     completing a `full` mbarrier; a slot is reused once all consumer warps
+//     arrived on its `empty` mbarrier.
+//   * warps 1..15 = consumers. A unit's rows are dealt out as tasks of
+//     32/G rows (shared-memory atomic dispenser). Within a task each lane owns
+//     one contiguous SEGMENT of one row (G = 2^lg segments per row; lg = 0:
+//     a lane per row) and walks it with a running column offset that starts
+//     at the row's checkpoint — no scans, no scratch. Codewords are looked up
+//     8 at a time, the next batch issued before the current one is applied
+//     (hot prefix of the packed entry table in shared memory, the rest through
+//     the read-only path). Per non-zero slot: S += x (every non-zero) and
+//     T += x (code-2 non-zeros); a row's result is lmin*S + (lmax-lmin)*T
+//     (= lmin*S1 + lmax*S2), reduced over its G lanes, bf16-rounded once
+//     (codec.py:243).
 //   * the entry table prefix is filled by one bulk copy at kernel start.
-// Entry format "matvec" (built in qmoe_kernels.cu, esz = bytes per staged x):
+// Entry format "matvec" (built in qmoe_host.cpp, esz = bytes per staged x):
 //   bits 0-4 len = 2n | bits 5-11, 12-18, 19-25: position * esz of non-zero
 //   slot 0..2 | bits 26-28 slot used | bits 29-31 slot is code 2 (row max).
 //
@@ -33,12 +39,13 @@ namespace {
 
 constexpr int NCONS = 15;                  // consumer warps (16 warps total: 4 per SMSP)
 constexpr int THREADS = (NCONS + 1) * 32;  // + one producer warp
-constexpr int STAGES = 3;
-constexpr int KS = 8;                      // codewords per lane per pass
-constexpr int CW_CAP = 4096;               // codewords per staged unit
-constexpr int ROW_CAP = 256;               // rows per staged unit
-constexpr uint32_t COLD_ZERO = 65536;      // global tables carry a zero entry here
+constexpr int STAGES = 8;
+constexpr int CW_CAP = 3072;               // codewords per staged unit
+constexpr int ROW_CAP = 128;               // rows per staged unit
+constexpr int BATCH = 8;                   // codewords looked up per batch per lane
+constexpr uint32_t COLD_ZERO = 65536;      // tables carry zero entries from here
 constexpr int NT_STREAM = 2;               // tokens per unit on the streaming path
+constexpr int RING = 64;                   // producer record ring
 
 // ----------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -67,75 +74,26 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ int lds_s32(uint32_t a) { return (int)lds32(a); }
-
-// codeword of slot (predicated; COLD_ZERO when past the end of the row)
-__device__ __forceinline__ uint32_t load_cw(uint32_t a, bool valid) {
-  uint32_t v;
-  asm volatile(
-      "{\n .reg .pred p;\n .reg .u16 h;\n setp.ne.u32 p, %2, 0;\n mov.u32 %0, %3;\n"
-      " @p ld.shared.u16 h, [%1];\n @p cvt.u32.u16 %0, h;\n}"
-      : "=r"(v)
-      : "r"(a), "r"((uint32_t)valid), "n"(COLD_ZERO)
-      : "memory");
-  return v;
-}
-
-// packed entry: hot prefix from shared memory, the rest (and the zero
-// sentinel at COLD_ZERO) through the non-coherent read-only path
-__device__ __forceinline__ uint32_t lookup(uint32_t c, uint32_t H, uint32_t tab_s, const uint32_t* gtab) {
-  uint32_t e;
-  asm volatile(
-      "{\n .reg .pred ph;\n .reg .u32 a;\n .reg .u64 g;\n"
-      " setp.lt.u32 ph, %1, %2;\n"
-      " mad.lo.u32 a, %1, 4, %3;\n"
-      " mad.wide.u32 g, %1, 4, %4;\n"
-      " @ph ld.shared.u32 %0, [a];\n"
-      " @!ph ld.global.nc.u32 %0, [g];\n}"
-      : "=r"(e)
-      : "r"(c), "r"(H), "r"(tab_s), "l"(gtab)
-      : "memory");
-  return e;
-}
-
-// one non-zero slot: if used, acc += level * x[xoff + field]
 template <int ESZ>
-__device__ __forceinline__ void slot(uint32_t e, int j, uint32_t xoff, float lmin, float lmax, float& acc) {
-  const uint32_t used = (e >> (26 + j)) & 1u;
-  const uint32_t field = (e >> (5 + 7 * j)) & 0x7Fu;
-  const float w = ((e >> (29 + j)) & 1u) ? lmax : lmin;
-  if (ESZ == 4) {
-    float v;
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n mov.f32 %0, 0f00000000;\n"
-        " @p ld.shared.f32 %0, [%1];\n}"
-        : "=f"(v)
-        : "r"(xoff + field), "r"(used)
-        : "memory");
-    acc = fmaf(w, v, acc);
-  } else {
-    uint32_t h;
-    asm volatile(
-        "{\n .reg .pred p;\n .reg .u16 s;\n setp.ne.u32 p, %2, 0;\n mov.u32 %0, 0;\n"
-        " @p ld.shared.u16 s, [%1];\n @p cvt.u32.u16 %0, s;\n}"
-        : "=r"(h)
-        : "r"(xoff + field), "r"(used)
-        : "memory");
-    acc = fmaf(w, __uint_as_float(h << 16), acc);
-  }
-}
+struct XType;
+template <>
+struct XType<4> {
+  using T = float;
+  static __device__ __forceinline__ float get(float v) { return v; }
+};
+template <>
+struct XType<2> {
+  using T = uint16_t;
+  static __device__ __forceinline__ float get(uint16_t v) { return __uint_as_float(uint32_t(v) << 16); }
+};
 
 // ----------------------------------------------------------------- records
-struct Rec {  // == qmoe_work (64 bytes)
+struct Rec {  // == qmoe_work (80 bytes)
   const uint16_t* cw;
   const int32_t* ro;
   const uint32_t* mm;
-  int32_t cols, row0, row1, ntok, cw0, cw1;
+  const uint16_t* ck;
+  int32_t cols, row0, row1, ntok, cw0, cw1, lg, pad;
   int32_t tok[QMOE_NT_MAX];
 };
 static_assert(sizeof(Rec) == sizeof(qmoe_work), "record layout");
@@ -143,18 +101,19 @@ static_assert(sizeof(Rec) == sizeof(qmoe_work), "record layout");
 // per-slot staging metadata written by the producer before the full arrive
 struct SlotMeta {
   Rec r;
-  uint32_t cw_s, ro_s, mm_s, x_s;  // shared addresses of the staged ranges
-  int32_t direct;                  // 1: unit exceeds the slot, read global
-  int32_t pad[3];
+  uint32_t cw_s, ro_s, mm_s, ck_s, x_s;  // byte offsets (from the smem base) of the staged ranges
+  int32_t direct;                        // 1: unit exceeds the slot, read global
+  int32_t next;                          // task dispenser (smem atomic)
+  int32_t pad;
 };
 
 struct StreamParams {
-  const uint32_t* gtab;       // matvec-format table, 65537 entries (zero sentinel last)
+  const uint32_t* gtab;       // matvec-format table variant (zero entries from 65536)
   int H;                      // entries staged in shared memory
   const qmoe_work* work;      // explicit work list (or nullptr: implicit single matrix)
   const int32_t* n_work;
   int max_work;
-  qmoe_matrix single;         // implicit mode
+  qmoe_matrix single;         // implicit mode (lane per row, no checkpoints)
   int rows_per_unit;
   int64_t ntok_single;
   int ntu_single;
@@ -173,14 +132,17 @@ __device__ __forceinline__ void make_rec(const StreamParams& P, int u, Rec& R) {
     const uint4* s = reinterpret_cast<const uint4*>(P.work + u);
     uint4* d = reinterpret_cast<uint4*>(&R);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) d[i] = __ldg(s + i);
+    for (int i = 0; i < 5; ++i) d[i] = __ldg(s + i);
   } else {
     const int nblk = (P.single.rows + P.rows_per_unit - 1) / P.rows_per_unit;
     const int chunk = u / nblk, blk = u % nblk;
     R.cw = P.single.cw;
     R.ro = P.single.row_off;
     R.mm = P.single.row_minmax;
+    R.ck = nullptr;
     R.cols = P.single.cols;
+    R.lg = 0;
+    R.pad = 0;
     R.row0 = blk * P.rows_per_unit;
     R.row1 = min(P.single.rows, R.row0 + P.rows_per_unit);
     const int64_t t0 = (int64_t)chunk * P.ntu_single;
@@ -190,15 +152,6 @@ __device__ __forceinline__ void make_rec(const StreamParams& P, int u, Rec& R) {
     R.cw0 = __ldg(R.ro + R.row0);
     R.cw1 = __ldg(R.ro + R.row1);
   }
-}
-
-__device__ __forceinline__ Rec shfl_rec(const Rec& R, int src) {
-  Rec o;
-  const int* a = reinterpret_cast<const int*>(&R);
-  int* b = reinterpret_cast<int*>(&o);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) b[i] = __shfl_sync(FULL_MASK, a[i], src);
-  return o;
 }
 
 __device__ __forceinline__ bool same_x(const Rec& a, const Rec& b) {
@@ -216,109 +169,130 @@ __device__ __forceinline__ uint32_t span(const void* begin, size_t nbytes, uint3
 }
 
 // ----------------------------------------------------------------- consumer
-// G lanes share one row; lane `gl` owns codewords [gl*K, gl*K + K) of this pass.
-template <int K, int NT, int ESZ>
-__device__ __noinline__ void seg(uint32_t cw_a, int cnt, int gl, int G, uint32_t tab_s, uint32_t H,
-                                   const uint32_t* gtab, uint32_t xbase, uint32_t xslot, int& base, float lmin,
-                                   float lmax, float (&acc)[NT]) {
-  const int my0 = gl * K;
-  uint32_t t[K];
-  int sum = 0;
+// Look up BATCH codewords of this lane's segment starting at k0 (past the
+// segment's end: the zero entry at COLD_ZERO).
+__device__ __forceinline__ void lookup_batch(uint32_t (&t)[BATCH], const uint16_t* cw, int cnt, int k0,
+                                             const uint32_t* tab, uint32_t H, const uint32_t* __restrict__ gtab) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const uint32_t c = load_cw(cw_a + 2u * (my0 + k), my0 + k < cnt);
-    t[k] = lookup(c, H, tab_s, gtab);
-    sum += int(t[k] & 31u);
+  for (int u = 0; u < BATCH; ++u) {
+    const uint32_t c = (k0 + u < cnt) ? (uint32_t)cw[k0 + u] : COLD_ZERO;
+    t[u] = c < H ? tab[c] : __ldg(gtab + c);
   }
-  int incl = sum;
+}
+
+// Apply BATCH entries at the running column `off` (elements).
+template <int NT, int ESZ>
+__device__ __forceinline__ void apply_batch(const uint32_t (&t)[BATCH], const typename XType<ESZ>::T* xs, int xslot,
+                                            int& off, float (&S)[NT], float (&T)[NT]) {
+  using XT = typename XType<ESZ>::T;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    if (d >= G) break;
-    const int v = __shfl_up_sync(FULL_MASK, incl, d, G);
-    if (gl >= d) incl += v;
-  }
-  uint32_t xoff = xbase + (uint32_t)(base + incl - sum) * ESZ;
-  base += __shfl_sync(FULL_MASK, incl, G - 1, G);
+  for (int u = 0; u < BATCH; ++u) {
+    const uint32_t e = t[u];
+    const char* xo = reinterpret_cast<const char*>(xs + off);
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const uint32_t e = t[k];
+    for (int j = 0; j < 3; ++j) {
+      const bool used = (e >> (26 + j)) & 1u;
+      const bool two = (e >> (29 + j)) & 1u;
+      const XT* xp = reinterpret_cast<const XT*>(xo + ((e >> (5 + 7 * j)) & 0x7Fu));
 #pragma unroll
-    for (int q = 0; q < NT; ++q) {
-      slot<ESZ>(e, 0, xoff + q * xslot, lmin, lmax, acc[q]);
-      slot<ESZ>(e, 1, xoff + q * xslot, lmin, lmax, acc[q]);
-      slot<ESZ>(e, 2, xoff + q * xslot, lmin, lmax, acc[q]);
+      for (int q = 0; q < NT; ++q) {
+        const float v = used ? XType<ESZ>::get(xp[q * xslot]) : 0.f;
+        S[q] += v;
+        T[q] += two ? v : 0.f;
+      }
     }
-    xoff += (e & 31u) * ESZ;
+    off += int(e & 31u);
   }
 }
 
 template <int NT, int ESZ>
-__device__ __forceinline__ void run_unit(const StreamParams& P, const SlotMeta& M, uint32_t tab_s, int cwarp,
-                                         int u) {
-  const Rec& R = M.r;
+__device__ __forceinline__ void run_unit(const StreamParams& P, SlotMeta& M, const uint8_t* smem) {
+  using XT = typename XType<ESZ>::T;
   const int lane = threadIdx.x & 31;
-  const int nrows = R.row1 - R.row0;
-  const int avg = nrows > 0 ? (R.cw1 - R.cw0) / nrows : 0;
-  const int G = avg <= 48 ? 8 : (avg <= 96 ? 16 : 32);
-  const int RG = 32 / G;
-  const int g = lane / G, gl = lane % G;
-  const int ngroups = (nrows + RG - 1) / RG;
-  const uint32_t xslot = (uint32_t)P.xcap * ESZ;
-  // rotate the group -> warp assignment per unit so imbalance averages out
-  int gi0 = cwarp - (u % NCONS);
-  if (gi0 < 0) gi0 += NCONS;
-  for (int gi = gi0; gi < ngroups; gi += NCONS) {
-    const int i = gi * RG + g;
+  // everything the task loop needs, read once
+  const int row0 = M.r.row0, nrows = M.r.row1 - M.r.row0, cw0 = M.r.cw0, cols = M.r.cols, ntok = M.r.ntok;
+  const int lg = M.r.lg;
+  int tok[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) tok[q] = M.r.tok[q];
+  const uint16_t* cwp = reinterpret_cast<const uint16_t*>(smem + M.cw_s);
+  const int32_t* rop = reinterpret_cast<const int32_t*>(smem + M.ro_s);
+  const uint32_t* mmp = reinterpret_cast<const uint32_t*>(smem + M.mm_s);
+  const uint16_t* ckp = reinterpret_cast<const uint16_t*>(smem + M.ck_s);
+  const XT* xs = reinterpret_cast<const XT*>(smem + M.x_s);
+  const uint32_t* tab = reinterpret_cast<const uint32_t*>(smem);
+  int32_t* next = &M.next;
+  const int G = 1 << lg;
+  const int rg = lane >> lg, seg = lane & (G - 1);
+  const int ntasks = (nrows + (32 >> lg) - 1) >> (5 - lg);
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t* gtab = P.gtab;
+  const int xslot = P.xcap;
+  for (;;) {
+    int task = 0;
+    if (lane == 0) task = atomicAdd(next, 1);
+    task = __shfl_sync(FULL_MASK, task, 0);
+    if (task >= ntasks) break;
+    const int i = (task << (5 - lg)) + rg;
     const bool valid = i < nrows;
-    int s = 0, n = 0;
+    int b = 0, cnt = 0, off = 0;
     uint32_t mm = 0;
     if (valid) {
-      s = lds_s32(M.ro_s + 4u * i) - R.cw0;
-      n = lds_s32(M.ro_s + 4u * (i + 1)) - R.cw0 - s;
-      mm = lds32(M.mm_s + 4u * i);
+      const int s = rop[i] - cw0;
+      const int n = rop[i + 1] - rop[i];
+      b = s + ((seg * n) >> lg);
+      cnt = s + (((seg + 1) * n) >> lg) - b;
+      off = seg ? (int)ckp[i * (G - 1) + seg - 1] : 0;
+      mm = mmp[i];
     }
-    const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
-    const int maxn = __reduce_max_sync(FULL_MASK, n);
-    float acc[NT];
+    const int maxc = __reduce_max_sync(FULL_MASK, cnt);
+    float S[NT], T[NT];
 #pragma unroll
-    for (int q = 0; q < NT; ++q) acc[q] = 0.f;
-    int base = 0;
-    for (int p = 0; p < maxn; p += G * KS) {
-      const int K = (min(maxn - p, G * KS) + G - 1) / G;
-      const uint32_t cw_a = M.cw_s + 2u * (uint32_t)(s + p);
-      const int cnt = n - p;
-      switch (K) {
-#define QMOE_K(KK) \
-  case KK: seg<KK, NT, ESZ>(cw_a, cnt, gl, G, tab_s, (uint32_t)P.H, P.gtab, M.x_s, xslot, base, lmin, lmax, acc); break;
-        QMOE_K(1) QMOE_K(2) QMOE_K(3) QMOE_K(4) QMOE_K(5) QMOE_K(6) QMOE_K(7) QMOE_K(8)
-#undef QMOE_K
-        default: break;
-      }
+    for (int q = 0; q < NT; ++q) S[q] = T[q] = 0.f;
+    const uint16_t* c = cwp + b;
+    uint32_t ta[BATCH], tb[BATCH];
+    lookup_batch(ta, c, cnt, 0, tab, H, gtab);
+    for (int k0 = 0;;) {
+      if (k0 + BATCH < maxc) lookup_batch(tb, c, cnt, k0 + BATCH, tab, H, gtab);
+      apply_batch<NT, ESZ>(ta, xs, xslot, off, S, T);
+      k0 += BATCH;
+      if (k0 >= maxc) break;
+      if (k0 + BATCH < maxc) lookup_batch(ta, c, cnt, k0 + BATCH, tab, H, gtab);
+      apply_batch<NT, ESZ>(tb, xs, xslot, off, S, T);
+      k0 += BATCH;
+      if (k0 >= maxc) break;
     }
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
 #pragma unroll
-      for (int d = 16; d >= 1; d >>= 1)
-        if (d < G) acc[q] += __shfl_xor_sync(FULL_MASK, acc[q], d);
+      for (int d = 1; d < 32; d <<= 1)
+        if (d < G) {
+          S[q] += __shfl_xor_sync(FULL_MASK, S[q], d);
+          T[q] += __shfl_xor_sync(FULL_MASK, T[q], d);
+        }
     }
-    if (!valid || gl != 0) continue;
-    const int r = R.row0 + i;
-    if (base != R.cols) {  // row decodes to the wrong number of values: never written
+    if (!valid || seg != G - 1) continue;  // the last segment's lane ends the row
+    const int r = row0 + i;
+    if (off != cols) {  // row decodes to the wrong number of values: never written
       if (P.bad) {
         atomicAdd(P.bad, 1);
         atomicMin(P.bad + 1, r);
       }
       continue;
     }
+    const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
+    const float dl = lmax - lmin;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      if (q >= R.ntok) break;
-      const float v = bf16_round_dev(acc[q]);
+      if (q >= ntok) break;
+      const float v = bf16_round_dev(fmaf(lmin, S[q], dl * T[q]));
       if (P.y_mode == QMOE_Y_RELU_BF16) {
-        uint16_t* yp = reinterpret_cast<uint16_t*>(P.y) + (int64_t)R.tok[q] * P.ldy + r;
+        uint16_t* yp = reinterpret_cast<uint16_t*>(P.y) + (int64_t)tok[q] * P.ldy + r;
         *yp = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+      } else if (P.y_mode == QMOE_Y_STORE_F32) {
+        reinterpret_cast<float*>(P.y)[(int64_t)tok[q] * P.ldy + r] = v + 0.f;  // == 0 + v
       } else {
-        float* yp = reinterpret_cast<float*>(P.y) + (int64_t)R.tok[q] * P.ldy + r;
+        float* yp = reinterpret_cast<float*>(P.y) + (int64_t)tok[q] * P.ldy + r;
         *yp = *yp + v;
       }
     }
@@ -335,7 +309,7 @@ __device__ void run_unit_direct(const StreamParams& P, const SlotMeta& M, int cw
     const int s = __ldg(R.ro + r), e = __ldg(R.ro + r + 1);
     const uint32_t mm = __ldg(R.mm + r);
     const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
-    float acc[QMOE_NT_MAX] = {0.f, 0.f, 0.f, 0.f};
+    float acc0 = 0.f, acc1 = 0.f;
     int base = 0;
     for (int p0 = s; p0 < e; p0 += 32) {
       const uint32_t c = p0 + lane < e ? (uint32_t)__ldg(R.cw + p0 + lane) : COLD_ZERO;
@@ -352,15 +326,17 @@ __device__ void run_unit_direct(const StreamParams& P, const SlotMeta& M, int cw
         if (!((t >> (26 + j)) & 1u)) continue;
         const int col = off + int(((t >> (5 + 7 * j)) & 0x7Fu) / ESZ);
         const float w = ((t >> (29 + j)) & 1u) ? lmax : lmin;
-        for (int q = 0; q < R.ntok; ++q) {
+        for (int q = 0; q < R.ntok && q < 2; ++q) {
           const int64_t xi = (int64_t)R.tok[q] * P.ldx + col;
           const float xv = ESZ == 2 ? __uint_as_float(uint32_t(__ldg(reinterpret_cast<const uint16_t*>(P.x) + xi)) << 16)
                                     : __ldg(reinterpret_cast<const float*>(P.x) + xi);
-          acc[q] = fmaf(w, xv, acc[q]);
+          if (q == 0) acc0 = fmaf(w, xv, acc0);
+          else acc1 = fmaf(w, xv, acc1);
         }
       }
     }
-    for (int q = 0; q < QMOE_NT_MAX; ++q) acc[q] = warp_sum(acc[q]);
+    acc0 = warp_sum(acc0);
+    acc1 = warp_sum(acc1);
     if (lane != 0) continue;
     if (base != R.cols) {
       if (P.bad) {
@@ -369,10 +345,12 @@ __device__ void run_unit_direct(const StreamParams& P, const SlotMeta& M, int cw
       }
       continue;
     }
-    for (int q = 0; q < R.ntok; ++q) {
-      const float v = bf16_round_dev(acc[q]);
+    for (int q = 0; q < R.ntok && q < 2; ++q) {
+      const float v = bf16_round_dev(q == 0 ? acc0 : acc1);
       if (P.y_mode == QMOE_Y_RELU_BF16)
         reinterpret_cast<uint16_t*>(P.y)[(int64_t)R.tok[q] * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+      else if (P.y_mode == QMOE_Y_STORE_F32)
+        reinterpret_cast<float*>(P.y)[(int64_t)R.tok[q] * P.ldy + r] = v + 0.f;
       else {
         float* yp = reinterpret_cast<float*>(P.y) + (int64_t)R.tok[q] * P.ldy + r;
         *yp = *yp + v;
@@ -382,15 +360,14 @@ __device__ void run_unit_direct(const StreamParams& P, const SlotMeta& M, int cw
 }
 
 struct Carve {
-  uint32_t tab_s, bar_full, bar_empty, bar_tab, cwbuf, robuf, mmbuf, xbuf, xbytes;
+  uint32_t tab_s, bar_full, bar_empty, bar_tab, cwbuf, robuf, mmbuf, ckbuf, xbuf, xbytes;
   SlotMeta* meta;
   Rec* ring;  // producer's record ring [RING]
 };
-constexpr int RING = 64;
 
-// Producer warp: keeps the work records of the next 32 units in flight in
-// registers, the current 64 in a shared-memory ring, and stages one unit per
-// iteration into the ring of STAGES slots (lane 0 issues the bulk copies).
+// Producer warp: keeps the records of the next 32 units in flight in
+// registers, the current ones in a shared-memory ring, and stages one unit
+// per iteration into the ring of STAGES slots (lane 0 issues the bulk copies).
 template <int ESZ>
 __device__ __noinline__ void producer(const StreamParams& P, const Carve& C, int u0, int u1) {
   const int lane = threadIdx.x & 31;
@@ -407,8 +384,8 @@ __device__ __noinline__ void producer(const StreamParams& P, const Carve& C, int
   if (u0 + RING + lane < u1) make_rec(P, u0 + RING + lane, nxt);
   __syncwarp();
   int cur_xb = 1;
-  int last_x_unit[2] = {-1, -1};
-  int consumed = -1;  // highest relative unit known consumed
+  int last_x0 = -1, last_x1 = -1;  // last unit that used x buffer 0 / 1
+  int consumed = -1;               // highest relative unit known consumed
   for (int u = u0; u < u1; ++u) {
     const int rel = u - u0;
     if (lane == 0) {
@@ -423,56 +400,62 @@ __device__ __noinline__ void producer(const StreamParams& P, const Carve& C, int
       SlotMeta& M = C.meta[s];
       const int nrows = R.row1 - R.row0;
       const int ncw = R.cw1 - R.cw0;
+      const int nck = (1 << R.lg) - 1;
       M.r = R;
-      M.direct = (ncw > CW_CAP || nrows > ROW_CAP) ? 1 : 0;
+      M.direct = (ncw > CW_CAP || nrows > ROW_CAP || nck > 7) ? 1 : 0;
+      M.next = 0;
       const bool reuse = rel > 0 && same_x(C.ring[(rel - 1) % RING], R);
       int xb = cur_xb;
       if (!reuse) {
         xb = cur_xb ^ 1;
-        const int v = last_x_unit[xb];
+        const int v = xb ? last_x1 : last_x0;
         while (v >= 0 && consumed < v) {
           ++consumed;
           mbar_wait(C.bar_empty + 8 * (consumed % STAGES), (uint32_t)((consumed / STAGES) & 1));
         }
       }
-      last_x_unit[xb] = rel;
+      if (xb) last_x1 = rel;
+      else last_x0 = rel;
       cur_xb = xb;
-      M.x_s = C.xbuf + (uint32_t)xb * C.xbytes;
+      M.x_s = C.xbuf + (uint32_t)xb * C.xbytes - C.tab_s;
       const uint32_t full = C.bar_full + 8 * s;
       const uint32_t cw_dst = C.cwbuf + s * (CW_CAP * 2 + 64);
       const uint32_t ro_dst = C.robuf + s * (ROW_CAP * 4 + 64);
       const uint32_t mm_dst = C.mmbuf + s * (ROW_CAP * 4 + 64);
-      uintptr_t acw = 0, aro = 0, amm = 0;
-      uint32_t bcw = 0, bro = 0, bmm = 0, dcw = 0, dro = 0, dmm = 0, total = 0;
+      const uint32_t ck_dst = C.ckbuf + s * (ROW_CAP * 2 * 7 + 64);
+      uintptr_t acw = 0, aro = 0, amm = 0, ack = 0;
+      uint32_t bcw = 0, bro = 0, bmm = 0, bck = 0, dcw = 0, dro = 0, dmm = 0, dck = 0, total = 0;
       if (!M.direct) {
         bcw = span(R.cw + R.cw0, (size_t)ncw * 2, dcw, acw);
         bro = span(R.ro + R.row0, (size_t)(nrows + 1) * 4, dro, aro);
         bmm = span(R.mm + R.row0, (size_t)nrows * 4, dmm, amm);
-        total = bcw + bro + bmm;
+        if (nck) bck = span(R.ck + (size_t)R.row0 * nck, (size_t)nrows * nck * 2, dck, ack);
+        total = bcw + bro + bmm + bck;
       }
       const size_t xrow = (size_t)R.cols * ESZ;
       const uint32_t xrow16 = (uint32_t)((xrow + 15) & ~size_t(15));  // x rows are 16-byte aligned
       if (!reuse) total += xrow16 * (uint32_t)R.ntok;
-      M.cw_s = cw_dst + dcw;
-      M.ro_s = ro_dst + dro;
-      M.mm_s = mm_dst + dmm;
+      M.cw_s = cw_dst + dcw - C.tab_s;
+      M.ro_s = ro_dst + dro - C.tab_s;
+      M.mm_s = mm_dst + dmm - C.tab_s;
+      M.ck_s = ck_dst + dck - C.tab_s;
       fence_proxy_async();
       mbar_arrive_expect_tx(full, total);  // releases M.* to the consumers
       if (bcw) bulk_g2s(cw_dst, reinterpret_cast<const void*>(acw), bcw, full);
       if (bro) bulk_g2s(ro_dst, reinterpret_cast<const void*>(aro), bro, full);
       if (bmm) bulk_g2s(mm_dst, reinterpret_cast<const void*>(amm), bmm, full);
+      if (bck) bulk_g2s(ck_dst, reinterpret_cast<const void*>(ack), bck, full);
       if (!reuse) {
         for (int q = 0; q < R.ntok; ++q)
-          bulk_g2s(M.x_s + (uint32_t)q * P.xcap * ESZ,
+          bulk_g2s(C.tab_s + M.x_s + (uint32_t)q * P.xcap * ESZ,
                    reinterpret_cast<const uint8_t*>(P.x) + (int64_t)R.tok[q] * P.ldx * ESZ, xrow16, full);
       }
     }
-    // refill: after the last unit of a 32-batch, park the prefetched records
-    // (units rel+33 .. rel+64 relative... i.e. the batch two ahead) in the
-    // half of the ring that just drained, and prefetch the next batch
+    // after the last unit of a 32-batch: park the prefetched records in the
+    // ring half that just drained and prefetch the next batch
     if ((rel & 31) == 31) {
       __syncwarp();
-      const int v = u + 1 + (RING - 32) + lane;  // units [u+33, u+65) relative to the ring's next half
+      const int v = u + 1 + (RING - 32) + lane;
       if (v < u1) C.ring[(v - u0) % RING] = nxt;
       __syncwarp();
       if (v + 32 < u1) make_rec(P, v + 32, nxt);
@@ -501,6 +484,8 @@ __global__ void __launch_bounds__(THREADS, 1) stream_matvec_kernel(StreamParams 
   p += STAGES * (ROW_CAP * 4 + 64);
   C.mmbuf = saddr(p);
   p += STAGES * (ROW_CAP * 4 + 64);
+  C.ckbuf = saddr(p);
+  p += STAGES * (ROW_CAP * 2 * 7 + 64);
   C.xbuf = saddr(p);  // [2][ntmax][xcap]
   C.xbytes = (uint32_t)P.ntmax * P.xcap * ESZ;
 
@@ -534,10 +519,10 @@ __global__ void __launch_bounds__(THREADS, 1) stream_matvec_kernel(StreamParams 
       const int rel = u - u0;
       const int s = rel % STAGES;
       mbar_wait(C.bar_full + 8 * s, (uint32_t)((rel / STAGES) & 1));
-      const SlotMeta& M = C.meta[s];
+      SlotMeta& M = C.meta[s];
       if (M.direct) run_unit_direct<ESZ>(P, M, cwarp);
-      else if (M.r.ntok == 1) run_unit<1, ESZ>(P, M, C.tab_s, cwarp, u);
-      else run_unit<2, ESZ>(P, M, C.tab_s, cwarp, u);
+      else if (M.r.ntok == 1) run_unit<1, ESZ>(P, M, smem);
+      else run_unit<2, ESZ>(P, M, smem);
       __syncwarp();
       if (lane == 0) mbar_arrive(C.bar_empty + 8 * s);
     }
@@ -636,6 +621,8 @@ __global__ void __launch_bounds__(256) general_matvec_kernel(GeneralParams P) {
         const float v = bf16_round_dev(acc[q]);
         if (P.y_mode == QMOE_Y_RELU_BF16) {
           reinterpret_cast<uint16_t*>(P.y)[(int64_t)tok[q] * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+        } else if (P.y_mode == QMOE_Y_STORE_F32) {
+          reinterpret_cast<float*>(P.y)[(int64_t)tok[q] * P.ldy + r] = v + 0.f;
         } else {
           float* yp = reinterpret_cast<float*>(P.y) + (int64_t)tok[q] * P.ldy + r;
           *yp = *yp + v;
@@ -647,8 +634,8 @@ __global__ void __launch_bounds__(256) general_matvec_kernel(GeneralParams P) {
 
 // ----------------------------------------------------------------- host side
 size_t fixed_smem() {
-  return 128 + ((sizeof(SlotMeta) * STAGES + 127) / 128) * 128 + sizeof(Rec) * RING + STAGES * (CW_CAP * 2 + 64) +
-         2 * STAGES * (ROW_CAP * 4 + 64);
+  return 128 + ((sizeof(SlotMeta) * STAGES + 127) / 128) * 128 + sizeof(Rec) * RING +
+         STAGES * (CW_CAP * 2 + 64) + 2 * STAGES * (ROW_CAP * 4 + 64) + STAGES * (ROW_CAP * 2 * 7 + 64);
 }
 
 int hot_override() {
@@ -688,9 +675,9 @@ int launch_stream(const qmoe_dict* d, StreamParams& P, int esz, int max_cols, in
 }
 
 const uint32_t* pick_table(const qmoe_dict* d, const uint32_t* user, int esz) {
-  // codebooks hold both variants back to back: [esz 4 | esz 2], 65537 entries each
-  if (user) return esz == 4 ? user : user + (QMOE_DICT_SIZE + 1);
-  return esz == 4 ? d->d_mtab : d->d_mtab + (QMOE_DICT_SIZE + 1);
+  // tables hold both variants back to back: [esz 4 | esz 2], MT_STRIDE entries each
+  if (user) return esz == 4 ? user : user + qmoe::MT_STRIDE;
+  return esz == 4 ? d->d_mtab : d->d_mtab + qmoe::MT_STRIDE;
 }
 
 }  // namespace
@@ -717,7 +704,7 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
     StreamParams P{};
     P.gtab = pick_table(d, nullptr, esz);
     P.work = nullptr;
-    P.single = qmoe_matrix{d_cw, d_row_off, d_mm, (int32_t)rows, (int32_t)cols, 0, 0};
+    P.single = qmoe_matrix{d_cw, d_row_off, d_mm, nullptr, (int32_t)rows, (int32_t)cols, 0, 0};
     P.rows_per_unit = rpu;
     P.ntok_single = ntok;
     P.ntu_single = ntu;
@@ -737,7 +724,7 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
   }
   GeneralParams G{};
   G.words = d->d_words;
-  G.single = qmoe_matrix{d_cw, d_row_off, d_mm, (int32_t)rows, (int32_t)cols, 0, 0};
+  G.single = qmoe_matrix{d_cw, d_row_off, d_mm, nullptr, (int32_t)rows, (int32_t)cols, 0, 0};
   G.ntok_single = ntok;
   G.x = d_x;
   G.x_bf16 = x_dtype == QMOE_X_BF16;
@@ -770,7 +757,7 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
                         int64_t ldx, void* d_y, int y_mode, int64_t ldy, int32_t* d_bad, void* stream) {
   if (!d || !d->d_stab || !d_work || !d_n_work || max_work < 0 || max_cols <= 0 || max_ntok < 1 ||
       max_ntok > QMOE_NT_MAX || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16) ||
-      (y_mode != QMOE_Y_ACCUM_F32 && y_mode != QMOE_Y_RELU_BF16))
+      (y_mode != QMOE_Y_ACCUM_F32 && y_mode != QMOE_Y_RELU_BF16 && y_mode != QMOE_Y_STORE_F32))
     return qmoe::fail(QMOE_EINVAL, "bad argument");
   const int esz = x_dtype == QMOE_X_BF16 ? 2 : 4;
   if (!aligned16(d_x) || (ldx * esz) % 16) return qmoe::fail(QMOE_EINVAL, "x rows must be 16-byte aligned");

@@ -33,7 +33,7 @@ def _rows_per_unit(mats, target_cw: int = 4096) -> int:
     rows = sum(m.rows for m in mats)
     per_row = max(1.0, cw / max(1, rows))
     r = int(target_cw / per_row)
-    r = max(8, min(r, mats[0].rows, 512))
+    r = max(4, min(r, mats[0].rows, 128))
     return r
 
 
@@ -42,7 +42,7 @@ class CompressedMoELayer:
     all DeviceMatrix on one device."""
 
     def __init__(self, wi: list[DeviceMatrix], wo: list[DeviceMatrix], dic: Dictionary, max_tokens: int = 64,
-                 target_cw_per_unit: int = 3072, tokens_per_unit: int = 2, codebook: bool = True):
+                 target_cw_per_unit: int = 2048, tokens_per_unit: int = 2, codebook: bool = True):
         import torch
 
         if len(wi) != len(wo) or not wi:
@@ -68,6 +68,9 @@ class CompressedMoELayer:
                 self.codebook.apply(mats)
             elif len({id(m.codebook) for m in mats}) == 1:
                 self.codebook = mats[0].codebook
+        for m in list(wi) + list(wo):  # row-segment checkpoints (kernel-private)
+            if m.ck is None and m.lg == 0:
+                m.build_checkpoints(dic)
         descs = (_lib.QmoeMatrix * (2 * self.E))()
         for e in range(self.E):
             descs[2 * e] = _lib.QmoeMatrix(*wi[e].descriptor())
@@ -127,7 +130,7 @@ class CompressedMoELayer:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
             self.handle, self._table(), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 4, self.max_units,
             self.d_ff, self.tokens_per_unit, _lib.ptr(self.h), _lib.QMOE_X_BF16, self.h.stride(0), _lib.ptr(out),
-            _lib.QMOE_Y_ACCUM_F32, out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
+            _lib.QMOE_Y_STORE_F32, out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def forward_device(self, x, assign, out=None, stream=None):
         """x: (T, d_model) CUDA bf16/f32, assign: (T,) CUDA int32 expert ids.
@@ -148,7 +151,6 @@ class CompressedMoELayer:
             x = buf
         self.plan(assign, stream)
         self.pass_wi(x, stream)
-        out.zero_()
         self.pass_wo(out, stream)
         return out
 

@@ -120,3 +120,31 @@ def test_codebook_reindexing_is_exact(dic):
         out, bad = decompress_device(m, dic)
         assert int(bad[0]) == 0
         assert torch.equal(out, codes)
+
+
+@pytest.mark.parametrize("d_model,d_ff", [(256, 2048), (512, 8192)])
+def test_moe_segmented_rows_vs_oracle(dic, odic, d_model, d_ff):
+    """Long rows use G = 2^lg lanes per row with precomputed column
+    checkpoints (lg = 1..3); outputs must still match the composed oracle."""
+    rng = np.random.default_rng(d_ff)
+    E = 3
+    wi, wo, host = [], [], []
+    for e in range(E):
+        pair = []
+        for rows, cols, lst in ((d_ff, d_model, wi), (d_model, d_ff, wo)):
+            w = (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+            t = q.rtn_quantize(w, q.make_grid(w))
+            c = q.encode(t, dic)
+            dm = q.DeviceMatrix.from_host(c, dic, torch.device("cuda", 0))
+            lst.append(dm)
+            pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
+        host.append(tuple(pair))
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=8)
+    assert max(m.lg for m in wo) >= 1
+    x = q.bf16_round(rng.normal(size=(7, d_model)).astype(np.float32))
+    assign = np.array([0, 1, 2, 0, 0, 2, 1], np.int32)
+    y = layer.forward(x, assign)
+    y_ref = O.moe_layer(x, assign, host, odic)
+    d = bf16_ulp_diff(y, y_ref)
+    assert d.max() <= 2
+    assert np.mean(d == 0) >= 0.99
