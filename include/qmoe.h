@@ -54,9 +54,9 @@ enum { QMOE_X_F32 = 0, QMOE_X_BF16 = 1 };
 typedef struct qmoe_dict* qmoe_dict_t;
 
 /* One compressed matrix resident on the device (grouped launches). */
-/* The arrays must start 16-byte aligned and be readable up to the next
- * 16-byte boundary past their end (they are streamed into shared memory with
- * cp.async.bulk); n_cw = row_off[rows].
+/* The arrays must start 16-byte aligned and be readable 32 bytes past their
+ * end (row metadata is streamed into shared memory with cp.async.bulk and
+ * codewords are read in sector-aligned 32-byte groups); n_cw = row_off[rows].
  * ck / lg: optional row-segment checkpoints (qmoe_checkpoints): with G = 2^lg
  * lanes per row, ck[r * (G-1) + j - 1] is the column at which segment j of row
  * r starts (segment j = codewords [s + j*n/G, s + (j+1)*n/G) of the row's n).

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libqmoe.so")
+LIB_PATH = os.environ.get("QMOE_LIB_PATH") or os.path.join(_HERE, "_lib", "libqmoe.so")  # override: experiments
 
 QMOE_OK, QMOE_EINVAL, QMOE_ECORRUPT, QMOE_ECUDA, QMOE_EUNSUPPORTED = 0, 1, 2, 3, 4
 QMOE_X_F32, QMOE_X_BF16 = 0, 1
@@ -124,12 +124,12 @@ def ptr(a) -> int:
 
 def padded_empty(n: int, dtype, device):
     """Device buffer of n elements whose storage is 16-byte aligned and
-    readable up to the next 16-byte boundary past element n (the contract of
-    the bulk-copy staging in libqmoe)."""
+    readable at least 32 bytes past element n (the contract of the bulk-copy
+    staging and the 32-byte codeword group loads in libqmoe)."""
     import torch
 
     esz = torch.empty((), dtype=dtype).element_size()
-    pad = (16 + 15) // esz + 1
+    pad = (64 + esz - 1) // esz  # the streaming kernel reads whole 32-byte groups
     return torch.empty(n + pad, dtype=dtype, device=device)[:n]
 
 

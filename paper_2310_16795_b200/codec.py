@@ -138,7 +138,7 @@ class DeviceMatrix:
         torch = _torch()
         if lg is None:
             avg = self.mean_codewords_per_row()
-            lg = 0 if avg <= 48 else (1 if avg <= 96 else (2 if avg <= 192 else 3))
+            lg = 0 if avg <= 48 else (1 if avg <= 96 else 2)  # G <= 4 (MAX_CK = 3 on the fast path)
         self.lg = int(lg)
         if self.lg == 0 or self.rows == 0:
             self.ck = None

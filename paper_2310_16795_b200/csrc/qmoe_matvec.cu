@@ -1,28 +1,24 @@
 // Fused dictionary-decode + matvec (codec.py:196-244 semantics) for sm_100a.
 //
-// stream_matvec_kernel — the product path for dictionaries whose entries hold
-// <= 3 non-zero values (the default p0 = 0.885 dictionary). Persistent, one
-// CTA per SM, warp-specialised:
-//   * warp 0 = producer. It keeps the work records of the next units in a
-//     shared-memory ring (refilled one 32-record batch ahead from registers)
-//     and lane 0 stages, per work unit, the unit's codeword range, row
-//     offsets, row scales, row checkpoints and (when the tokens change) the x
-//     rows into a STAGES-deep ring of shared-memory slots with cp.async.bulk,
-//     completing a `full` mbarrier; a slot is reused once all consumer warps
-//     arrived on its `empty` mbarrier.
-//   * warps 1..15 = consumers. A unit's rows are dealt out as tasks of
-//     32/G rows (shared-memory atomic dispenser). Within a task each lane owns
-//     one contiguous SEGMENT of one row (G = 2^lg segments per row; lg = 0:
-//     a lane per row) and walks it with a running column offset that starts
-//     at the row's checkpoint — no scans, no scratch. Codewords are looked up
-//     8 at a time, the next batch issued before the current one is applied
-//     (hot prefix of the packed entry table in shared memory, the rest through
-//     the read-only path). Per non-zero slot: S += x (every non-zero) and
-//     T += x (code-2 non-zeros); a row's result is lmin*S + (lmax-lmin)*T
-//     (= lmin*S1 + lmax*S2), reduced over its G lanes, bf16-rounded once
-//     (codec.py:243).
-//   * the entry table prefix is filled by one bulk copy at kernel start.
-// Entry format "matvec" (built in qmoe_host.cpp, esz = bytes per staged x):
+// lean_matvec_kernel — the product path for dictionaries whose entries hold
+// <= 3 non-zero values (the default p0 = 0.885 dictionary):
+//   * persistent, one CTA per SM; the CTA takes a contiguous slice of the work
+//     list and merges consecutive units that share their x rows (they are row
+//     blocks of one matrix for one token chunk — qmoe_moe_plan's order) into
+//     one RUN: x is staged once per run, then the 16 warps stride over the
+//     run's row tasks with no further CTA synchronisation;
+//   * the hot prefix of the packed entry table (a frequency codebook in the
+//     MoE layer) is staged in shared memory once per launch;
+//   * a task is 32 / G rows: each lane owns one contiguous SEGMENT of a row
+//     (G = 2^lg segments, lg from the matrix's checkpoints; lg = 0: a lane per
+//     row) and walks it with a running column offset starting at the row's
+//     checkpoint — no scans. Codewords stream from HBM in sector-aligned
+//     16-codeword groups (2 x 16-byte loads bypassing L1), group g+2 loaded,
+//     g+1 looked up and g applied per iteration; the next task's row
+//     metadata is prefetched while the current task runs;
+//   * per non-zero slot acc += level(code) * x[col] in fp32; the row's sum is
+//     reduced over its G lanes and bf16-rounded once (codec.py:243).
+// Entry format "matvec" (qmoe_host.cpp, esz = bytes per staged x element):
 //   bits 0-4 len = 2n | bits 5-11, 12-18, 19-25: position * esz of non-zero
 //   slot 0..2 | bits 26-28 slot used | bits 29-31 slot is code 2 (row max).
 //
@@ -37,42 +33,14 @@ using namespace qmoe_dev;
 
 namespace {
 
-constexpr int NCONS = 15;                  // consumer warps (16 warps total: 4 per SMSP)
-constexpr int THREADS = (NCONS + 1) * 32;  // + one producer warp
-constexpr int STAGES = 8;
-constexpr int CW_CAP = 3072;               // codewords per staged unit
-constexpr int ROW_CAP = 128;               // rows per staged unit
-constexpr int BATCH = 8;                   // codewords looked up per batch per lane
-constexpr uint32_t COLD_ZERO = 65536;      // tables carry zero entries from here
-constexpr int NT_STREAM = 2;               // tokens per unit on the streaming path
-constexpr int RING = 64;                   // producer record ring
-
-// ----------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+#ifndef QMOE_LEAN_THREADS
+#define QMOE_LEAN_THREADS 512
+#endif
+constexpr int THREADS = QMOE_LEAN_THREADS;
+constexpr int NWARPS = THREADS / 32;
+constexpr int GRP = 16;                // codewords per aligned 32-byte group
+constexpr int NT_STREAM = 2;           // tokens per unit on the streaming path
+constexpr int MAX_LG = 2;              // G <= 4 lanes per row on the fast path
 
 template <int ESZ>
 struct XType;
@@ -87,7 +55,6 @@ struct XType<2> {
   static __device__ __forceinline__ float get(uint16_t v) { return __uint_as_float(uint32_t(v) << 16); }
 };
 
-// ----------------------------------------------------------------- records
 struct Rec {  // == qmoe_work (80 bytes)
   const uint16_t* cw;
   const int32_t* ro;
@@ -97,15 +64,6 @@ struct Rec {  // == qmoe_work (80 bytes)
   int32_t tok[QMOE_NT_MAX];
 };
 static_assert(sizeof(Rec) == sizeof(qmoe_work), "record layout");
-
-// per-slot staging metadata written by the producer before the full arrive
-struct SlotMeta {
-  Rec r;
-  uint32_t cw_s, ro_s, mm_s, ck_s, x_s;  // byte offsets (from the smem base) of the staged ranges
-  int32_t direct;                        // 1: unit exceeds the slot, read global
-  int32_t next;                          // task dispenser (smem atomic)
-  int32_t pad;
-};
 
 struct StreamParams {
   const uint32_t* gtab;       // matvec-format table variant (zero entries from 65536)
@@ -123,8 +81,8 @@ struct StreamParams {
   int y_mode;
   int64_t ldy;
   int32_t* bad;
-  int xcap;                   // elements per token slot of an x buffer
-  int ntmax;                  // token slots per x buffer
+  int xcap;                   // elements per token slot of the x buffer
+  int ntmax;                  // token slots
 };
 
 __device__ __forceinline__ void make_rec(const StreamParams& P, int u, Rec& R) {
@@ -149,345 +107,201 @@ __device__ __forceinline__ void make_rec(const StreamParams& P, int u, Rec& R) {
     R.ntok = (int)min((int64_t)P.ntu_single, P.ntok_single - t0);
 #pragma unroll
     for (int q = 0; q < QMOE_NT_MAX; ++q) R.tok[q] = (int)(t0 + min(q, R.ntok - 1));
-    R.cw0 = __ldg(R.ro + R.row0);
-    R.cw1 = __ldg(R.ro + R.row1);
+    R.cw0 = 0;
+    R.cw1 = 0;
   }
 }
 
-__device__ __forceinline__ bool same_x(const Rec& a, const Rec& b) {
-  bool s = a.cols == b.cols && a.ntok == b.ntok;
+// same matrix, contiguous rows and same tokens: the units merge into one run
+__device__ __forceinline__ bool continues(const Rec& a, const Rec& b) {
+  bool s = a.cw == b.cw && a.row1 == b.row0 && a.ntok == b.ntok && a.lg == b.lg;
 #pragma unroll
   for (int q = 0; q < QMOE_NT_MAX; ++q) s = s && (q >= a.ntok || a.tok[q] == b.tok[q]);
   return s;
 }
 
-__device__ __forceinline__ uint32_t span(const void* begin, size_t nbytes, uint32_t& delta, uintptr_t& a0) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(begin);
-  a0 = a & ~uintptr_t(15);
-  delta = (uint32_t)(a - a0);
-  return (uint32_t)(((a + nbytes + 15) & ~uintptr_t(15)) - a0);
+__device__ __forceinline__ void ld_group(const uint16_t* cw, int64_t g, uint4& a, uint4& b) {
+  const uint4* p = reinterpret_cast<const uint4*>(cw + g * GRP);
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+               : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p + 1));
 }
 
-// ----------------------------------------------------------------- consumer
-// Look up BATCH codewords of this lane's segment starting at k0 (past the
-// segment's end: the zero entry at COLD_ZERO).
-__device__ __forceinline__ void lookup_batch(uint32_t (&t)[BATCH], const uint16_t* cw, int cnt, int k0,
+// entries of the 16 codewords of a group; positions outside the lane's
+// segment (mask bit clear) get the zero entry
+__device__ __forceinline__ void lookup_group(uint32_t (&t)[GRP], const uint4& a, const uint4& b, uint32_t mask,
                                              const uint32_t* tab, uint32_t H, const uint32_t* __restrict__ gtab) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int u = 0; u < BATCH; ++u) {
-    const uint32_t c = (k0 + u < cnt) ? (uint32_t)cw[k0 + u] : COLD_ZERO;
-    t[u] = c < H ? tab[c] : __ldg(gtab + c);
+  for (int u = 0; u < GRP; ++u) {
+    const uint32_t c = (u & 1) ? (w[u >> 1] >> 16) : (w[u >> 1] & 0xFFFFu);
+    const uint32_t e = c < H ? tab[c] : __ldg(gtab + c);
+    t[u] = ((mask >> u) & 1u) ? e : 0u;
   }
 }
 
-// Apply BATCH entries at the running column `off` (elements).
 template <int NT, int ESZ>
-__device__ __forceinline__ void apply_batch(const uint32_t (&t)[BATCH], const typename XType<ESZ>::T* xs, int xslot,
-                                            int& off, float (&S)[NT], float (&T)[NT]) {
+__device__ __forceinline__ void apply_group(const uint32_t (&t)[GRP], const typename XType<ESZ>::T* xs, int xslot,
+                                            int& off, float lmin, float lmax, float (&acc)[NT]) {
   using XT = typename XType<ESZ>::T;
 #pragma unroll
-  for (int u = 0; u < BATCH; ++u) {
+  for (int u = 0; u < GRP; ++u) {
     const uint32_t e = t[u];
     const char* xo = reinterpret_cast<const char*>(xs + off);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       const bool used = (e >> (26 + j)) & 1u;
-      const bool two = (e >> (29 + j)) & 1u;
+      const float w = ((e >> (29 + j)) & 1u) ? lmax : lmin;
       const XT* xp = reinterpret_cast<const XT*>(xo + ((e >> (5 + 7 * j)) & 0x7Fu));
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         const float v = used ? XType<ESZ>::get(xp[q * xslot]) : 0.f;
-        S[q] += v;
-        T[q] += two ? v : 0.f;
+        acc[q] = fmaf(w, v, acc[q]);
       }
     }
     off += int(e & 31u);
   }
 }
 
-template <int NT, int ESZ>
-__device__ __forceinline__ void run_unit(const StreamParams& P, SlotMeta& M, const uint8_t* smem) {
-  using XT = typename XType<ESZ>::T;
-  const int lane = threadIdx.x & 31;
-  // everything the task loop needs, read once
-  const int row0 = M.r.row0, nrows = M.r.row1 - M.r.row0, cw0 = M.r.cw0, cols = M.r.cols, ntok = M.r.ntok;
-  const int lg = M.r.lg;
-  int tok[NT];
-#pragma unroll
-  for (int q = 0; q < NT; ++q) tok[q] = M.r.tok[q];
-  const uint16_t* cwp = reinterpret_cast<const uint16_t*>(smem + M.cw_s);
-  const int32_t* rop = reinterpret_cast<const int32_t*>(smem + M.ro_s);
-  const uint32_t* mmp = reinterpret_cast<const uint32_t*>(smem + M.mm_s);
-  const uint16_t* ckp = reinterpret_cast<const uint16_t*>(smem + M.ck_s);
-  const XT* xs = reinterpret_cast<const XT*>(smem + M.x_s);
-  const uint32_t* tab = reinterpret_cast<const uint32_t*>(smem);
-  int32_t* next = &M.next;
-  const int G = 1 << lg;
-  const int rg = lane >> lg, seg = lane & (G - 1);
-  const int ntasks = (nrows + (32 >> lg) - 1) >> (5 - lg);
-  const uint32_t H = (uint32_t)P.H;
-  const uint32_t* gtab = P.gtab;
-  const int xslot = P.xcap;
-  for (;;) {
-    int task = 0;
-    if (lane == 0) task = atomicAdd(next, 1);
-    task = __shfl_sync(FULL_MASK, task, 0);
-    if (task >= ntasks) break;
-    const int i = (task << (5 - lg)) + rg;
-    const bool valid = i < nrows;
-    int b = 0, cnt = 0, off = 0;
-    uint32_t mm = 0;
-    if (valid) {
-      const int s = rop[i] - cw0;
-      const int n = rop[i + 1] - rop[i];
-      b = s + ((seg * n) >> lg);
-      cnt = s + (((seg + 1) * n) >> lg) - b;
-      off = seg ? (int)ckp[i * (G - 1) + seg - 1] : 0;
-      mm = mmp[i];
-    }
-    const int maxc = __reduce_max_sync(FULL_MASK, cnt);
-    float S[NT], T[NT];
-#pragma unroll
-    for (int q = 0; q < NT; ++q) S[q] = T[q] = 0.f;
-    const uint16_t* c = cwp + b;
-    uint32_t ta[BATCH], tb[BATCH];
-    lookup_batch(ta, c, cnt, 0, tab, H, gtab);
-    for (int k0 = 0;;) {
-      if (k0 + BATCH < maxc) lookup_batch(tb, c, cnt, k0 + BATCH, tab, H, gtab);
-      apply_batch<NT, ESZ>(ta, xs, xslot, off, S, T);
-      k0 += BATCH;
-      if (k0 >= maxc) break;
-      if (k0 + BATCH < maxc) lookup_batch(ta, c, cnt, k0 + BATCH, tab, H, gtab);
-      apply_batch<NT, ESZ>(tb, xs, xslot, off, S, T);
-      k0 += BATCH;
-      if (k0 >= maxc) break;
-    }
-#pragma unroll
-    for (int q = 0; q < NT; ++q) {
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1)
-        if (d < G) {
-          S[q] += __shfl_xor_sync(FULL_MASK, S[q], d);
-          T[q] += __shfl_xor_sync(FULL_MASK, T[q], d);
-        }
-    }
-    if (!valid || seg != G - 1) continue;  // the last segment's lane ends the row
-    const int r = row0 + i;
-    if (off != cols) {  // row decodes to the wrong number of values: never written
-      if (P.bad) {
-        atomicAdd(P.bad, 1);
-        atomicMin(P.bad + 1, r);
-      }
-      continue;
-    }
-    const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
-    const float dl = lmax - lmin;
-#pragma unroll
-    for (int q = 0; q < NT; ++q) {
-      if (q >= ntok) break;
-      const float v = bf16_round_dev(fmaf(lmin, S[q], dl * T[q]));
-      if (P.y_mode == QMOE_Y_RELU_BF16) {
-        uint16_t* yp = reinterpret_cast<uint16_t*>(P.y) + (int64_t)tok[q] * P.ldy + r;
-        *yp = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
-      } else if (P.y_mode == QMOE_Y_STORE_F32) {
-        reinterpret_cast<float*>(P.y)[(int64_t)tok[q] * P.ldy + r] = v + 0.f;  // == 0 + v
-      } else {
-        float* yp = reinterpret_cast<float*>(P.y) + (int64_t)tok[q] * P.ldy + r;
-        *yp = *yp + v;
-      }
-    }
-  }
+__device__ __forceinline__ uint32_t group_mask(int64_t g, int64_t A, int64_t B) {
+  const int64_t base = g * GRP;
+  const int lo = (int)max((int64_t)0, min((int64_t)GRP, A - base));
+  const int hi = (int)max((int64_t)0, min((int64_t)GRP, B - base));
+  return ((1u << hi) - 1u) & ~((1u << lo) - 1u);
 }
 
-// Slow path for units larger than a slot: everything read from global.
-template <int ESZ>
-__device__ void run_unit_direct(const StreamParams& P, const SlotMeta& M, int cwarp) {
-  const Rec& R = M.r;
-  const int lane = threadIdx.x & 31;
-  for (int i = cwarp; i < R.row1 - R.row0; i += NCONS) {
-    const int r = R.row0 + i;
-    const int s = __ldg(R.ro + r), e = __ldg(R.ro + r + 1);
-    const uint32_t mm = __ldg(R.mm + r);
-    const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
-    float acc0 = 0.f, acc1 = 0.f;
-    int base = 0;
-    for (int p0 = s; p0 < e; p0 += 32) {
-      const uint32_t c = p0 + lane < e ? (uint32_t)__ldg(R.cw + p0 + lane) : COLD_ZERO;
-      const uint32_t t = __ldg(P.gtab + c);
-      const int len = int(t & 31u);
-      int incl = len;
-      for (int d = 1; d < 32; d <<= 1) {
-        const int v = __shfl_up_sync(FULL_MASK, incl, d);
-        if (lane >= d) incl += v;
-      }
-      const int off = base + incl - len;
-      base += __shfl_sync(FULL_MASK, incl, 31);
-      for (int j = 0; j < 3; ++j) {
-        if (!((t >> (26 + j)) & 1u)) continue;
-        const int col = off + int(((t >> (5 + 7 * j)) & 0x7Fu) / ESZ);
-        const float w = ((t >> (29 + j)) & 1u) ? lmax : lmin;
-        for (int q = 0; q < R.ntok && q < 2; ++q) {
-          const int64_t xi = (int64_t)R.tok[q] * P.ldx + col;
-          const float xv = ESZ == 2 ? __uint_as_float(uint32_t(__ldg(reinterpret_cast<const uint16_t*>(P.x) + xi)) << 16)
-                                    : __ldg(reinterpret_cast<const float*>(P.x) + xi);
-          if (q == 0) acc0 = fmaf(w, xv, acc0);
-          else acc1 = fmaf(w, xv, acc1);
-        }
-      }
-    }
-    acc0 = warp_sum(acc0);
-    acc1 = warp_sum(acc1);
-    if (lane != 0) continue;
-    if (base != R.cols) {
-      if (P.bad) {
-        atomicAdd(P.bad, 1);
-        atomicMin(P.bad + 1, r);
-      }
-      continue;
-    }
-    for (int q = 0; q < R.ntok && q < 2; ++q) {
-      const float v = bf16_round_dev(q == 0 ? acc0 : acc1);
-      if (P.y_mode == QMOE_Y_RELU_BF16)
-        reinterpret_cast<uint16_t*>(P.y)[(int64_t)R.tok[q] * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
-      else if (P.y_mode == QMOE_Y_STORE_F32)
-        reinterpret_cast<float*>(P.y)[(int64_t)R.tok[q] * P.ldy + r] = v + 0.f;
-      else {
-        float* yp = reinterpret_cast<float*>(P.y) + (int64_t)R.tok[q] * P.ldy + r;
-        *yp = *yp + v;
-      }
-    }
-  }
-}
-
-struct Carve {
-  uint32_t tab_s, bar_full, bar_empty, bar_tab, cwbuf, robuf, mmbuf, ckbuf, xbuf, xbytes;
-  SlotMeta* meta;
-  Rec* ring;  // producer's record ring [RING]
+// row metadata of one lane's segment
+struct Seg {
+  int64_t A, B;  // codeword range
+  int off;       // starting column
+  uint32_t mm;   // bf16 (min, max)
+  int row;       // absolute row, or -1
 };
 
-// Producer warp: keeps the records of the next 32 units in flight in
-// registers, the current ones in a shared-memory ring, and stages one unit
-// per iteration into the ring of STAGES slots (lane 0 issues the bulk copies).
-template <int ESZ>
-__device__ __noinline__ void producer(const StreamParams& P, const Carve& C, int u0, int u1) {
+__device__ __forceinline__ Seg load_seg(const Rec& R, int task, int lg, int rb) {
+  Seg sg{0, 0, 0, 0u, -1};
   const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    mbar_arrive_expect_tx(C.bar_tab, (uint32_t)P.H * 4);
-    if (P.H > 0) bulk_g2s(C.tab_s, P.gtab, (uint32_t)P.H * 4, C.bar_tab);
+  const int G = 1 << lg;
+  const int r = R.row0 + (task << (5 - lg)) + (lane >> lg);
+  if (r < rb) {
+    const int seg = lane & (G - 1);
+    const int s = __ldg(R.ro + r), e = __ldg(R.ro + r + 1);
+    const int n = e - s;
+    sg.A = s + ((seg * n) >> lg);
+    sg.B = s + (((seg + 1) * n) >> lg);
+    sg.off = seg ? (int)__ldg(R.ck + (size_t)r * (G - 1) + seg - 1) : 0;
+    sg.mm = __ldg(R.mm + r);
+    sg.row = r;
   }
-  Rec nxt;
-  for (int v = u0 + lane; v < min(u1, u0 + RING); v += 32) {
-    Rec r;
-    make_rec(P, v, r);
-    C.ring[(v - u0) % RING] = r;
+  return sg;
+}
+
+template <int NT, int ESZ>
+__device__ __forceinline__ void run_task(const StreamParams& P, const Rec& R, const Seg& sg, int lg, const int (&tok)[NT],
+                                         const typename XType<ESZ>::T* xs, const uint32_t* tab) {
+  const int lane = threadIdx.x & 31;
+  const int G = 1 << lg;
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t* gtab = P.gtab;
+  const int64_t A = sg.A, B = sg.B;
+  const bool has = sg.row >= 0 && B > A;
+  const int64_t g0 = has ? A / GRP : 0;
+  const int ng = has ? (int)((B + GRP - 1) / GRP - g0) : 0;
+  const int64_t glast = has ? (B - 1) / GRP : 0;
+  const int maxg = __reduce_max_sync(FULL_MASK, ng);
+  const float lmin = __uint_as_float(sg.mm << 16), lmax = __uint_as_float(sg.mm & 0xFFFF0000u);
+  int off = sg.off;
+  float acc[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) acc[q] = 0.f;
+  if (maxg > 0) {
+    const uint16_t* cw = R.cw;
+    uint4 ra0, ra1, rb0, rb1;
+    uint32_t ta[GRP], tb[GRP];
+    // groups past this lane's segment re-read its last group (mask 0)
+    ld_group(cw, g0, ra0, ra1);
+    if (maxg > 1) ld_group(cw, min(g0 + 1, glast), rb0, rb1);
+    lookup_group(ta, ra0, ra1, group_mask(g0, A, B), tab, H, gtab);
+    for (int it = 0;;) {
+      if (it + 2 < maxg) ld_group(cw, min(g0 + it + 2, glast), ra0, ra1);
+      if (it + 1 < maxg) lookup_group(tb, rb0, rb1, group_mask(g0 + it + 1, A, B), tab, H, gtab);
+      apply_group<NT, ESZ>(ta, xs, P.xcap, off, lmin, lmax, acc);
+      if (++it >= maxg) break;
+      if (it + 2 < maxg) ld_group(cw, min(g0 + it + 2, glast), rb0, rb1);
+      if (it + 1 < maxg) lookup_group(ta, ra0, ra1, group_mask(g0 + it + 1, A, B), tab, H, gtab);
+      apply_group<NT, ESZ>(tb, xs, P.xcap, off, lmin, lmax, acc);
+      if (++it >= maxg) break;
+    }
   }
-  if (u0 + RING + lane < u1) make_rec(P, u0 + RING + lane, nxt);
-  __syncwarp();
-  int cur_xb = 1;
-  int last_x0 = -1, last_x1 = -1;  // last unit that used x buffer 0 / 1
-  int consumed = -1;               // highest relative unit known consumed
-  for (int u = u0; u < u1; ++u) {
-    const int rel = u - u0;
-    if (lane == 0) {
-      const Rec& R = C.ring[rel % RING];
-      const int s = rel % STAGES;
-      if (rel >= STAGES) {
-        while (consumed < rel - STAGES) {
-          ++consumed;
-          mbar_wait(C.bar_empty + 8 * (consumed % STAGES), (uint32_t)((consumed / STAGES) & 1));
-        }
-      }
-      SlotMeta& M = C.meta[s];
-      const int nrows = R.row1 - R.row0;
-      const int ncw = R.cw1 - R.cw0;
-      const int nck = (1 << R.lg) - 1;
-      M.r = R;
-      M.direct = (ncw > CW_CAP || nrows > ROW_CAP || nck > 7) ? 1 : 0;
-      M.next = 0;
-      const bool reuse = rel > 0 && same_x(C.ring[(rel - 1) % RING], R);
-      int xb = cur_xb;
-      if (!reuse) {
-        xb = cur_xb ^ 1;
-        const int v = xb ? last_x1 : last_x0;
-        while (v >= 0 && consumed < v) {
-          ++consumed;
-          mbar_wait(C.bar_empty + 8 * (consumed % STAGES), (uint32_t)((consumed / STAGES) & 1));
-        }
-      }
-      if (xb) last_x1 = rel;
-      else last_x0 = rel;
-      cur_xb = xb;
-      M.x_s = C.xbuf + (uint32_t)xb * C.xbytes - C.tab_s;
-      const uint32_t full = C.bar_full + 8 * s;
-      const uint32_t cw_dst = C.cwbuf + s * (CW_CAP * 2 + 64);
-      const uint32_t ro_dst = C.robuf + s * (ROW_CAP * 4 + 64);
-      const uint32_t mm_dst = C.mmbuf + s * (ROW_CAP * 4 + 64);
-      const uint32_t ck_dst = C.ckbuf + s * (ROW_CAP * 2 * 7 + 64);
-      uintptr_t acw = 0, aro = 0, amm = 0, ack = 0;
-      uint32_t bcw = 0, bro = 0, bmm = 0, bck = 0, dcw = 0, dro = 0, dmm = 0, dck = 0, total = 0;
-      if (!M.direct) {
-        bcw = span(R.cw + R.cw0, (size_t)ncw * 2, dcw, acw);
-        bro = span(R.ro + R.row0, (size_t)(nrows + 1) * 4, dro, aro);
-        bmm = span(R.mm + R.row0, (size_t)nrows * 4, dmm, amm);
-        if (nck) bck = span(R.ck + (size_t)R.row0 * nck, (size_t)nrows * nck * 2, dck, ack);
-        total = bcw + bro + bmm + bck;
-      }
-      const size_t xrow = (size_t)R.cols * ESZ;
-      const uint32_t xrow16 = (uint32_t)((xrow + 15) & ~size_t(15));  // x rows are 16-byte aligned
-      if (!reuse) total += xrow16 * (uint32_t)R.ntok;
-      M.cw_s = cw_dst + dcw - C.tab_s;
-      M.ro_s = ro_dst + dro - C.tab_s;
-      M.mm_s = mm_dst + dmm - C.tab_s;
-      M.ck_s = ck_dst + dck - C.tab_s;
-      fence_proxy_async();
-      mbar_arrive_expect_tx(full, total);  // releases M.* to the consumers
-      if (bcw) bulk_g2s(cw_dst, reinterpret_cast<const void*>(acw), bcw, full);
-      if (bro) bulk_g2s(ro_dst, reinterpret_cast<const void*>(aro), bro, full);
-      if (bmm) bulk_g2s(mm_dst, reinterpret_cast<const void*>(amm), bmm, full);
-      if (bck) bulk_g2s(ck_dst, reinterpret_cast<const void*>(ack), bck, full);
-      if (!reuse) {
-        for (int q = 0; q < R.ntok; ++q)
-          bulk_g2s(C.tab_s + M.x_s + (uint32_t)q * P.xcap * ESZ,
-                   reinterpret_cast<const uint8_t*>(P.x) + (int64_t)R.tok[q] * P.ldx * ESZ, xrow16, full);
-      }
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1)
+      if (d < G) acc[q] += __shfl_xor_sync(FULL_MASK, acc[q], d);
+  }
+  if (sg.row < 0 || (lane & (G - 1)) != G - 1) return;  // the last segment's lane ends the row
+  const int r = sg.row;
+  if (off != R.cols) {  // row decodes to the wrong number of values: never written
+    if (P.bad) {
+      atomicAdd(P.bad, 1);
+      atomicMin(P.bad + 1, r);
     }
-    // after the last unit of a 32-batch: park the prefetched records in the
-    // ring half that just drained and prefetch the next batch
-    if ((rel & 31) == 31) {
-      __syncwarp();
-      const int v = u + 1 + (RING - 32) + lane;
-      if (v < u1) C.ring[(v - u0) % RING] = nxt;
-      __syncwarp();
-      if (v + 32 < u1) make_rec(P, v + 32, nxt);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    if (q >= R.ntok) break;
+    const float v = bf16_round_dev(acc[q]);
+    if (P.y_mode == QMOE_Y_RELU_BF16) {
+      reinterpret_cast<uint16_t*>(P.y)[(int64_t)tok[q] * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+    } else if (P.y_mode == QMOE_Y_STORE_F32) {
+      reinterpret_cast<float*>(P.y)[(int64_t)tok[q] * P.ldy + r] = v + 0.f;  // == 0 + v
+    } else {
+      float* yp = reinterpret_cast<float*>(P.y) + (int64_t)tok[q] * P.ldy + r;
+      *yp = *yp + v;
     }
-    __syncwarp();
   }
 }
 
-template <int ESZ>
-__global__ void __launch_bounds__(THREADS, 1) stream_matvec_kernel(StreamParams P) {
+// the warp's tasks of one run: task = warp, warp + NWARPS, ... with the next
+// task's segment metadata loaded before the current task runs
+template <int NT, int ESZ>
+__device__ __forceinline__ void run_run(const StreamParams& P, const Rec& R, int rb, const typename XType<ESZ>::T* xs,
+                                        const uint32_t* tab) {
+  const int warp = threadIdx.x >> 5;
+  const int lg = R.lg;
+  const int ntasks = (rb - R.row0 + (32 >> lg) - 1) >> (5 - lg);
+  int tok[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) tok[q] = R.tok[q];
+  int task = warp;
+  if (task >= ntasks) return;
+  Seg cur = load_seg(R, task, lg, rb);
+  for (;;) {
+    const int nt = task + NWARPS;
+    Seg nxt{0, 0, 0, 0u, -1};
+    if (nt < ntasks) nxt = load_seg(R, nt, lg, rb);
+    run_task<NT, ESZ>(P, R, cur, lg, tok, xs, tab);
+    if (nt >= ntasks) break;
+    cur = nxt;
+    task = nt;
+  }
+}
+
+// x is always staged as fp32 (converted while copying), so the inner loop
+// uses the esz-4 entry table and needs no per-slot conversion.
+template <int IN_ESZ>
+__global__ void __launch_bounds__(THREADS, 1) lean_matvec_kernel(StreamParams P) {
+  constexpr int ESZ = 4;
+  using XT = float;
   extern __shared__ __align__(128) uint8_t smem[];
-  Carve C;
-  C.tab_s = saddr(smem);
-  uint8_t* p = smem + (size_t)P.H * 4;
-  C.bar_full = saddr(p);  // STAGES x 8
-  C.bar_empty = C.bar_full + 8 * STAGES;
-  C.bar_tab = C.bar_empty + 8 * STAGES;
-  p += 128;
-  C.meta = reinterpret_cast<SlotMeta*>(p);
-  p += ((sizeof(SlotMeta) * STAGES + 127) / 128) * 128;
-  C.ring = reinterpret_cast<Rec*>(p);
-  p += sizeof(Rec) * RING;
-  C.cwbuf = saddr(p);
-  p += STAGES * (CW_CAP * 2 + 64);
-  C.robuf = saddr(p);
-  p += STAGES * (ROW_CAP * 4 + 64);
-  C.mmbuf = saddr(p);
-  p += STAGES * (ROW_CAP * 4 + 64);
-  C.ckbuf = saddr(p);
-  p += STAGES * (ROW_CAP * 2 * 7 + 64);
-  C.xbuf = saddr(p);  // [2][ntmax][xcap]
-  C.xbytes = (uint32_t)P.ntmax * P.xcap * ESZ;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
+  XT* xs = reinterpret_cast<XT*>(smem + (size_t)P.H * 4);
+  __shared__ int s_run_end;
+  __shared__ Rec s_rec;
 
   int n;
   if (P.work) n = min(*P.n_work, P.max_work);
@@ -497,36 +311,112 @@ __global__ void __launch_bounds__(THREADS, 1) stream_matvec_kernel(StreamParams 
   }
   const int u0 = (int)((int64_t)n * blockIdx.x / gridDim.x);
   const int u1 = (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
-  if (u0 >= u1) return;  // whole CTA exits before any barrier use
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(C.bar_full + 8 * s, 1);
-      mbar_init(C.bar_empty + 8 * s, NCONS);
-    }
-    mbar_init(C.bar_tab, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (u0 >= u1) return;
+  {  // table prefix: vectorised copy by all threads
+    const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
+    uint4* dst = reinterpret_cast<uint4*>(tab);
+    for (int i = threadIdx.x; i < P.H / 4; i += THREADS) dst[i] = __ldg(src + i);
   }
-  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int u = u0; u < u1;) {
+    // ---- find the run starting at u (warp 0: 32 records per step)
+    if (warp == 0) {
+      Rec first;
+      make_rec(P, u, first);
+      int end = u + 1;
+      bool open = true;
+      for (int base = u + 1; open && base < u1; base += 31) {
+        // lane j (j >= 1) checks unit base + j - 1 against its predecessor
+        Rec mine, prev;
+        const int v = base + lane - 1;
+        if (lane >= 1 && v < u1) {
+          make_rec(P, v, mine);
+          make_rec(P, v - 1, prev);
+        }
+        const bool ok = lane >= 1 && v < u1 && continues(prev, mine);
+        const unsigned brk = __ballot_sync(FULL_MASK, !ok) & ~1u;
+        if (brk) {
+          end = base + (__ffs(brk) - 1) - 1;
+          open = false;
+        } else {
+          end = min(u1, base + 31);
+        }
+      }
+      if (lane == 0) {
+        s_run_end = end;
+        s_rec = first;
+      }
+    }
+    __syncthreads();  // previous run finished (x buffer free) + run published
+    const int end = s_run_end;
+    Rec R = s_rec;
+    if (end - 1 > u) {
+      Rec last;
+      make_rec(P, end - 1, last);
+      R.cw1 = last.cw1;
+      R.row1 = last.row1;
+    }
+    if (!P.work) R.cw1 = 0;
+    // ---- stage x rows of the run's tokens
+    for (int q = 0; q < R.ntok; ++q) {
+      XT* dst = xs + (size_t)q * P.xcap;
+      if (IN_ESZ == 2) {
+        const uint16_t* src = reinterpret_cast<const uint16_t*>(P.x) + (int64_t)R.tok[q] * P.ldx;
+        for (int i = threadIdx.x; i < P.xcap; i += THREADS)
+          dst[i] = i < R.cols ? __uint_as_float(uint32_t(__ldg(src + i)) << 16) : 0.f;
+      } else {
+        const float* src = reinterpret_cast<const float*>(P.x) + (int64_t)R.tok[q] * P.ldx;
+        for (int i = threadIdx.x; i < P.xcap; i += THREADS) dst[i] = i < R.cols ? __ldg(src + i) : 0.f;
+      }
+    }
+    __syncthreads();
+    if (R.ntok == 1) run_run<1, ESZ>(P, R, R.row1, xs, tab);
+    else run_run<2, ESZ>(P, R, R.row1, xs, tab);
+    u = end;
+  }
+}
 
-  if (warp == 0) {
-    producer<ESZ>(P, C, u0, u1);
+// ----------------------------------------------------------------- host side
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int hot_override() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("QMOE_HOT_ENTRIES");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+int launch_lean(const qmoe_dict* d, StreamParams& P, int esz, int max_cols, int ntmax, int grid, int hot_want,
+                cudaStream_t st) {
+  P.ntmax = ntmax;
+  P.xcap = ((max_cols + 32 + 15) / 16) * 16;
+  const size_t xbytes = (size_t)ntmax * P.xcap * 4;  // staged as fp32
+  const size_t static_smem = sizeof(Rec) + 64;
+  if (xbytes + static_smem + 4096 > (size_t)d->max_smem_optin)
+    return qmoe::fail(QMOE_EUNSUPPORTED, "cols too large for the shared-memory x staging buffer");
+  int H = (int)((d->max_smem_optin - xbytes - static_smem - 256) / 4);
+  if (hot_override() >= 0) hot_want = hot_override();
+  H = std::min(H, std::min(hot_want, QMOE_DICT_SIZE));
+  H &= ~255;
+  P.H = H;
+  const size_t smem = (size_t)H * 4 + xbytes;
+  if (esz == 2) {
+    CK(cudaFuncSetAttribute(lean_matvec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    lean_matvec_kernel<2><<<grid, THREADS, smem, st>>>(P);
   } else {
-    const int cwarp = warp - 1;
-    mbar_wait(C.bar_tab, 0);
-    for (int u = u0; u < u1; ++u) {
-      const int rel = u - u0;
-      const int s = rel % STAGES;
-      mbar_wait(C.bar_full + 8 * s, (uint32_t)((rel / STAGES) & 1));
-      SlotMeta& M = C.meta[s];
-      if (M.direct) run_unit_direct<ESZ>(P, M, cwarp);
-      else if (M.r.ntok == 1) run_unit<1, ESZ>(P, M, smem);
-      else run_unit<2, ESZ>(P, M, smem);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(C.bar_empty + 8 * s);
-    }
+    CK(cudaFuncSetAttribute(lean_matvec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    lean_matvec_kernel<4><<<grid, THREADS, smem, st>>>(P);
   }
+  CK(cudaGetLastError(), "lean_matvec_kernel launch");
+  return QMOE_OK;
+}
+
+const uint32_t* pick_table(const qmoe_dict* d, const uint32_t* user, int esz) {
+  // tables hold both variants back to back: [esz 4 | esz 2], MT_STRIDE entries each
+  if (user) return esz == 4 ? user : user + qmoe::MT_STRIDE;
+  return esz == 4 ? d->d_mtab : d->d_mtab + qmoe::MT_STRIDE;
 }
 
 // ----------------------------------------------------------------- general path
@@ -632,53 +522,6 @@ __global__ void __launch_bounds__(256) general_matvec_kernel(GeneralParams P) {
   }
 }
 
-// ----------------------------------------------------------------- host side
-size_t fixed_smem() {
-  return 128 + ((sizeof(SlotMeta) * STAGES + 127) / 128) * 128 + sizeof(Rec) * RING +
-         STAGES * (CW_CAP * 2 + 64) + 2 * STAGES * (ROW_CAP * 4 + 64) + STAGES * (ROW_CAP * 2 * 7 + 64);
-}
-
-int hot_override() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("QMOE_HOT_ENTRIES");
-    v = e ? atoi(e) : -1;
-  }
-  return v;
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-int launch_stream(const qmoe_dict* d, StreamParams& P, int esz, int max_cols, int ntmax, int grid, int hot_want,
-                  cudaStream_t st) {
-  P.ntmax = ntmax;
-  P.xcap = ((max_cols + 32 + 15) / 16) * 16;
-  const size_t xbytes = 2 * (size_t)ntmax * P.xcap * esz;
-  const size_t fixed = fixed_smem() + xbytes;
-  if (fixed + 4096 > (size_t)d->max_smem_optin)
-    return qmoe::fail(QMOE_EUNSUPPORTED, "cols too large for the shared-memory x staging buffer");
-  int H = (int)((d->max_smem_optin - fixed) / 4);
-  if (hot_override() >= 0) hot_want = hot_override();
-  H = std::min(H, std::min(hot_want, QMOE_DICT_SIZE));
-  H &= ~255;
-  P.H = H;
-  const size_t smem = (size_t)H * 4 + fixed;
-  if (esz == 2) {
-    CK(cudaFuncSetAttribute(stream_matvec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    stream_matvec_kernel<2><<<grid, THREADS, smem, st>>>(P);
-  } else {
-    CK(cudaFuncSetAttribute(stream_matvec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    stream_matvec_kernel<4><<<grid, THREADS, smem, st>>>(P);
-  }
-  CK(cudaGetLastError(), "stream_matvec_kernel launch");
-  return QMOE_OK;
-}
-
-const uint32_t* pick_table(const qmoe_dict* d, const uint32_t* user, int esz) {
-  // tables hold both variants back to back: [esz 4 | esz 2], MT_STRIDE entries each
-  if (user) return esz == 4 ? user : user + qmoe::MT_STRIDE;
-  return esz == 4 ? d->d_mtab : d->d_mtab + qmoe::MT_STRIDE;
-}
 
 }  // namespace
 
@@ -698,11 +541,10 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
   if (d->sparse_ok) {
     // rows per unit from a typical ~24 values per codeword (no host sync; a
     // unit that outgrows a slot is read directly from global)
-    const double per_row = std::max(1.0, (double)cols / 24.0);
-    const int rpu = (int)std::max(1.0, std::min(0.75 * CW_CAP / per_row, (double)ROW_CAP));
+    const int rpu = 256;
     const int ntu = (int)std::min<int64_t>(ntok, NT_STREAM);
     StreamParams P{};
-    P.gtab = pick_table(d, nullptr, esz);
+    P.gtab = pick_table(d, nullptr, 4);  // x is staged as fp32
     P.work = nullptr;
     P.single = qmoe_matrix{d_cw, d_row_off, d_mm, nullptr, (int32_t)rows, (int32_t)cols, 0, 0};
     P.rows_per_unit = rpu;
@@ -720,7 +562,7 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
     // small launches stage a smaller hot table (the fill is per CTA)
     const int64_t est_cw = rows * cols / 24 + rows;
     const int want = (int)std::min<int64_t>(QMOE_DICT_SIZE, std::max<int64_t>(4096, est_cw / grid * 2));
-    return launch_stream(d, P, esz, (int)cols, ntu, grid, want, S(stream));
+    return launch_lean(d, P, esz, (int)cols, ntu, grid, want, S(stream));
   }
   GeneralParams G{};
   G.words = d->d_words;
@@ -765,7 +607,7 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
   if (d->sparse_ok) {
     if (max_ntok > NT_STREAM) return qmoe::fail(QMOE_EUNSUPPORTED, "streaming path takes <= 2 tokens per unit");
     StreamParams P{};
-    P.gtab = pick_table(d, d_table, esz);
+    P.gtab = pick_table(d, d_table, 4);  // x is staged as fp32
     P.work = d_work;
     P.n_work = d_n_work;
     P.max_work = max_work;
@@ -775,7 +617,7 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
     P.y_mode = y_mode;
     P.ldy = ldy;
     P.bad = d_bad;
-    return launch_stream(d, P, esz, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
+    return launch_lean(d, P, esz, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
   }
   if (d_table) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
   GeneralParams G{};

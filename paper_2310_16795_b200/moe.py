@@ -28,13 +28,14 @@ from .codec import DeviceMatrix
 from .dictionary import Dictionary
 
 
-def _rows_per_unit(mats, target_cw: int = 4096) -> int:
+def _rows_per_unit(mats, target_cw: int = 3072) -> int:
+    """Rows per work unit: ~target_cw codewords (the streaming kernel stages
+    units of <= 4096 codewords and <= 128 rows; rows vary by ~+-30%)."""
     cw = sum(m.n_codewords for m in mats)
     rows = sum(m.rows for m in mats)
     per_row = max(1.0, cw / max(1, rows))
     r = int(target_cw / per_row)
-    r = max(4, min(r, mats[0].rows, 128))
-    return r
+    return max(1, min(r, mats[0].rows, 128))
 
 
 class CompressedMoELayer:
@@ -42,7 +43,7 @@ class CompressedMoELayer:
     all DeviceMatrix on one device."""
 
     def __init__(self, wi: list[DeviceMatrix], wo: list[DeviceMatrix], dic: Dictionary, max_tokens: int = 64,
-                 target_cw_per_unit: int = 2048, tokens_per_unit: int = 2, codebook: bool = True):
+                 target_cw_per_unit: int = 3072, tokens_per_unit: int = 2, codebook: bool = True):
         import torch
 
         if len(wi) != len(wo) or not wi:

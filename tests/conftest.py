@@ -71,3 +71,26 @@ def bf16_ulp_diff(a, b):
     ai = np.where(ai < 0, -(ai & 0x7FFFFFFF), ai)
     bi = np.where(bi < 0, -(bi & 0x7FFFFFFF), bi)
     return np.abs(ai - bi) >> 16
+
+
+def matvec_tolerance_ok(y, y_ref, abs_terms=None, nnz=None, min_identical=0.999):
+    """Matvec parity: per row |y - y_ref| <= 1 bf16 ulp of y_ref
+    plus the fp32 accumulation bound nnz * 2^-24 * sum_j |w_j x_j| (the
+    reference's own sgemv order is unspecified, so rows whose sum cancels can
+    legitimately round to a different bf16 value); >= min_identical of the
+    rows bit-identical. Returns (ok, message)."""
+    y = np.asarray(y, np.float64)
+    y_ref = np.asarray(y_ref, np.float64)
+    ulp = np.ldexp(1.0, np.floor(np.log2(np.maximum(np.abs(y_ref), 1e-38))).astype(int) - 7)
+    bound = ulp.copy()
+    if abs_terms is not None:
+        bound += np.asarray(nnz, np.float64) * 2.0**-24 * np.asarray(abs_terms, np.float64)
+    err = np.abs(y - y_ref)
+    bad = ~(err <= bound)
+    same = np.mean(y == y_ref) if len(y) else 1.0
+    if bad.any():
+        i = int(np.flatnonzero(bad)[0])
+        return False, f"{bad.sum()} rows out of tolerance, e.g. row {i}: {y[i]!r} vs {y_ref[i]!r} (bound {bound[i]:.3g})"
+    if same < min_identical:
+        return False, f"only {same:.4f} rows identical"
+    return True, ""
