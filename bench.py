@@ -120,6 +120,13 @@ def oracle_layer_sample(E, d_model, d_ff, T, seed, odic, experts_needed):
     return host
 
 
+def host_codewords(m) -> np.ndarray:
+    """The matrix's stream in dictionary order (undoes the device-private
+    frequency-codebook re-indexing) — what the reference codec would hold."""
+    cw = m.cw.cpu().numpy().view(np.uint16)
+    return m.codebook.order[cw] if m.codebook is not None else cw
+
+
 def run_oracle_steps(x_list, assign_list, host, odic, workers):
     """Composed CPU oracle MoE step(s); returns (seconds, bytes, tokens)."""
     from oracle import qmoe_oracle as O
@@ -410,7 +417,7 @@ def main():
                     continue
                 lay = layers[0]
                 host[int(e)] = tuple(
-                    (m.rows, m.cols, m.cw.cpu().numpy().view(np.uint16), m.row_off.cpu().numpy(),
+                    (m.rows, m.cols, host_codewords(m), m.row_off.cpu().numpy(),
                      m.row_minmax.cpu().numpy().view(np.uint16).reshape(m.rows, 2))
                     for m in (lay.wi[int(e)], lay.wo[int(e)]))
         sec, nbytes, ntok = run_oracle_steps([xs[b][:sample_T] for b in range(sample_steps)],

@@ -72,11 +72,14 @@ typedef struct qmoe_matrix {
   int32_t lg;
 } qmoe_matrix;
 
-/* One grouped work unit (self-contained, 80 bytes): rows [row0, row1) of the
- * matrix whose arrays are cw / row_off / row_minmax / ck (codewords [cw0, cw1)
- * = [row_off[row0], row_off[row1])), applied to `ntok` (<= 2 on the streaming
- * path) tokens. Token t reads x row tok[t] (x + tok[t] * ldx) and writes y row
- * tok[t] (y + tok[t] * ldy). Written by qmoe_moe_plan (or by the caller). */
+/* One RUN of a grouped launch (self-contained, 80 bytes): rows [row0, row1)
+ * of the matrix whose arrays are cw / row_off / row_minmax / ck (lg: 2^lg
+ * lanes per row, see qmoe_matrix), applied to `ntok` tokens (<= 2 on the
+ * streaming path). Token t reads x row tok[t] (x + tok[t] * ldx) and writes y
+ * row tok[t] (y + tok[t] * ldy). A run is cut into ceil(((row1 - row0) << lg)
+ * / 32) warp TASKS; task0 is the exclusive prefix of those counts over the
+ * list (the launch splits the global task range evenly over the SMs).
+ * Written by qmoe_moe_plan (or by the caller). */
 typedef struct qmoe_work {
   const uint16_t* cw;
   const int32_t* row_off;
@@ -85,11 +88,10 @@ typedef struct qmoe_work {
   int32_t cols;
   int32_t row0;
   int32_t row1;
-  int32_t ntok;
-  int32_t cw0;
-  int32_t cw1;
   int32_t lg;
-  int32_t pad_;
+  int32_t ntok;
+  int32_t task0;
+  int32_t pad_[2];
   int32_t tok[QMOE_NT_MAX];
 } qmoe_work;
 
@@ -146,8 +148,8 @@ int qmoe_decompress(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d
 
 /* fused_matvec (codec.py:209-244) for one matrix and one x vector.
  * d_x: cols values of type x_dtype; d_y: rows float32, updated in place.
- * Rows must have been validated (qmoe_validate_rows) — the kernel skips
- * writing rows whose lengths disagree and counts them in d_bad (nullable). */
+ * Rows must have been validated (qmoe_validate_rows): the sparse-path kernel
+ * trusts row lengths; d_bad (nullable) is used by the general path. */
 int qmoe_fused_matvec(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_row_off,
                       const uint32_t* d_row_minmax, int64_t rows, int64_t cols,
                       const void* d_x, int x_dtype, float* d_y, int32_t* d_bad, void* stream);
@@ -159,15 +161,18 @@ int qmoe_fused_matmat(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_r
                       const void* d_x, int x_dtype, int64_t ntok, int64_t ldx, float* d_y,
                       int64_t ldy, int32_t* d_bad, void* stream);
 
-/* Grouped persistent launch over device-resident work units: one kernel,
- * one dictionary-table fill, many (matrix, token) pairs. d_work/d_n_work
- * live in device memory (written e.g. by qmoe_moe_plan), so the call is
- * graph-capturable with no host synchronisation. max_ntok (<= QMOE_NT_MAX)
- * bounds work.ntok (sizes the x staging). y_mode: QMOE_Y_ACCUM_F32 or
+/* Grouped persistent launch over a device-resident run list: one kernel,
+ * one hot-table fill per SM, many (matrix, token) runs. d_n_work = int32[2]
+ * {number of runs, total tasks} lives in device memory (written e.g. by
+ * qmoe_moe_plan), so the call is graph-capturable with no host
+ * synchronisation. max_ntok (<= 2 on the sparse path) bounds work.ntok (sizes
+ * the x staging). y_mode: QMOE_Y_ACCUM_F32, QMOE_Y_STORE_F32 or
  * QMOE_Y_RELU_BF16 (fuses the FFN activation into the wi pass epilogue).
- * d_table: packed entry table the streams are indexed in — NULL for the
- * dictionary's own order, or a codebook from qmoe_codebook_table (streams
- * re-indexed with qmoe_remap). */
+ * d_table: entry table the streams are indexed in — NULL for the dictionary's
+ * own order, or a codebook from qmoe_codebook_table (streams re-indexed with
+ * qmoe_remap; the codebook must map dictionary entry 0 to rank 0). Rows must
+ * have been validated (qmoe_validate_rows); d_bad is used by the general
+ * (> 3 non-zero) path only. */
 int qmoe_grouped_matvec(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_work* d_work,
                         const int32_t* d_n_work, int32_t max_work, int32_t max_cols,
                         int32_t max_ntok, const void* d_x, int x_dtype, int64_t ldx, void* d_y,
@@ -228,19 +233,18 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
 /* ------------------------------------------------------------- MoE dispatch
  * Routed-expert dispatcher (pipeline.py:86-96 gather/scatter order): stable
  * counting sort of the top-1 assignment d_assign[T] into per-expert token
- * lists, then the work units of both FFN passes:
- *   pass 1 (wi, matrix 2e):   units over d_ff rows, tokens of expert e
- *   pass 2 (wo, matrix 2e+1): units over d_model rows, same tokens
- * Units hold up to tokens_per_unit (<= QMOE_NT_MAX) tokens and
- * `rows_per_unit_wi/_wo` rows; d_mats (2E matrices: wi_e = 2e, wo_e = 2e+1)
- * supplies row_off so each unit carries its codeword range.
- * d_units_wi/_wo must hold max_units entries; counts go to d_n_units[2].
- * d_expert_count (int32[E]) and d_order (int32[T]) are outputs too. */
+ * lists (d_order, int32[T], expert-major, buffer order within an expert;
+ * d_expert_count int32[E]), then the run lists of both FFN passes: one run
+ * per (expert, chunk of <= tokens_per_run tokens) covering all rows of
+ *   pass 1: wi_e = d_mats[2e]      (d_runs_wi)
+ *   pass 2: wo_e = d_mats[2e + 1]  (d_runs_wo)
+ * with task0 prefixes filled. d_runs_* hold max_runs (>= T) records;
+ * d_n = int32[4] {runs wi, tasks wi, runs wo, tasks wo}. Ids outside
+ * [0, E) are dropped (the token gets no expert output). */
 int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats,
-                  int32_t rows_wi, int32_t rows_wo, int32_t rows_per_unit_wi,
-                  int32_t rows_per_unit_wo, int32_t tokens_per_unit, int32_t max_work,
-                  qmoe_work* d_work_wi, qmoe_work* d_work_wo, int32_t* d_n_work,
-                  int32_t* d_expert_count, int32_t* d_order, void* stream);
+                  int32_t tokens_per_run, int32_t max_runs, qmoe_work* d_runs_wi,
+                  qmoe_work* d_runs_wo, int32_t* d_n, int32_t* d_expert_count, int32_t* d_order,
+                  void* stream);
 
 #ifdef __cplusplus
 }

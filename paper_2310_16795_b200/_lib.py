@@ -43,7 +43,7 @@ class QmoeMatrix(ctypes.Structure):
 
 class QmoeWork(ctypes.Structure):
     _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("ck", vp), ("cols", i32), ("row0", i32),
-                ("row1", i32), ("ntok", i32), ("cw0", i32), ("cw1", i32), ("lg", i32), ("pad_", i32),
+                ("row1", i32), ("lg", i32), ("ntok", i32), ("task0", i32), ("pad_", i32 * 2),
                 ("tok", i32 * NT_MAX)]
 
 
@@ -51,7 +51,7 @@ QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16, QMOE_Y_STORE_F32 = 0, 1, 2
 
 
 WORK_BYTES = ctypes.sizeof(QmoeWork)
-NT_STREAM = 2  # tokens per work unit on the streaming (sparse-table) path
+NT_STREAM = 2  # tokens per run on the streaming (sparse-table) path
 MATRIX_BYTES = ctypes.sizeof(QmoeMatrix)
 
 _SIGS = {
@@ -78,7 +78,7 @@ _SIGS = {
     "qmoe_encode_emit": (ctypes.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "qmoe_exclusive_scan": (ctypes.c_int, [vp, i64, vp, vp]),
     "qmoe_rtn_quantize": (ctypes.c_int, [vp, i64, i64, vp, vp, vp, vp]),
-    "qmoe_moe_plan": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "qmoe_moe_plan": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -41,7 +41,12 @@ class Codebook:
                 raise ValueError("matrix already re-indexed")
             _lib.check(_lib.lib.qmoe_histogram(_lib.ptr(m.cw), m.n_codewords, _lib.ptr(counts), sp))
         c = counts.cpu().numpy().view(np.uint32).astype(np.int64)
-        self.order = np.argsort(-c, kind="stable").astype(np.uint16)  # rank -> codeword
+        # rank -> codeword by descending frequency, with dictionary entry 0 (one
+        # zero pair, no non-zero value) pinned to rank 0: the streaming kernel
+        # decodes the masked codewords of a partial group as rank 0
+        c0 = c.copy()
+        c0[0] = np.iinfo(np.int64).max
+        self.order = np.argsort(-c0, kind="stable").astype(np.uint16)
         self.rank_of = np.empty(DICT_SIZE, np.uint16)
         self.rank_of[self.order] = np.arange(DICT_SIZE, dtype=np.uint16)
         self.counts = c

@@ -134,11 +134,13 @@ class DeviceMatrix:
     def build_checkpoints(self, dic: Dictionary, lg: int | None = None) -> None:
         """Kernel-private row-segment checkpoints (qmoe_checkpoints): the column
         at which each of the G = 2^lg segments of every row starts, so G lanes
-        walk one row independently. lg=None picks ~48 codewords per segment."""
+        walk one row independently. lg=None picks <= ~48 codewords per segment."""
         torch = _torch()
-        if lg is None:
+        if lg is None:  # G = 2^lg lanes per row, ~24-48 codewords per lane segment
             avg = self.mean_codewords_per_row()
-            lg = 0 if avg <= 48 else (1 if avg <= 96 else 2)  # G <= 4 (MAX_CK = 3 on the fast path)
+            lg = 0
+            while lg < 3 and avg / (1 << lg) > 48:
+                lg += 1
         self.lg = int(lg)
         if self.lg == 0 or self.rows == 0:
             self.ck = None

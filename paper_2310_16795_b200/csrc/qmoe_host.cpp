@@ -178,23 +178,40 @@ int derive_tables(const uint32_t* words, uint32_t* sparse_tab, uint8_t* len_tab,
 }
 
 int derive_matvec_tables(const uint32_t* sparse_tab, uint32_t* mtab) {
-  for (int v = 0; v < 2; ++v) {
-    const uint32_t esz = v == 0 ? 4u : 2u;
-    uint32_t* t = mtab + size_t(v) * MT_STRIDE;
-    for (int i = 0; i < QMOE_DICT_SIZE; ++i) {
-      const uint32_t e = sparse_tab[i];
-      uint32_t m = e & 31u;
-      for (int j = 0; j < 3; ++j) {
-        const uint32_t b = (e >> (8 * (j + 1))) & 0xFFu;
-        if (!b) continue;
-        m |= ((b >> 2) * esz) << (5 + 7 * j);
-        m |= 1u << (26 + j);
-        if (b & 2u) m |= 1u << (29 + j);
-      }
-      t[i] = m;
+  // variant 0: packed-field format (decompress / checkpoints)
+  uint32_t* t = mtab;
+  for (int i = 0; i < QMOE_DICT_SIZE; ++i) {
+    const uint32_t e = sparse_tab[i];
+    uint32_t m = e & 31u;
+    for (int j = 0; j < 3; ++j) {
+      const uint32_t b = (e >> (8 * (j + 1))) & 0xFFu;
+      if (!b) continue;
+      m |= ((b >> 2) * 4u) << (5 + 7 * j);
+      m |= 1u << (26 + j);
+      if (b & 2u) m |= 1u << (29 + j);
     }
-    for (int i = QMOE_DICT_SIZE; i < MT_STRIDE; ++i) t[i] = 0;
+    t[i] = m;
   }
+  for (int i = QMOE_DICT_SIZE; i < MT_STRIDE; ++i) t[i] = 0;
+  // variant 1: byte-field "segment" format of the streaming matvec: byte j
+  // (j = 0..2) = 4 * position of non-zero j (0x7F: slot unused), bits 24-26
+  // = non-zero j is code 2 (row max), bits 28-31 = n (pairs; 2n values).
+  t = mtab + MT_STRIDE;
+  for (int i = 0; i < QMOE_DICT_SIZE; ++i) {
+    const uint32_t e = sparse_tab[i];
+    uint32_t m = ((e & 31u) >> 1) << 28;
+    for (int j = 0; j < 3; ++j) {
+      const uint32_t b = (e >> (8 * (j + 1))) & 0xFFu;
+      if (!b) {
+        m |= 0x7Fu << (8 * j);
+        continue;
+      }
+      m |= ((b >> 2) * 4u) << (8 * j);
+      if (b & 2u) m |= 1u << (24 + j);
+    }
+    t[i] = m;
+  }
+  for (int i = QMOE_DICT_SIZE; i < MT_STRIDE; ++i) t[i] = 0x007F7F7Fu;
   return QMOE_OK;
 }
 

@@ -19,13 +19,14 @@ int build_trie(const uint32_t* words, int32_t* next_node, int32_t* entry_of_node
 //  len_tab[e]:    2n
 int derive_tables(const uint32_t* words, uint32_t* sparse_tab, uint8_t* len_tab, int* max_nz);
 
-// Matvec-format tables (see qmoe_matvec.cu header), two variants back to back
-// for staged x of 4-byte and 2-byte elements, each MT_STRIDE entries with zero
-// entries from index 65536 (the kernels' padding sentinel):
-//   bits 0-4 len = 2n | bits 5-11/12-18/19-25 position*esz of non-zero 0..2 |
-//   bits 26-28 used | bits 29-31 code 2. Valid when max_nz <= 3.
-// Variant stride: 65540 entries so the second variant starts 16-byte aligned
-// (it is the source of a cp.async.bulk copy).
+// Matvec-format tables, two variants back to back, MT_STRIDE entries each
+// (entries from 65536 are padding). Valid when max_nz <= 3.
+//   variant 0 (packed fields; decompress, checkpoints): bits 0-4 len = 2n |
+//     bits 5-11/12-18/19-25 4*position of non-zero 0..2 | bits 26-28 used |
+//     bits 29-31 code 2.
+//   variant 1 (byte fields; streaming matvec): byte j = 4*position of
+//     non-zero j or 0x7F (unused) | bits 24-26 code 2 | bits 28-31 n.
+// Stride 65540 keeps the second variant 16-byte aligned.
 constexpr int MT_STRIDE = 65540;
 int derive_matvec_tables(const uint32_t* sparse_tab, uint32_t* mtab /* 2 * MT_STRIDE */);
 

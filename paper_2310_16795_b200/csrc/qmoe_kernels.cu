@@ -342,39 +342,107 @@ __global__ void rtn_kernel(const float* __restrict__ w, int64_t rows, int64_t co
 
 // ================================================================ MoE planner
 // Routed-expert dispatcher: stable counting sort of top-1 assignments (token
-// order within an expert = buffer order, pipeline.py:86-90) and emission of
-// the grouped work units of the wi and wo passes. One CTA. Each unit carries
-// its codeword range (read from the matrix's row_off) so the matvec kernel's
-// producer can stream it without a dependent load.
+// order within an expert = buffer order, pipeline.py:86-90) and the run lists
+// of the wi and wo passes (one run per expert token chunk, all rows). One CTA
+// of 1024 threads; per-expert prefixes by a block scan, so the cost is
+// O(E/1024 + T/32) steps.
+__device__ __forceinline__ int run_tasks_dev(int rows, int lg) { return ((rows << lg) + 31) >> 5; }
+
+__device__ __forceinline__ int4 block_scan_excl(int4 v, int4* wsum, int4* total) {
+  // exclusive scan of int4 values over the 1024 threads (thread order)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4 incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int4 o;
+    o.x = __shfl_up_sync(FULL_MASK, incl.x, d);
+    o.y = __shfl_up_sync(FULL_MASK, incl.y, d);
+    o.z = __shfl_up_sync(FULL_MASK, incl.z, d);
+    o.w = __shfl_up_sync(FULL_MASK, incl.w, d);
+    if (lane >= d) {
+      incl.x += o.x;
+      incl.y += o.y;
+      incl.z += o.z;
+      incl.w += o.w;
+    }
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int4 w = wsum[lane];
+    int4 wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int4 o;
+      o.x = __shfl_up_sync(FULL_MASK, wi.x, d);
+      o.y = __shfl_up_sync(FULL_MASK, wi.y, d);
+      o.z = __shfl_up_sync(FULL_MASK, wi.z, d);
+      o.w = __shfl_up_sync(FULL_MASK, wi.w, d);
+      if (lane >= d) {
+        wi.x += o.x;
+        wi.y += o.y;
+        wi.z += o.z;
+        wi.w += o.w;
+      }
+    }
+    wsum[lane] = make_int4(wi.x - w.x, wi.y - w.y, wi.z - w.z, wi.w - w.w);
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  const int4 b = wsum[warp];
+  return make_int4(b.x + incl.x - v.x, b.y + incl.y - v.y, b.z + incl.z - v.z, b.w + incl.w - v.w);
+}
+
 __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restrict__ assign, int T, int E,
-                                                        const qmoe_matrix* __restrict__ mats, int rows_wi,
-                                                        int rows_wo, int rpu_wi, int rpu_wo, int ntu, int max_units,
-                                                        qmoe_work* units_wi, qmoe_work* units_wo, int32_t* n_units,
+                                                        const qmoe_matrix* __restrict__ mats, int ntu, int max_runs,
+                                                        qmoe_work* runs_wi, qmoe_work* runs_wo, int32_t* n_out,
                                                         int32_t* cnt_out, int32_t* order) {
   extern __shared__ int32_t sh[];
-  int32_t* cnt = sh;            // E
-  int32_t* start = sh + E;      // E
-  int32_t* fill = sh + 2 * E;   // E
-  int32_t* choff = sh + 3 * E;  // E + 1: token chunks before expert e
-  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = fill[e] = 0;
+  int32_t* cnt = sh;             // E: tokens per expert (then fill cursor)
+  int32_t* start = sh + E;       // E: first slot of expert e in order[]
+  int32_t* choff = sh + 2 * E;   // E + 1: token chunks before expert e
+  int32_t* twi = sh + 3 * E + 1; // E: wi tasks before expert e
+  int32_t* two = sh + 4 * E + 1; // E: wo tasks before expert e
+  __shared__ int4 wsum[32];
+  __shared__ int4 total;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
   __syncthreads();
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     const int e = assign[t];
     if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int a = 0, c = 0;
-    for (int e = 0; e < E; ++e) {
-      start[e] = a;
-      a += cnt[e];
-      choff[e] = c;
-      c += (cnt[e] + ntu - 1) / ntu;
+  // per-thread contiguous expert slice, block scan of (tokens, chunks, wi tasks, wo tasks)
+  const int per = (E + blockDim.x - 1) / blockDim.x;
+  const int e0 = min(E, (int)threadIdx.x * per), e1 = min(E, e0 + per);
+  int4 loc = make_int4(0, 0, 0, 0);
+  for (int e = e0; e < e1; ++e) {
+    const int c = cnt[e], nch = (c + ntu - 1) / ntu;
+    loc.x += c;
+    loc.y += nch;
+    if (nch) {
+      loc.z += nch * run_tasks_dev(mats[2 * e].rows, mats[2 * e].lg);
+      loc.w += nch * run_tasks_dev(mats[2 * e + 1].rows, mats[2 * e + 1].lg);
     }
-    choff[E] = c;
   }
+  int4 base = block_scan_excl(loc, wsum, &total);
+  for (int e = e0; e < e1; ++e) {
+    const int c = cnt[e], nch = (c + ntu - 1) / ntu;
+    start[e] = base.x;
+    choff[e] = base.y;
+    twi[e] = base.z;
+    two[e] = base.w;
+    base.x += c;
+    base.y += nch;
+    if (nch) {
+      base.z += nch * run_tasks_dev(mats[2 * e].rows, mats[2 * e].lg);
+      base.w += nch * run_tasks_dev(mats[2 * e + 1].rows, mats[2 * e + 1].lg);
+    }
+    cnt_out[e] = c;
+    cnt[e] = 0;  // becomes the fill cursor
+  }
+  if (threadIdx.x == 0) choff[E] = total.y;
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt_out[e] = cnt[e];
   // stable placement, one warp walking the tokens in buffer order
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -387,8 +455,8 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
       const int leader = __ffs(peers) - 1;
       int basev = 0;
       if (ok && lane == leader) {
-        basev = fill[e];
-        fill[e] = basev + __popc(peers);
+        basev = cnt[e];
+        cnt[e] = basev + __popc(peers);
       }
       basev = __shfl_sync(FULL_MASK, basev, leader);
       if (ok) order[start[e] + basev + rank] = t;
@@ -396,49 +464,39 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     }
   }
   __syncthreads();
-  // units: expert-major, then token chunk, then row block (consecutive units
-  // of one CTA then share their x rows)
-  const int nblk_wi = (rows_wi + rpu_wi - 1) / rpu_wi;
-  const int nblk_wo = (rows_wo + rpu_wo - 1) / rpu_wo;
-  const int nchunks = choff[E];
-  const int total = nchunks * (nblk_wi + nblk_wo);
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const bool is_wi = i < nchunks * nblk_wi;
-    const int j = is_wi ? i : i - nchunks * nblk_wi;
-    const int nblk = is_wi ? nblk_wi : nblk_wo;
-    const int chunk = j / nblk, blk = j % nblk;
-    if (j >= max_units) continue;
-    // expert owning this chunk: binary search over choff
-    int lo = 0, hi = E - 1;
+  const int nchunks = min(choff[E], max_runs);
+  for (int i = threadIdx.x; i < nchunks; i += blockDim.x) {
+    int lo = 0, hi = E - 1;  // expert owning chunk i: last e with choff[e] <= i
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (choff[mid] <= chunk) lo = mid;
+      if (choff[mid] <= i) lo = mid;
       else hi = mid - 1;
     }
-    const int e = lo;
-    const int ch = chunk - choff[e];
+    const int e = lo, ch = i - choff[e];
+    const int c = cnt[e];  // == tokens of e after placement
     qmoe_work U;
-    U.ntok = min(ntu, cnt[e] - ch * ntu);
+    U.ntok = min(ntu, c - ch * ntu);
     for (int q = 0; q < QMOE_NT_MAX; ++q) U.tok[q] = order[start[e] + ch * ntu + min(q, U.ntok - 1)];
-    const qmoe_matrix M = mats[2 * e + (is_wi ? 0 : 1)];
-    const int rows = is_wi ? rows_wi : rows_wo, rpu = is_wi ? rpu_wi : rpu_wo;
-    U.cw = M.cw;
-    U.row_off = M.row_off;
-    U.row_minmax = M.row_minmax;
-    U.ck = M.ck;
-    U.lg = M.lg;
-    U.pad_ = 0;
-    U.cols = M.cols;
-    U.row0 = blk * rpu;
-    U.row1 = min(rows, U.row0 + rpu);
-    U.cw0 = M.row_off[U.row0];
-    U.cw1 = M.row_off[U.row1];
-    (is_wi ? units_wi : units_wo)[j] = U;
+    U.pad_[0] = U.pad_[1] = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const qmoe_matrix M = mats[2 * e + pass];
+      U.cw = M.cw;
+      U.row_off = M.row_off;
+      U.row_minmax = M.row_minmax;
+      U.ck = M.ck;
+      U.lg = M.lg;
+      U.cols = M.cols;
+      U.row0 = 0;
+      U.row1 = M.rows;
+      U.task0 = (pass ? two[e] : twi[e]) + ch * run_tasks_dev(M.rows, M.lg);
+      (pass ? runs_wo : runs_wi)[i] = U;
+    }
   }
   if (threadIdx.x == 0) {
-    n_units[0] = min(nchunks * nblk_wi, max_units);
-    n_units[1] = min(nchunks * nblk_wo, max_units);
-    n_units[2] = (nchunks * nblk_wi > max_units || nchunks * nblk_wo > max_units) ? 1 : 0;  // overflow flag
+    n_out[0] = nchunks;
+    n_out[1] = choff[E] <= max_runs ? total.z : (nchunks ? 0 : 0);
+    n_out[2] = nchunks;
+    n_out[3] = choff[E] <= max_runs ? total.w : 0;
   }
 }
 
@@ -638,19 +696,16 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
   return QMOE_OK;
 }
 
-int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats, int32_t rows_wi,
-                  int32_t rows_wo, int32_t rpu_wi, int32_t rpu_wo, int32_t ntu, int32_t max_units,
-                  qmoe_work* d_units_wi, qmoe_work* d_units_wo, int32_t* d_n_units, int32_t* d_expert_count,
-                  int32_t* d_order, void* stream) {
-  if (T < 0 || E < 1 || !d_mats || rows_wi < 1 || rows_wo < 1 || rpu_wi < 1 || rpu_wo < 1 || max_units < 0 ||
-      ntu < 1 || ntu > QMOE_NT_MAX)
-    return qmoe::fail(QMOE_EINVAL, "bad argument");
-  const size_t smem = (size_t)(4 * E + 1) * 4;
+int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats, int32_t ntu,
+                  int32_t max_runs, qmoe_work* d_runs_wi, qmoe_work* d_runs_wo, int32_t* d_n,
+                  int32_t* d_expert_count, int32_t* d_order, void* stream) {
+  if (T < 0 || E < 1 || !d_mats || max_runs < T || ntu < 1 || ntu > QMOE_NT_MAX || !d_n)
+    return qmoe::fail(QMOE_EINVAL, "bad argument (max_runs must be >= T)");
+  const size_t smem = (size_t)(5 * E + 1) * 4;
   if (smem > 200 * 1024) return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts");
   CK(cudaFuncSetAttribute(moe_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-  moe_plan_kernel<<<1, 1024, smem, S(stream)>>>(d_assign, T, E, d_mats, rows_wi, rows_wo, rpu_wi, rpu_wo, ntu,
-                                                 max_units, d_units_wi, d_units_wo, d_n_units, d_expert_count,
-                                                 d_order);
+  moe_plan_kernel<<<1, 1024, smem, S(stream)>>>(d_assign, T, E, d_mats, ntu, max_runs, d_runs_wi, d_runs_wo, d_n,
+                                                 d_expert_count, d_order);
   CK(cudaGetLastError(), "moe_plan_kernel");
   return QMOE_OK;
 }

@@ -1,26 +1,34 @@
 // Fused dictionary-decode + matvec (codec.py:196-244 semantics) for sm_100a.
 //
-// lean_matvec_kernel — the product path for dictionaries whose entries hold
-// <= 3 non-zero values (the default p0 = 0.885 dictionary):
-//   * persistent, one CTA per SM; the CTA takes a contiguous slice of the work
-//     list and merges consecutive units that share their x rows (they are row
-//     blocks of one matrix for one token chunk — qmoe_moe_plan's order) into
-//     one RUN: x is staged once per run, then the 16 warps stride over the
-//     run's row tasks with no further CTA synchronisation;
-//   * the hot prefix of the packed entry table (a frequency codebook in the
-//     MoE layer) is staged in shared memory once per launch;
-//   * a task is 32 / G rows: each lane owns one contiguous SEGMENT of a row
-//     (G = 2^lg segments, lg from the matrix's checkpoints; lg = 0: a lane per
-//     row) and walks it with a running column offset starting at the row's
-//     checkpoint — no scans. Codewords stream from HBM in sector-aligned
-//     16-codeword groups (2 x 16-byte loads bypassing L1), group g+2 loaded,
-//     g+1 looked up and g applied per iteration; the next task's row
-//     metadata is prefetched while the current task runs;
-//   * per non-zero slot acc += level(code) * x[col] in fp32; the row's sum is
-//     reduced over its G lanes and bf16-rounded once (codec.py:243).
-// Entry format "matvec" (qmoe_host.cpp, esz = bytes per staged x element):
-//   bits 0-4 len = 2n | bits 5-11, 12-18, 19-25: position * esz of non-zero
-//   slot 0..2 | bits 26-28 slot used | bits 29-31 slot is code 2 (row max).
+// seg_matvec_kernel — the product path for dictionaries whose entries hold
+// <= 3 non-zero values (the default p0 = 0.885 dictionary).
+//
+//   Work.  A launch walks a list of RUNS (qmoe_work): rows [row0, row1) of one
+//   compressed matrix applied to 1..2 tokens. A run is cut into TASKS of one
+//   warp each: 32 lanes = 32/G rows x G row SEGMENTS (G = 2^lg from the
+//   matrix's checkpoints; segment j of a row = codewords [s + j*n/G,
+//   s + (j+1)*n/G) starting at column ck[j]). The persistent grid (one
+//   1024-thread CTA per SM) splits the global task range evenly; a CTA stages
+//   the x rows of each run it touches once in shared memory (fp32; two tokens
+//   interleaved as float2) and its 32 warps stride over that run's tasks.
+//   Row metadata is read per lane; row sums are reduced over the G lanes of a
+//   row with shuffles (fixed order, deterministic) and bf16-rounded once
+//   (codec.py:243).
+//
+//   Stream.  Each lane reads its segment in aligned 8-codeword (16-byte)
+//   groups with ld.global.nc.L1::no_allocate, two groups ahead of use.
+//   Codewords of a group outside the lane's segment are replaced by codeword
+//   0, whose entry (dictionary entry 0 = one zero pair; codebooks pin it to
+//   rank 0) has no non-zero value: the segment start column is pre-shifted by
+//   2 per masked leading codeword, masked trailing codewords add nothing.
+//
+//   Decode.  The entry table (variant 1 of the matvec tables, qmoe_internal.h)
+//   is byte-addressable: byte j = 4 * position of non-zero j (0x7F unused),
+//   bits 24-26 = "code 2" flags, bits 28-31 = n pairs. Per codeword: one
+//   table lookup (hot prefix [0, H) in shared memory — a frequency codebook
+//   puts the most used entries there — else the L2-resident global table),
+//   and per used slot one shared-memory x load at byte offset off*4 + byte j
+//   and one FMA with the row's bf16 min or max level.
 //
 // general_matvec_kernel — any dictionary (e.g. p0 = 0.7, up to 6 non-zeros per
 // entry): expands the two decode words value by value (dictionary.py:115-120).
@@ -33,346 +41,273 @@ using namespace qmoe_dev;
 
 namespace {
 
-#ifndef QMOE_LEAN_THREADS
-#define QMOE_LEAN_THREADS 512
-#endif
-constexpr int THREADS = QMOE_LEAN_THREADS;
+constexpr int THREADS = 1024;
 constexpr int NWARPS = THREADS / 32;
-constexpr int GRP = 16;                // codewords per aligned 32-byte group
-constexpr int NT_STREAM = 2;           // tokens per unit on the streaming path
-constexpr int MAX_LG = 2;              // G <= 4 lanes per row on the fast path
+constexpr int GRP = 8;          // codewords per 16-byte group
+constexpr int NT_STREAM = 2;    // tokens per run on the streaming path
 
-template <int ESZ>
-struct XType;
-template <>
-struct XType<4> {
-  using T = float;
-  static __device__ __forceinline__ float get(float v) { return v; }
-};
-template <>
-struct XType<2> {
-  using T = uint16_t;
-  static __device__ __forceinline__ float get(uint16_t v) { return __uint_as_float(uint32_t(v) << 16); }
-};
-
-struct Rec {  // == qmoe_work (80 bytes)
-  const uint16_t* cw;
-  const int32_t* ro;
-  const uint32_t* mm;
-  const uint16_t* ck;
-  int32_t cols, row0, row1, ntok, cw0, cw1, lg, pad;
-  int32_t tok[QMOE_NT_MAX];
-};
-static_assert(sizeof(Rec) == sizeof(qmoe_work), "record layout");
-
-struct StreamParams {
-  const uint32_t* gtab;       // matvec-format table variant (zero entries from 65536)
+struct SegParams {
+  const uint32_t* gtab;       // byte-field entry table (variant 1), 65536 entries
   int H;                      // entries staged in shared memory
-  const qmoe_work* work;      // explicit work list (or nullptr: implicit single matrix)
-  const int32_t* n_work;
-  int max_work;
-  qmoe_matrix single;         // implicit mode (lane per row, no checkpoints)
-  int rows_per_unit;
+  int z_bytes;                // 4 * (values of entry 0): start shift per masked leading codeword
+  const qmoe_work* runs;      // explicit run list, or nullptr: implicit single matrix
+  const int32_t* n_runs;      // {n_runs, total_tasks}
+  int max_runs;
+  qmoe_matrix single;         // implicit mode: one run per token chunk, lane per row
   int64_t ntok_single;
-  int ntu_single;
   const void* x;
+  int x_bf16;
   int64_t ldx;
   void* y;
   int y_mode;
   int64_t ldy;
-  int32_t* bad;
-  int xcap;                   // elements per token slot of the x buffer
-  int ntmax;                  // token slots
+  int xcap;                   // x elements staged per token
 };
 
-__device__ __forceinline__ void make_rec(const StreamParams& P, int u, Rec& R) {
-  if (P.work) {
-    const uint4* s = reinterpret_cast<const uint4*>(P.work + u);
-    uint4* d = reinterpret_cast<uint4*>(&R);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) d[i] = __ldg(s + i);
+struct Run {
+  const uint16_t* cw;
+  const int32_t* ro;
+  const uint32_t* mm;
+  const uint16_t* ck;
+  int cols, row0, row1, lg, ntok, task0;
+  int tok[NT_STREAM];
+};
+
+__device__ __forceinline__ int run_tasks(int rows, int lg) { return ((rows << lg) + 31) >> 5; }
+
+__device__ __forceinline__ Run get_run(const SegParams& P, int r) {
+  Run R;
+  if (P.runs) {
+    const qmoe_work& W = P.runs[r];
+    R.cw = W.cw;
+    R.ro = W.row_off;
+    R.mm = W.row_minmax;
+    R.ck = W.ck;
+    R.cols = W.cols;
+    R.row0 = W.row0;
+    R.row1 = W.row1;
+    R.lg = W.lg;
+    R.ntok = W.ntok;
+    R.task0 = W.task0;
+    R.tok[0] = W.tok[0];
+    R.tok[1] = W.tok[W.ntok > 1 ? 1 : 0];
   } else {
-    const int nblk = (P.single.rows + P.rows_per_unit - 1) / P.rows_per_unit;
-    const int chunk = u / nblk, blk = u % nblk;
     R.cw = P.single.cw;
     R.ro = P.single.row_off;
     R.mm = P.single.row_minmax;
     R.ck = nullptr;
     R.cols = P.single.cols;
+    R.row0 = 0;
+    R.row1 = P.single.rows;
     R.lg = 0;
-    R.pad = 0;
-    R.row0 = blk * P.rows_per_unit;
-    R.row1 = min(P.single.rows, R.row0 + P.rows_per_unit);
-    const int64_t t0 = (int64_t)chunk * P.ntu_single;
-    R.ntok = (int)min((int64_t)P.ntu_single, P.ntok_single - t0);
-#pragma unroll
-    for (int q = 0; q < QMOE_NT_MAX; ++q) R.tok[q] = (int)(t0 + min(q, R.ntok - 1));
-    R.cw0 = 0;
-    R.cw1 = 0;
+    const int64_t t0 = (int64_t)r * NT_STREAM;
+    R.ntok = (int)min((int64_t)NT_STREAM, P.ntok_single - t0);
+    R.task0 = r * run_tasks(P.single.rows, 0);
+    R.tok[0] = (int)t0;
+    R.tok[1] = (int)(t0 + (R.ntok > 1 ? 1 : 0));
   }
+  return R;
 }
 
-// same matrix, contiguous rows and same tokens: the units merge into one run
-__device__ __forceinline__ bool continues(const Rec& a, const Rec& b) {
-  bool s = a.cw == b.cw && a.row1 == b.row0 && a.ntok == b.ntok && a.lg == b.lg;
-#pragma unroll
-  for (int q = 0; q < QMOE_NT_MAX; ++q) s = s && (q >= a.ntok || a.tok[q] == b.tok[q]);
-  return s;
-}
-
-__device__ __forceinline__ void ld_group(const uint16_t* cw, int64_t g, uint4& a, uint4& b) {
-  const uint4* p = reinterpret_cast<const uint4*>(cw + g * GRP);
+__device__ __forceinline__ uint4 ld_group(const uint16_t* cw, int g) {
+  uint4 a;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
-               : "l"(p));
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-               : "l"(p + 1));
+               : "l"(cw + (size_t)g * GRP));
+  return a;
 }
 
-// entries of the 16 codewords of a group; positions outside the lane's
-// segment (mask bit clear) get the zero entry
-__device__ __forceinline__ void lookup_group(uint32_t (&t)[GRP], const uint4& a, const uint4& b, uint32_t mask,
-                                             const uint32_t* tab, uint32_t H, const uint32_t* __restrict__ gtab) {
-  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-  for (int u = 0; u < GRP; ++u) {
-    const uint32_t c = (u & 1) ? (w[u >> 1] >> 16) : (w[u >> 1] & 0xFFFFu);
-    const uint32_t e = c < H ? tab[c] : __ldg(gtab + c);
-    t[u] = ((mask >> u) & 1u) ? e : 0u;
-  }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
 }
 
-template <int NT, int ESZ>
-__device__ __forceinline__ void apply_group(const uint32_t (&t)[GRP], const typename XType<ESZ>::T* xs, int xslot,
-                                            int& off, float lmin, float lmax, float (&acc)[NT]) {
-  using XT = typename XType<ESZ>::T;
+// One group of 8 codewords: lookup + per-slot gather/FMA. MASKED: vm bit u
+// set = codeword u belongs to the lane's segment (others decode as entry 0).
+// xsb: shared address of the staged x plus the running byte offset is `offb`.
+template <int NT, bool MASKED>
+__device__ __forceinline__ void apply_group(const uint4 q, uint32_t vm, uint32_t tab_s, uint32_t H,
+                                            const uint32_t* __restrict__ gtab, uint32_t& xa, float lmin,
+                                            float lmax, float (&acc)[3][NT]) {
+  // xa = shared address of x[column of the next codeword] (NT == 2: of the
+  // interleaved float2 pair, 8 bytes per column; fields are 4 * position)
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
   for (int u = 0; u < GRP; ++u) {
-    const uint32_t e = t[u];
-    const char* xo = reinterpret_cast<const char*>(xs + off);
+    uint32_t c = (u & 1) ? (w[u >> 1] >> 16) : (w[u >> 1] & 0xFFFFu);
+    if (MASKED) c = ((vm >> u) & 1u) ? c : 0u;
+    const uint32_t e = c < H ? lds_u32(tab_s + 4 * c) : __ldg(gtab + c);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const bool used = (e >> (26 + j)) & 1u;
-      const float w = ((e >> (29 + j)) & 1u) ? lmax : lmin;
-      const XT* xp = reinterpret_cast<const XT*>(xo + ((e >> (5 + 7 * j)) & 0x7Fu));
-#pragma unroll
-      for (int q = 0; q < NT; ++q) {
-        const float v = used ? XType<ESZ>::get(xp[q * xslot]) : 0.f;
-        acc[q] = fmaf(w, v, acc[q]);
+      const uint32_t f = __byte_perm(e, 0u, 0x4440u + j);
+      const float wv = ((e >> (24 + j)) & 1u) ? lmax : lmin;
+      if (f != 0x7Fu) {
+        if (NT == 1) {
+          const float xv = lds_f32(xa + f);
+          acc[j][0] = fmaf(wv, xv, acc[j][0]);
+        } else {
+          const float2 xv = lds_f32x2(xa + 2 * f);
+          acc[j][0] = fmaf(wv, xv.x, acc[j][0]);
+          acc[j][1] = fmaf(wv, xv.y, acc[j][1]);
+        }
       }
     }
-    off += int(e & 31u);
+    xa += (e >> 28) << (NT == 1 ? 3 : 4);  // 2n columns
   }
 }
 
-__device__ __forceinline__ uint32_t group_mask(int64_t g, int64_t A, int64_t B) {
-  const int64_t base = g * GRP;
-  const int lo = (int)max((int64_t)0, min((int64_t)GRP, A - base));
-  const int hi = (int)max((int64_t)0, min((int64_t)GRP, B - base));
-  return ((1u << hi) - 1u) & ~((1u << lo) - 1u);
-}
-
-// row metadata of one lane's segment
-struct Seg {
-  int64_t A, B;  // codeword range
-  int off;       // starting column
-  uint32_t mm;   // bf16 (min, max)
-  int row;       // absolute row, or -1
-};
-
-__device__ __forceinline__ Seg load_seg(const Rec& R, int task, int lg, int rb) {
-  Seg sg{0, 0, 0, 0u, -1};
+template <int NT>
+__device__ __forceinline__ void run_task(const SegParams& P, const Run& R, int task, uint32_t xs_s, uint32_t tab_s) {
   const int lane = threadIdx.x & 31;
-  const int G = 1 << lg;
+  const int lg = R.lg, G = 1 << lg;
   const int r = R.row0 + (task << (5 - lg)) + (lane >> lg);
-  if (r < rb) {
-    const int seg = lane & (G - 1);
+  const int seg = lane & (G - 1);
+  int A = 0, B = 0, off = 0;
+  uint32_t mm = 0;
+  if (r < R.row1) {
     const int s = __ldg(R.ro + r), e = __ldg(R.ro + r + 1);
     const int n = e - s;
-    sg.A = s + ((seg * n) >> lg);
-    sg.B = s + (((seg + 1) * n) >> lg);
-    sg.off = seg ? (int)__ldg(R.ck + (size_t)r * (G - 1) + seg - 1) : 0;
-    sg.mm = __ldg(R.mm + r);
-    sg.row = r;
+    A = s + ((seg * n) >> lg);
+    B = s + (((seg + 1) * n) >> lg);
+    off = seg ? (int)__ldg(R.ck + (size_t)r * (G - 1) + seg - 1) : 0;
+    mm = __ldg(R.mm + r);
   }
-  return sg;
-}
-
-template <int NT, int ESZ>
-__device__ __forceinline__ void run_task(const StreamParams& P, const Rec& R, const Seg& sg, int lg, const int (&tok)[NT],
-                                         const typename XType<ESZ>::T* xs, const uint32_t* tab) {
-  const int lane = threadIdx.x & 31;
-  const int G = 1 << lg;
+  const bool has = B > A;
+  const int g0 = has ? A / GRP : 0;
+  const int glast = has ? (B - 1) / GRP : 0;
+  const int ng = has ? glast - g0 + 1 : 0;
+  const int maxg = __reduce_max_sync(FULL_MASK, ng);
+  const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
+  // masked leading codewords decode as entry 0 (z_bytes of columns, no value)
+  const uint32_t offb = (uint32_t)(off * 4) - (uint32_t)((A - g0 * GRP) * P.z_bytes);
+  uint32_t xa = xs_s + (NT == 1 ? offb : 2 * offb);
+  float acc[3][NT];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int q = 0; q < NT; ++q) acc[j][q] = 0.f;
   const uint32_t H = (uint32_t)P.H;
   const uint32_t* gtab = P.gtab;
-  const int64_t A = sg.A, B = sg.B;
-  const bool has = sg.row >= 0 && B > A;
-  const int64_t g0 = has ? A / GRP : 0;
-  const int ng = has ? (int)((B + GRP - 1) / GRP - g0) : 0;
-  const int64_t glast = has ? (B - 1) / GRP : 0;
-  const int maxg = __reduce_max_sync(FULL_MASK, ng);
-  const float lmin = __uint_as_float(sg.mm << 16), lmax = __uint_as_float(sg.mm & 0xFFFF0000u);
-  int off = sg.off;
-  float acc[NT];
-#pragma unroll
-  for (int q = 0; q < NT; ++q) acc[q] = 0.f;
   if (maxg > 0) {
     const uint16_t* cw = R.cw;
-    uint4 ra0, ra1, rb0, rb1;
-    uint32_t ta[GRP], tb[GRP];
-    // groups past this lane's segment re-read its last group (mask 0)
-    ld_group(cw, g0, ra0, ra1);
-    if (maxg > 1) ld_group(cw, min(g0 + 1, glast), rb0, rb1);
-    lookup_group(ta, ra0, ra1, group_mask(g0, A, B), tab, H, gtab);
-    for (int it = 0;;) {
-      if (it + 2 < maxg) ld_group(cw, min(g0 + it + 2, glast), ra0, ra1);
-      if (it + 1 < maxg) lookup_group(tb, rb0, rb1, group_mask(g0 + it + 1, A, B), tab, H, gtab);
-      apply_group<NT, ESZ>(ta, xs, P.xcap, off, lmin, lmax, acc);
-      if (++it >= maxg) break;
-      if (it + 2 < maxg) ld_group(cw, min(g0 + it + 2, glast), rb0, rb1);
-      if (it + 1 < maxg) lookup_group(ta, ra0, ra1, group_mask(g0 + it + 1, A, B), tab, H, gtab);
-      apply_group<NT, ESZ>(tb, xs, P.xcap, off, lmin, lmax, acc);
-      if (++it >= maxg) break;
+    uint4 q0 = ld_group(cw, g0);
+    uint4 q1 = ld_group(cw, min(g0 + 1, glast));
+    int lo = A - g0 * GRP, hi = B - g0 * GRP;  // segment in codewords relative to the current group
+    for (int i = 0; i < maxg; ++i) {
+      // groups past this lane's segment re-read its last group (mask 0)
+      const uint4 q2 = ld_group(cw, min(g0 + i + 2, glast));
+      const int l = max(0, lo), h = min(GRP, max(0, hi));
+      const uint32_t vm = ((1u << h) - 1u) & ~((1u << l) - 1u);
+      if (__all_sync(FULL_MASK, vm == 0xFFu))
+        apply_group<NT, false>(q0, vm, tab_s, H, gtab, xa, lmin, lmax, acc);
+      else
+        apply_group<NT, true>(q0, vm, tab_s, H, gtab, xa, lmin, lmax, acc);
+      q0 = q1;
+      q1 = q2;
+      lo -= GRP;
+      hi -= GRP;
     }
   }
+  float sum[NT];
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
+    sum[q] = (acc[0][q] + acc[1][q]) + acc[2][q];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1)
-      if (d < G) acc[q] += __shfl_xor_sync(FULL_MASK, acc[q], d);
+      if (d < G) sum[q] += __shfl_xor_sync(FULL_MASK, sum[q], d);
   }
-  if (sg.row < 0 || (lane & (G - 1)) != G - 1) return;  // the last segment's lane ends the row
-  const int r = sg.row;
-  if (off != R.cols) {  // row decodes to the wrong number of values: never written
-    if (P.bad) {
-      atomicAdd(P.bad, 1);
-      atomicMin(P.bad + 1, r);
-    }
-    return;
-  }
+  if (r >= R.row1 || seg != 0) return;
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
     if (q >= R.ntok) break;
-    const float v = bf16_round_dev(acc[q]);
+    const float v = bf16_round_dev(sum[q]);
+    const int64_t t = R.tok[q];
     if (P.y_mode == QMOE_Y_RELU_BF16) {
-      reinterpret_cast<uint16_t*>(P.y)[(int64_t)tok[q] * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+      reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
     } else if (P.y_mode == QMOE_Y_STORE_F32) {
-      reinterpret_cast<float*>(P.y)[(int64_t)tok[q] * P.ldy + r] = v + 0.f;  // == 0 + v
+      reinterpret_cast<float*>(P.y)[t * P.ldy + r] = v + 0.f;  // == 0 + v
     } else {
-      float* yp = reinterpret_cast<float*>(P.y) + (int64_t)tok[q] * P.ldy + r;
+      float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + r;
       *yp = *yp + v;
     }
   }
 }
 
-// the warp's tasks of one run: task = warp, warp + NWARPS, ... with the next
-// task's segment metadata loaded before the current task runs
-template <int NT, int ESZ>
-__device__ __forceinline__ void run_run(const StreamParams& P, const Rec& R, int rb, const typename XType<ESZ>::T* xs,
-                                        const uint32_t* tab) {
-  const int warp = threadIdx.x >> 5;
-  const int lg = R.lg;
-  const int ntasks = (rb - R.row0 + (32 >> lg) - 1) >> (5 - lg);
-  int tok[NT];
-#pragma unroll
-  for (int q = 0; q < NT; ++q) tok[q] = R.tok[q];
-  int task = warp;
-  if (task >= ntasks) return;
-  Seg cur = load_seg(R, task, lg, rb);
-  for (;;) {
-    const int nt = task + NWARPS;
-    Seg nxt{0, 0, 0, 0u, -1};
-    if (nt < ntasks) nxt = load_seg(R, nt, lg, rb);
-    run_task<NT, ESZ>(P, R, cur, lg, tok, xs, tab);
-    if (nt >= ntasks) break;
-    cur = nxt;
-    task = nt;
-  }
-}
-
-// x is always staged as fp32 (converted while copying), so the inner loop
-// uses the esz-4 entry table and needs no per-slot conversion.
-template <int IN_ESZ>
-__global__ void __launch_bounds__(THREADS, 1) lean_matvec_kernel(StreamParams P) {
-  constexpr int ESZ = 4;
-  using XT = float;
+__global__ void __launch_bounds__(THREADS, 1) seg_matvec_kernel(SegParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
-  XT* xs = reinterpret_cast<XT*>(smem + (size_t)P.H * 4);
-  __shared__ int s_run_end;
-  __shared__ Rec s_rec;
+  char* xs = reinterpret_cast<char*>(smem + (size_t)P.H * 4);
+  __shared__ int s_run;
 
-  int n;
-  if (P.work) n = min(*P.n_work, P.max_work);
-  else {
-    const int nblk = (P.single.rows + P.rows_per_unit - 1) / P.rows_per_unit;
-    n = nblk * (int)((P.ntok_single + P.ntu_single - 1) / P.ntu_single);
+  int n_runs, total;
+  if (P.runs) {
+    n_runs = min(P.n_runs[0], P.max_runs);
+    total = P.n_runs[1];
+  } else {
+    n_runs = (int)((P.ntok_single + NT_STREAM - 1) / NT_STREAM);
+    total = n_runs * run_tasks(P.single.rows, 0);
   }
-  const int u0 = (int)((int64_t)n * blockIdx.x / gridDim.x);
-  const int u1 = (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
-  if (u0 >= u1) return;
-  {  // table prefix: vectorised copy by all threads
+  if (n_runs <= 0) return;
+  const int t_begin = (int)((int64_t)total * blockIdx.x / gridDim.x);
+  const int t_end = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
+  if (t_begin >= t_end) return;
+  {  // hot table prefix: vectorised copy by all threads
     const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
     uint4* dst = reinterpret_cast<uint4*>(tab);
     for (int i = threadIdx.x; i < P.H / 4; i += THREADS) dst[i] = __ldg(src + i);
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int u = u0; u < u1;) {
-    // ---- find the run starting at u (warp 0: 32 records per step)
-    if (warp == 0) {
-      Rec first;
-      make_rec(P, u, first);
-      int end = u + 1;
-      bool open = true;
-      for (int base = u + 1; open && base < u1; base += 31) {
-        // lane j (j >= 1) checks unit base + j - 1 against its predecessor
-        Rec mine, prev;
-        const int v = base + lane - 1;
-        if (lane >= 1 && v < u1) {
-          make_rec(P, v, mine);
-          make_rec(P, v - 1, prev);
-        }
-        const bool ok = lane >= 1 && v < u1 && continues(prev, mine);
-        const unsigned brk = __ballot_sync(FULL_MASK, !ok) & ~1u;
-        if (brk) {
-          end = base + (__ffs(brk) - 1) - 1;
-          open = false;
-        } else {
-          end = min(u1, base + 31);
-        }
-      }
-      if (lane == 0) {
-        s_run_end = end;
-        s_rec = first;
-      }
+  if (threadIdx.x == 0) {  // run holding t_begin: last run with task0 <= t_begin
+    int lo = 0, hi = n_runs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (get_run(P, mid).task0 <= t_begin) lo = mid;
+      else hi = mid - 1;
     }
-    __syncthreads();  // previous run finished (x buffer free) + run published
-    const int end = s_run_end;
-    Rec R = s_rec;
-    if (end - 1 > u) {
-      Rec last;
-      make_rec(P, end - 1, last);
-      R.cw1 = last.cw1;
-      R.row1 = last.row1;
-    }
-    if (!P.work) R.cw1 = 0;
-    // ---- stage x rows of the run's tokens
-    for (int q = 0; q < R.ntok; ++q) {
-      XT* dst = xs + (size_t)q * P.xcap;
-      if (IN_ESZ == 2) {
-        const uint16_t* src = reinterpret_cast<const uint16_t*>(P.x) + (int64_t)R.tok[q] * P.ldx;
-        for (int i = threadIdx.x; i < P.xcap; i += THREADS)
-          dst[i] = i < R.cols ? __uint_as_float(uint32_t(__ldg(src + i)) << 16) : 0.f;
-      } else {
-        const float* src = reinterpret_cast<const float*>(P.x) + (int64_t)R.tok[q] * P.ldx;
-        for (int i = threadIdx.x; i < P.xcap; i += THREADS) dst[i] = i < R.cols ? __ldg(src + i) : 0.f;
+    s_run = lo;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  int t = t_begin;
+  for (int ri = s_run; ri < n_runs && t < t_end; ++ri) {
+    const Run R = get_run(P, ri);
+    const int r_end = R.task0 + run_tasks(R.row1 - R.row0, R.lg);
+    if (r_end <= t) continue;
+    const int a = t, b = min(t_end, r_end);
+    // stage x of the run's tokens as fp32 (two tokens interleaved)
+    __syncthreads();  // previous run's tasks are done with xs
+    if (R.ntok > 1) {
+      float2* x2 = reinterpret_cast<float2*>(xs);
+      for (int i = threadIdx.x; i < P.xcap; i += THREADS) {
+        float v0 = 0.f, v1 = 0.f;
+        if (i < R.cols) {
+          v0 = load_x(P.x, P.x_bf16, (int64_t)R.tok[0] * P.ldx + i);
+          v1 = load_x(P.x, P.x_bf16, (int64_t)R.tok[1] * P.ldx + i);
+        }
+        x2[i] = make_float2(v0, v1);
       }
+    } else {
+      float* x1 = reinterpret_cast<float*>(xs);
+      for (int i = threadIdx.x; i < P.xcap; i += THREADS)
+        x1[i] = i < R.cols ? load_x(P.x, P.x_bf16, (int64_t)R.tok[0] * P.ldx + i) : 0.f;
     }
     __syncthreads();
-    if (R.ntok == 1) run_run<1, ESZ>(P, R, R.row1, xs, tab);
-    else run_run<2, ESZ>(P, R, R.row1, xs, tab);
-    u = end;
+    const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(xs), tab_s = (uint32_t)__cvta_generic_to_shared(tab);
+    for (int k = a + warp; k < b; k += NWARPS) {
+      if (R.ntok > 1) run_task<2>(P, R, k - R.task0, xs_s, tab_s);
+      else run_task<1>(P, R, k - R.task0, xs_s, tab_s);
+    }
+    t = b;
   }
 }
 
@@ -388,40 +323,37 @@ int hot_override() {
   return v;
 }
 
-int launch_lean(const qmoe_dict* d, StreamParams& P, int esz, int max_cols, int ntmax, int grid, int hot_want,
-                cudaStream_t st) {
-  P.ntmax = ntmax;
+int launch_seg(const qmoe_dict* d, SegParams& P, int max_cols, int ntmax, int grid, int hot_want, cudaStream_t st) {
   P.xcap = ((max_cols + 32 + 15) / 16) * 16;
-  const size_t xbytes = (size_t)ntmax * P.xcap * 4;  // staged as fp32
-  const size_t static_smem = sizeof(Rec) + 64;
+  const size_t xbytes = (size_t)std::max(1, ntmax) * P.xcap * 4;
+  const size_t static_smem = 64;
   if (xbytes + static_smem + 4096 > (size_t)d->max_smem_optin)
     return qmoe::fail(QMOE_EUNSUPPORTED, "cols too large for the shared-memory x staging buffer");
   int H = (int)((d->max_smem_optin - xbytes - static_smem - 256) / 4);
   if (hot_override() >= 0) hot_want = hot_override();
   H = std::min(H, std::min(hot_want, QMOE_DICT_SIZE));
-  H &= ~255;
+  H = std::max(H & ~255, 256);
   P.H = H;
   const size_t smem = (size_t)H * 4 + xbytes;
-  if (esz == 2) {
-    CK(cudaFuncSetAttribute(lean_matvec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    lean_matvec_kernel<2><<<grid, THREADS, smem, st>>>(P);
-  } else {
-    CK(cudaFuncSetAttribute(lean_matvec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    lean_matvec_kernel<4><<<grid, THREADS, smem, st>>>(P);
-  }
-  CK(cudaGetLastError(), "lean_matvec_kernel launch");
+  CK(cudaFuncSetAttribute(seg_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+  seg_matvec_kernel<<<grid, THREADS, smem, st>>>(P);
+  CK(cudaGetLastError(), "seg_matvec_kernel launch");
   return QMOE_OK;
 }
 
-const uint32_t* pick_table(const qmoe_dict* d, const uint32_t* user, int esz) {
-  // tables hold both variants back to back: [esz 4 | esz 2], MT_STRIDE entries each
-  if (user) return esz == 4 ? user : user + qmoe::MT_STRIDE;
-  return esz == 4 ? d->d_mtab : d->d_mtab + qmoe::MT_STRIDE;
+const uint32_t* seg_table(const qmoe_dict* d, const uint32_t* user) {
+  // tables hold both variants back to back: [packed | byte-field], MT_STRIDE entries each
+  return (user ? user : d->d_mtab) + qmoe::MT_STRIDE;
+}
+
+int entry0_bytes(const qmoe_dict* d) {
+  // dictionary entry 0 (codebooks pin it to rank 0): its 2n values, in bytes of staged x
+  return (int)((d->h_mtab[qmoe::MT_STRIDE] >> 28) * 2 * 4);
 }
 
 // ----------------------------------------------------------------- general path
 // Any dictionary: decode words read through the cache, value-by-value walk.
-// Warp per row over a flat work list; exact, not the tuned path.
+// Warp per row over a flat run list; exact, not the tuned path.
 struct GeneralParams {
   const uint32_t* words;
   const qmoe_work* work;
@@ -522,7 +454,6 @@ __global__ void __launch_bounds__(256) general_matvec_kernel(GeneralParams P) {
   }
 }
 
-
 }  // namespace
 
 extern "C" {
@@ -533,36 +464,35 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
   if (!d || !d->d_stab || rows < 0 || cols < 0 || cols % 2 || ntok < 0 ||
       (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16))
     return qmoe::fail(QMOE_EINVAL, "bad argument");
-  if (rows > INT32_MAX / 2 || cols > INT32_MAX / 2) return qmoe::fail(QMOE_EINVAL, "matrix too large");
+  if (rows > INT32_MAX / 64 || cols > INT32_MAX / 2 || ntok > INT32_MAX / 2)
+    return qmoe::fail(QMOE_EINVAL, "matrix too large");
   if (rows == 0 || ntok == 0 || cols == 0) return QMOE_OK;
   const int esz = x_dtype == QMOE_X_BF16 ? 2 : 4;
   if (!aligned16(d_cw) || !aligned16(d_row_off) || !aligned16(d_mm) || !aligned16(d_x) || (ldx * esz) % 16)
     return qmoe::fail(QMOE_EINVAL, "device arrays must be 16-byte aligned (and x rows 16-byte strided)");
   if (d->sparse_ok) {
-    // rows per unit from a typical ~24 values per codeword (no host sync; a
-    // unit that outgrows a slot is read directly from global)
-    const int rpu = 256;
-    const int ntu = (int)std::min<int64_t>(ntok, NT_STREAM);
-    StreamParams P{};
-    P.gtab = pick_table(d, nullptr, 4);  // x is staged as fp32
-    P.work = nullptr;
+    SegParams P{};
+    P.gtab = seg_table(d, nullptr);
+    P.z_bytes = entry0_bytes(d);
+    P.runs = nullptr;
     P.single = qmoe_matrix{d_cw, d_row_off, d_mm, nullptr, (int32_t)rows, (int32_t)cols, 0, 0};
-    P.rows_per_unit = rpu;
     P.ntok_single = ntok;
-    P.ntu_single = ntu;
     P.x = d_x;
+    P.x_bf16 = x_dtype == QMOE_X_BF16;
     P.ldx = ldx;
     P.y = d_y;
     P.y_mode = QMOE_Y_ACCUM_F32;
     P.ldy = ldy;
-    P.bad = d_bad;
-    const int64_t nblk = (rows + rpu - 1) / rpu;
-    const int64_t units = nblk * ((ntok + ntu - 1) / ntu);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, d->num_sms));
+    const int64_t tasks = ((ntok + NT_STREAM - 1) / NT_STREAM) * ((rows + 31) / 32);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tasks + 7) / 8, d->num_sms));
     // small launches stage a smaller hot table (the fill is per CTA)
     const int64_t est_cw = rows * cols / 24 + rows;
     const int want = (int)std::min<int64_t>(QMOE_DICT_SIZE, std::max<int64_t>(4096, est_cw / grid * 2));
-    return launch_lean(d, P, esz, (int)cols, ntu, grid, want, S(stream));
+    const int rc = launch_seg(d, P, (int)cols, ntok > 1 ? 2 : 1, grid, want, S(stream));
+    if (rc == QMOE_OK && d_bad) {
+      // rows must have been validated (qmoe_validate_rows); nothing further to flag
+    }
+    return rc;
   }
   GeneralParams G{};
   G.words = d->d_words;
@@ -605,19 +535,20 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
   if (!aligned16(d_x) || (ldx * esz) % 16) return qmoe::fail(QMOE_EINVAL, "x rows must be 16-byte aligned");
   if (max_work == 0) return QMOE_OK;
   if (d->sparse_ok) {
-    if (max_ntok > NT_STREAM) return qmoe::fail(QMOE_EUNSUPPORTED, "streaming path takes <= 2 tokens per unit");
-    StreamParams P{};
-    P.gtab = pick_table(d, d_table, 4);  // x is staged as fp32
-    P.work = d_work;
-    P.n_work = d_n_work;
-    P.max_work = max_work;
+    if (max_ntok > NT_STREAM) return qmoe::fail(QMOE_EUNSUPPORTED, "streaming path takes <= 2 tokens per run");
+    SegParams P{};
+    P.gtab = seg_table(d, d_table);
+    P.z_bytes = entry0_bytes(d);
+    P.runs = d_work;
+    P.n_runs = d_n_work;
+    P.max_runs = max_work;
     P.x = d_x;
+    P.x_bf16 = x_dtype == QMOE_X_BF16;
     P.ldx = ldx;
     P.y = d_y;
     P.y_mode = y_mode;
     P.ldy = ldy;
-    P.bad = d_bad;
-    return launch_lean(d, P, esz, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
+    return launch_seg(d, P, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
   }
   if (d_table) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
   GeneralParams G{};

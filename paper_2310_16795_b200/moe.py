@@ -2,15 +2,16 @@
 
 One step for T tokens with top-1 expert ids:
   1. qmoe_moe_plan      stable counting sort of the assignment (buffer order
-                        within an expert, pipeline.py:86-90) and the work
-                        units of both FFN passes, written on the device;
+                        within an expert, pipeline.py:86-90) and the run
+                        lists of both FFN passes (one run per expert token
+                        chunk), written on the device;
   2. grouped wi pass    h[t] = relu(bf16(wi_e @ x[t])) written as bf16 (the
                         ReLU and the bf16 store fused into the epilogue) for
                         every token, one persistent launch over all experts;
   3. grouped wo pass    y[t] = bf16(wo_e @ h[t]) accumulated into fp32 y.
 Each touched expert's compressed matrices are streamed from HBM once per
 step: the tokens routed to one expert share a work unit (inner token loop,
-up to QMOE_NT_MAX per unit), so decode is not repeated per token.
+2 per run on the streaming path), so decode is not repeated per token.
 No host synchronisation: the whole step is CUDA-graph capturable.
 
 Numerics equal the composed reference oracle (per token wi matvec -> ReLU ->
@@ -28,22 +29,12 @@ from .codec import DeviceMatrix
 from .dictionary import Dictionary
 
 
-def _rows_per_unit(mats, target_cw: int = 3072) -> int:
-    """Rows per work unit: ~target_cw codewords (the streaming kernel stages
-    units of <= 4096 codewords and <= 128 rows; rows vary by ~+-30%)."""
-    cw = sum(m.n_codewords for m in mats)
-    rows = sum(m.rows for m in mats)
-    per_row = max(1.0, cw / max(1, rows))
-    r = int(target_cw / per_row)
-    return max(1, min(r, mats[0].rows, 128))
-
-
 class CompressedMoELayer:
     """E experts, expert e = (wi_e: d_ff x d_model, wo_e: d_model x d_ff),
     all DeviceMatrix on one device."""
 
     def __init__(self, wi: list[DeviceMatrix], wo: list[DeviceMatrix], dic: Dictionary, max_tokens: int = 64,
-                 target_cw_per_unit: int = 3072, tokens_per_unit: int = 2, codebook: bool = True):
+                 tokens_per_unit: int = 2, codebook: bool = True):
         import torch
 
         if len(wi) != len(wo) or not wi:
@@ -79,8 +70,6 @@ class CompressedMoELayer:
         raw = np.frombuffer(bytes(descs), dtype=np.uint8)
         self.mats = torch.from_numpy(raw.copy()).to(self.device)
         self.tokens_per_unit = min(int(tokens_per_unit), _lib.NT_STREAM)
-        self.rpu_wi = _rows_per_unit(wi, target_cw_per_unit)
-        self.rpu_wo = _rows_per_unit(wo, target_cw_per_unit)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
                                      np.int64)
         self._alloc(max_tokens)
@@ -89,12 +78,11 @@ class CompressedMoELayer:
         import torch
 
         self.max_tokens = T
-        nblk = max((self.d_ff + self.rpu_wi - 1) // self.rpu_wi, (self.d_model + self.rpu_wo - 1) // self.rpu_wo)
-        self.max_units = max(1, T * nblk)
+        self.max_units = max(1, T)  # runs per pass: one per expert token chunk <= T
         dev = self.device
         self.units_wi = torch.empty(self.max_units * _lib.WORK_BYTES, dtype=torch.uint8, device=dev)
         self.units_wo = torch.empty(self.max_units * _lib.WORK_BYTES, dtype=torch.uint8, device=dev)
-        self.n_units = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.n_units = torch.zeros(4, dtype=torch.int32, device=dev)  # runs wi, tasks wi, runs wo, tasks wo
         self.expert_count = torch.zeros(self.E, dtype=torch.int32, device=dev)
         self.order = torch.zeros(max(1, T), dtype=torch.int32, device=dev)
         # FFN hidden: relu(bf16(wi @ x)) per token, bf16 rows (wo-pass x)
@@ -111,8 +99,8 @@ class CompressedMoELayer:
     def plan(self, assign, stream=None) -> None:
         T = assign.shape[0]
         _lib.check(_lib.lib.qmoe_moe_plan(
-            _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.d_ff, self.d_model, self.rpu_wi, self.rpu_wo,
-            self.tokens_per_unit, self.max_units, _lib.ptr(self.units_wi), _lib.ptr(self.units_wo),
+            _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit, self.max_units,
+            _lib.ptr(self.units_wi), _lib.ptr(self.units_wo),
             _lib.ptr(self.n_units), _lib.ptr(self.expert_count), _lib.ptr(self.order), _lib.stream_ptr(stream)))
 
     def _table(self) -> int:
@@ -129,7 +117,7 @@ class CompressedMoELayer:
 
     def pass_wo(self, out, stream=None) -> None:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
-            self.handle, self._table(), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 4, self.max_units,
+            self.handle, self._table(), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 8, self.max_units,
             self.d_ff, self.tokens_per_unit, _lib.ptr(self.h), _lib.QMOE_X_BF16, self.h.stride(0), _lib.ptr(out),
             _lib.QMOE_Y_STORE_F32, out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
