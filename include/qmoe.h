@@ -53,14 +53,23 @@ enum { QMOE_X_F32 = 0, QMOE_X_BF16 = 1 };
 
 typedef struct qmoe_dict* qmoe_dict_t;
 
-/* One compressed matrix resident on the device (grouped launches). */
-/* The arrays must start 16-byte aligned and be readable 32 bytes past their
- * end (row metadata is streamed into shared memory with cp.async.bulk and
- * codewords are read in sector-aligned 32-byte groups); n_cw = row_off[rows].
- * ck / lg: optional row-segment checkpoints (qmoe_checkpoints): with G = 2^lg
- * lanes per row, ck[r * (G-1) + j - 1] is the column at which segment j of row
- * r starts (segment j = codewords [s + j*n/G, s + (j+1)*n/G) of the row's n).
- * lg = 0, ck = NULL: one lane per row. */
+/* One compressed matrix resident on the device (grouped launches), in one of
+ * two layouts:
+ *  RAW (row_id == NULL): the reference format. cw / row_off / row_minmax as
+ *    in CompressedMatrix; the arrays must start 16-byte aligned and be
+ *    readable 32 bytes past their end. ck / lg: optional row-segment
+ *    checkpoints (qmoe_checkpoints): with G = 2^lg lanes per row,
+ *    ck[r * (G-1) + j - 1] is the column at which segment j of row r starts
+ *    (segment j = codewords [s + j*n/G, s + (j+1)*n/G) of the row's n).
+ *  PACKED (row_id != NULL, built by qmoe_pack): kernel-private. Rows sorted
+ *    by codeword count (descending), each row's stream padded with codeword 0
+ *    (no non-zero value) to whole 8-codeword groups:
+ *      cw         uint16[8 * G_total]  group g = cw[8g .. 8g+8)
+ *      row_off    int32[rows + 1]      first GROUP of sorted row i (G_total last)
+ *      row_minmax uint32[rows]         bf16 (min, max) of sorted row i
+ *      ck         uint16[G_total]      column at which group g starts in its row
+ *      row_id     uint16[rows]         original row of sorted row i
+ *    lg is then only a default: the lanes per row are chosen per run. */
 typedef struct qmoe_matrix {
   const uint16_t* cw;
   const int32_t* row_off;
@@ -70,16 +79,18 @@ typedef struct qmoe_matrix {
   int32_t cols;
   int32_t n_cw;
   int32_t lg;
+  const uint16_t* row_id;
 } qmoe_matrix;
 
 /* One RUN of a grouped launch (self-contained, 80 bytes): rows [row0, row1)
- * of the matrix whose arrays are cw / row_off / row_minmax / ck (lg: 2^lg
- * lanes per row, see qmoe_matrix), applied to `ntok` tokens (<= 2 on the
- * streaming path). Token t reads x row tok[t] (x + tok[t] * ldx) and writes y
- * row tok[t] (y + tok[t] * ldy). A run is cut into ceil(((row1 - row0) << lg)
- * / 32) warp TASKS; task0 is the exclusive prefix of those counts over the
- * list (the launch splits the global task range evenly over the SMs).
- * Written by qmoe_moe_plan (or by the caller). */
+ * of one matrix (fields as qmoe_matrix; row_id != NULL selects the PACKED
+ * layout, rows then being sorted-row indices), applied to `ntok` tokens (<= 2
+ * on the streaming path) with G = 2^lg lanes per row. Token t reads x row
+ * tok[t] (x + tok[t] * ldx) and writes y row tok[t] (y + tok[t] * ldy). A
+ * run is cut into ceil(((row1 - row0) << lg) / 32) warp TASKS; task0 is the
+ * exclusive prefix of those counts over the list (the launch splits the
+ * global task range evenly over the SMs). Written by qmoe_moe_plan (or by
+ * the caller). */
 typedef struct qmoe_work {
   const uint16_t* cw;
   const int32_t* row_off;
@@ -91,7 +102,7 @@ typedef struct qmoe_work {
   int32_t lg;
   int32_t ntok;
   int32_t task0;
-  int32_t pad_[2];
+  const uint16_t* row_id;
   int32_t tok[QMOE_NT_MAX];
 } qmoe_work;
 
@@ -100,8 +111,10 @@ enum {
   QMOE_Y_ACCUM_F32 = 0,     /* y (f32) += bf16(dot)                       (codec.py:243) */
   QMOE_Y_RELU_BF16 = 1,     /* y (bf16) = relu(bf16(dot)) — the FFN hidden h, written
                                once from zero: equals relu(fused_matvec(wi, x, y=0)) */
-  QMOE_Y_STORE_F32 = 2      /* y (f32) = 0 + bf16(dot): accumulate into a zero y
+  QMOE_Y_STORE_F32 = 2,     /* y (f32) = 0 + bf16(dot): accumulate into a zero y
                                without reading it */
+  QMOE_RUNS_PACKED = 0x100  /* flag OR-ed into y_mode: every run of the list is a
+                               PACKED-layout matrix (qmoe_pack) */
 };
 
 /* ------------------------------------------------------------------ host-only
@@ -200,6 +213,18 @@ int qmoe_checkpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* 
                      const int32_t* d_row_off, int64_t rows, int64_t cols, int lg, uint16_t* d_ck,
                      int32_t* d_bad, void* stream);
 
+/* PACKED layout of one RAW matrix (see qmoe_matrix), built once on the device.
+ * d_order: int32[rows], the sorted row order (row of sorted row i; e.g. a
+ * stable descending sort of the rows' codeword counts); d_gstart:
+ * int32[rows + 1], exclusive prefix over sorted rows of ceil(n_row / 8).
+ * Outputs d_pcw (uint16[8 * gstart[rows]] + 16 readable), d_pmm, d_pck
+ * (uint16[gstart[rows]]), d_rid. d_table as for qmoe_checkpoints (entry order
+ * of the stream). Rows that do not decode to cols values are counted in d_bad. */
+int qmoe_pack(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d_cw,
+              const int32_t* d_row_off, const uint32_t* d_row_minmax, int64_t rows, int64_t cols,
+              const int32_t* d_order, const int32_t* d_gstart, uint16_t* d_pcw, uint32_t* d_pmm,
+              uint16_t* d_pck, uint16_t* d_rid, int32_t* d_bad, void* stream);
+
 /* Paper Listing 1 kept as the "paper design on B200"
  * baseline: warp per row, lanes 0..27 extract, decode words read through the
  * cache, shuffle reduction. If d_trace is non-NULL it receives, per codeword
@@ -240,9 +265,10 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
  *   pass 2: wo_e = d_mats[2e + 1]  (d_runs_wo)
  * with task0 prefixes filled. d_runs_* hold max_runs (>= T) records;
  * d_n = int32[4] {runs wi, tasks wi, runs wo, tasks wo}. Ids outside
- * [0, E) are dropped (the token gets no expert output). */
+ * [0, E) are dropped (the token gets no expert output). lg_wi / lg_wo: lanes
+ * per row (2^lg) of the runs of PACKED matrices, -1 = the matrix's lg. */
 int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats,
-                  int32_t tokens_per_run, int32_t max_runs, qmoe_work* d_runs_wi,
+                  int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo, int32_t max_runs, qmoe_work* d_runs_wi,
                   qmoe_work* d_runs_wo, int32_t* d_n, int32_t* d_expert_count, int32_t* d_order,
                   void* stream);
 

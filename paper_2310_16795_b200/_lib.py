@@ -38,16 +38,17 @@ i32 = ctypes.c_int32
 
 class QmoeMatrix(ctypes.Structure):
     _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("ck", vp), ("rows", i32), ("cols", i32),
-                ("n_cw", i32), ("lg", i32)]
+                ("n_cw", i32), ("lg", i32), ("row_id", vp)]
 
 
 class QmoeWork(ctypes.Structure):
     _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("ck", vp), ("cols", i32), ("row0", i32),
-                ("row1", i32), ("lg", i32), ("ntok", i32), ("task0", i32), ("pad_", i32 * 2),
+                ("row1", i32), ("lg", i32), ("ntok", i32), ("task0", i32), ("row_id", vp),
                 ("tok", i32 * NT_MAX)]
 
 
 QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16, QMOE_Y_STORE_F32 = 0, 1, 2
+QMOE_RUNS_PACKED = 0x100
 
 
 WORK_BYTES = ctypes.sizeof(QmoeWork)
@@ -78,7 +79,8 @@ _SIGS = {
     "qmoe_encode_emit": (ctypes.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "qmoe_exclusive_scan": (ctypes.c_int, [vp, i64, vp, vp]),
     "qmoe_rtn_quantize": (ctypes.c_int, [vp, i64, i64, vp, vp, vp, vp]),
-    "qmoe_moe_plan": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "qmoe_moe_plan": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "qmoe_pack": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -92,6 +92,8 @@ class DeviceMatrix:
         # row-segment checkpoints (G = 2^lg lanes per row), see build_checkpoints
         self.ck = None
         self.lg = 0
+        # kernel-private PACKED layout (qmoe_pack), see build_layout
+        self.packed = None
 
     @property
     def n_codewords(self) -> int:
@@ -124,9 +126,49 @@ class DeviceMatrix:
         return self.bad_rows
 
     def descriptor(self) -> tuple:
-        """qmoe_matrix fields (include/qmoe.h)."""
+        """qmoe_matrix fields (include/qmoe.h): the PACKED layout when built."""
+        if self.packed is not None:
+            p = self.packed
+            return (p["cw"].data_ptr(), p["gstart"].data_ptr(), p["mm"].data_ptr(), p["ck"].data_ptr(), self.rows,
+                    self.cols, self.n_codewords, p["lg"], p["rid"].data_ptr())
         return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(),
-                self.ck.data_ptr() if self.ck is not None else 0, self.rows, self.cols, self.n_codewords, self.lg)
+                self.ck.data_ptr() if self.ck is not None else 0, self.rows, self.cols, self.n_codewords, self.lg, 0)
+
+    def build_layout(self, dic: Dictionary) -> None:
+        """Kernel-private PACKED layout (qmoe_pack): rows sorted by codeword
+        count, each padded with codeword 0 to whole 8-codeword groups, plus the
+        start column of every group — lanes then walk whole groups of one row
+        with no masking, and the lanes per row can be chosen per launch. The
+        host format and this matrix's own arrays are unchanged."""
+        torch = _torch()
+        dev = self.cw.device
+        n = (self.row_off[1:] - self.row_off[:-1]).to(torch.int64)
+        m = (n + 7) // 8
+        order = torch.sort(m, descending=True, stable=True).indices.to(torch.int32)
+        gstart = torch.zeros(self.rows + 1, dtype=torch.int64, device=dev)
+        gstart[1:] = torch.cumsum(m[order.long()], 0)
+        G_total = int(gstart[-1].item()) if self.rows else 0
+        gstart = _lib.padded_copy(gstart.to(torch.int32))
+        p = {
+            "cw": _lib.padded_empty(8 * G_total + 16, torch.int16, dev),
+            "gstart": gstart,
+            "mm": _lib.padded_empty(max(1, self.rows), torch.int32, dev),
+            "ck": _lib.padded_empty(max(1, G_total), torch.int16, dev),
+            "rid": _lib.padded_empty(max(1, self.rows), torch.int16, dev),
+            "groups": G_total,
+            "mean_groups": G_total / max(1, self.rows),
+        }
+        p["cw"][8 * G_total:].zero_()
+        bad = torch.tensor([0, INT32_MAX], dtype=torch.int32, device=dev)
+        table = self.codebook.table if self.codebook is not None else None
+        _lib.check(_lib.lib.qmoe_pack(dic.device_handle(dev.index), _lib.ptr(table), _lib.ptr(self.cw),
+                                      _lib.ptr(self.row_off), _lib.ptr(self.row_minmax), self.rows, self.cols,
+                                      _lib.ptr(order), _lib.ptr(gstart), _lib.ptr(p["cw"]), _lib.ptr(p["mm"]),
+                                      _lib.ptr(p["ck"]), _lib.ptr(p["rid"]), _lib.ptr(bad), _lib.stream_ptr()))
+        if int(bad[0].item()):
+            raise CorruptionError("row decodes to the wrong number of values")
+        p["lg"] = max(0, min(3, int(np.log2(max(1.0, p["mean_groups"] / 4)))))
+        self.packed = p
 
     def mean_codewords_per_row(self) -> float:
         return self.n_codewords / max(1, self.rows)

@@ -393,8 +393,13 @@ __device__ __forceinline__ int4 block_scan_excl(int4 v, int4* wsum, int4* total)
   return make_int4(b.x + incl.x - v.x, b.y + incl.y - v.y, b.z + incl.z - v.z, b.w + incl.w - v.w);
 }
 
+__device__ __forceinline__ int plan_lg(const qmoe_matrix& M, int lg_over) {
+  return (M.row_id && lg_over >= 0) ? lg_over : M.lg;
+}
+
 __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restrict__ assign, int T, int E,
-                                                        const qmoe_matrix* __restrict__ mats, int ntu, int max_runs,
+                                                        const qmoe_matrix* __restrict__ mats, int ntu, int lg_wi,
+                                                        int lg_wo, int max_runs,
                                                         qmoe_work* runs_wi, qmoe_work* runs_wo, int32_t* n_out,
                                                         int32_t* cnt_out, int32_t* order) {
   extern __shared__ int32_t sh[];
@@ -421,8 +426,8 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     loc.x += c;
     loc.y += nch;
     if (nch) {
-      loc.z += nch * run_tasks_dev(mats[2 * e].rows, mats[2 * e].lg);
-      loc.w += nch * run_tasks_dev(mats[2 * e + 1].rows, mats[2 * e + 1].lg);
+      loc.z += nch * run_tasks_dev(mats[2 * e].rows, plan_lg(mats[2 * e], lg_wi));
+      loc.w += nch * run_tasks_dev(mats[2 * e + 1].rows, plan_lg(mats[2 * e + 1], lg_wo));
     }
   }
   int4 base = block_scan_excl(loc, wsum, &total);
@@ -435,8 +440,8 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     base.x += c;
     base.y += nch;
     if (nch) {
-      base.z += nch * run_tasks_dev(mats[2 * e].rows, mats[2 * e].lg);
-      base.w += nch * run_tasks_dev(mats[2 * e + 1].rows, mats[2 * e + 1].lg);
+      base.z += nch * run_tasks_dev(mats[2 * e].rows, plan_lg(mats[2 * e], lg_wi));
+      base.w += nch * run_tasks_dev(mats[2 * e + 1].rows, plan_lg(mats[2 * e + 1], lg_wo));
     }
     cnt_out[e] = c;
     cnt[e] = 0;  // becomes the fill cursor
@@ -477,18 +482,18 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     qmoe_work U;
     U.ntok = min(ntu, c - ch * ntu);
     for (int q = 0; q < QMOE_NT_MAX; ++q) U.tok[q] = order[start[e] + ch * ntu + min(q, U.ntok - 1)];
-    U.pad_[0] = U.pad_[1] = 0;
     for (int pass = 0; pass < 2; ++pass) {
       const qmoe_matrix M = mats[2 * e + pass];
       U.cw = M.cw;
       U.row_off = M.row_off;
       U.row_minmax = M.row_minmax;
       U.ck = M.ck;
-      U.lg = M.lg;
+      U.row_id = M.row_id;
+      U.lg = plan_lg(M, pass ? lg_wo : lg_wi);
       U.cols = M.cols;
       U.row0 = 0;
       U.row1 = M.rows;
-      U.task0 = (pass ? two[e] : twi[e]) + ch * run_tasks_dev(M.rows, M.lg);
+      U.task0 = (pass ? two[e] : twi[e]) + ch * run_tasks_dev(M.rows, U.lg);
       (pass ? runs_wo : runs_wi)[i] = U;
     }
   }
@@ -538,6 +543,35 @@ __global__ void checkpoints_kernel(const uint32_t* __restrict__ tab, const uint1
     ++j;
   }
   if (off != cols && bad) {
+    atomicAdd(bad, 1);
+    atomicMin(bad + 1, (int)r);
+  }
+}
+
+// ================================================================ packed layout
+// qmoe_pack (include/qmoe.h): thread per sorted row copies the row's stream
+// into whole 8-codeword groups (padding with codeword 0 — entry 0, no value),
+// records the start column of every group, the row's levels and its id.
+__global__ void pack_kernel(const uint32_t* __restrict__ tab, const uint16_t* __restrict__ cw,
+                            const int32_t* __restrict__ row_off, const uint32_t* __restrict__ mm, int64_t rows,
+                            int64_t cols, const int32_t* __restrict__ order, const int32_t* __restrict__ gstart,
+                            uint16_t* __restrict__ pcw, uint32_t* __restrict__ pmm, uint16_t* __restrict__ pck,
+                            uint16_t* __restrict__ rid, int32_t* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int r = order[i];
+  const int s = row_off[r], n = row_off[r + 1] - s;
+  const int g0 = gstart[i], m = gstart[i + 1] - g0;
+  pmm[i] = mm[r];
+  rid[i] = (uint16_t)r;
+  int off = 0;
+  for (int k = 0; k < 8 * m; ++k) {
+    const uint16_t c = k < n ? cw[s + k] : (uint16_t)0;
+    pcw[(int64_t)8 * g0 + k] = c;
+    if ((k & 7) == 0) pck[g0 + (k >> 3)] = (uint16_t)min(off, 65535);
+    if (k < n) off += int(__ldg(tab + c) & 31u);
+  }
+  if ((off != cols || m != (n + 7) / 8) && bad) {
     atomicAdd(bad, 1);
     atomicMin(bad + 1, (int)r);
   }
@@ -697,16 +731,32 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
 }
 
 int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats, int32_t ntu,
-                  int32_t max_runs, qmoe_work* d_runs_wi, qmoe_work* d_runs_wo, int32_t* d_n,
+                  int32_t lg_wi, int32_t lg_wo, int32_t max_runs, qmoe_work* d_runs_wi, qmoe_work* d_runs_wo, int32_t* d_n,
                   int32_t* d_expert_count, int32_t* d_order, void* stream) {
-  if (T < 0 || E < 1 || !d_mats || max_runs < T || ntu < 1 || ntu > QMOE_NT_MAX || !d_n)
+  if (T < 0 || E < 1 || !d_mats || max_runs < T || ntu < 1 || ntu > QMOE_NT_MAX || !d_n || lg_wi > 5 || lg_wo > 5)
     return qmoe::fail(QMOE_EINVAL, "bad argument (max_runs must be >= T)");
   const size_t smem = (size_t)(5 * E + 1) * 4;
   if (smem > 200 * 1024) return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts");
   CK(cudaFuncSetAttribute(moe_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-  moe_plan_kernel<<<1, 1024, smem, S(stream)>>>(d_assign, T, E, d_mats, ntu, max_runs, d_runs_wi, d_runs_wo, d_n,
+  moe_plan_kernel<<<1, 1024, smem, S(stream)>>>(d_assign, T, E, d_mats, ntu, lg_wi, lg_wo, max_runs, d_runs_wi,
+                                                 d_runs_wo, d_n,
                                                  d_expert_count, d_order);
   CK(cudaGetLastError(), "moe_plan_kernel");
+  return QMOE_OK;
+}
+
+int qmoe_pack(qmoe_dict_t d, const uint32_t* d_table, const uint16_t* d_cw, const int32_t* d_row_off,
+              const uint32_t* d_mm, int64_t rows, int64_t cols, const int32_t* d_order, const int32_t* d_gstart,
+              uint16_t* d_pcw, uint32_t* d_pmm, uint16_t* d_pck, uint16_t* d_rid, int32_t* d_bad, void* stream) {
+  if (bad_dict(d) || rows < 0 || cols < 0 || cols > 65535 || rows > 65536 || !d_order || !d_gstart || !d_pcw ||
+      !d_pmm || !d_pck || !d_rid)
+    return qmoe::fail(QMOE_EINVAL, "bad argument (rows <= 65536, cols <= 65535)");
+  if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "packed layout needs a <=3-non-zero dictionary");
+  if (rows == 0) return QMOE_OK;
+  pack_kernel<<<(int)((rows + 127) / 128), 128, 0, S(stream)>>>(d_table ? d_table : d->d_mtab, d_cw, d_row_off, d_mm,
+                                                                 rows, cols, d_order, d_gstart, d_pcw, d_pmm, d_pck,
+                                                                 d_rid, d_bad);
+  CK(cudaGetLastError(), "pack_kernel");
   return QMOE_OK;
 }
 

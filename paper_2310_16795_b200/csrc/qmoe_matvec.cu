@@ -41,7 +41,10 @@ using namespace qmoe_dev;
 
 namespace {
 
-constexpr int THREADS = 1024;
+#ifndef QMOE_SEG_THREADS
+#define QMOE_SEG_THREADS 768
+#endif
+constexpr int THREADS = QMOE_SEG_THREADS;
 constexpr int NWARPS = THREADS / 32;
 constexpr int GRP = 8;          // codewords per 16-byte group
 constexpr int NT_STREAM = 2;    // tokens per run on the streaming path
@@ -69,6 +72,7 @@ struct Run {
   const int32_t* ro;
   const uint32_t* mm;
   const uint16_t* ck;
+  const uint16_t* rid;  // PACKED layout when non-null
   int cols, row0, row1, lg, ntok, task0;
   int tok[NT_STREAM];
 };
@@ -83,6 +87,7 @@ __device__ __forceinline__ Run get_run(const SegParams& P, int r) {
     R.ro = W.row_off;
     R.mm = W.row_minmax;
     R.ck = W.ck;
+    R.rid = W.row_id;
     R.cols = W.cols;
     R.row0 = W.row0;
     R.row1 = W.row1;
@@ -96,6 +101,7 @@ __device__ __forceinline__ Run get_run(const SegParams& P, int r) {
     R.ro = P.single.row_off;
     R.mm = P.single.row_minmax;
     R.ck = nullptr;
+    R.rid = nullptr;
     R.cols = P.single.cols;
     R.row0 = 0;
     R.row1 = P.single.rows;
@@ -117,41 +123,58 @@ __device__ __forceinline__ uint4 ld_group(const uint16_t* cw, int g) {
   return a;
 }
 
+extern __shared__ __align__(128) uint8_t seg_smem[];
+
+// Shared-memory accesses by 32-bit shared-window address. The window base is
+// produced by an opaque (volatile) asm so the compiler keeps it in a register
+// instead of rematerialising the CTA's window (S2R + LEA) at every access.
+__device__ __forceinline__ uint32_t smem_base() {
+  uint32_t b;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(b) : "l"(seg_smem));
+  return b;
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
   float2 v;
-  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
   return v;
 }
 
-// One group of 8 codewords: lookup + per-slot gather/FMA. MASKED: vm bit u
-// set = codeword u belongs to the lane's segment (others decode as entry 0).
-// xsb: shared address of the staged x plus the running byte offset is `offb`.
-template <int NT, bool MASKED>
-__device__ __forceinline__ void apply_group(const uint4 q, uint32_t vm, uint32_t tab_s, uint32_t H,
-                                            const uint32_t* __restrict__ gtab, uint32_t& xa, float lmin,
-                                            float lmax, float (&acc)[3][NT]) {
-  // xa = shared address of x[column of the next codeword] (NT == 2: of the
-  // interleaved float2 pair, 8 bytes per column; fields are 4 * position)
+// Entries of the 8 codewords of a group (lookup stage). MASKED: vm bit u set
+// = codeword u belongs to the lane's segment; the others decode as entry 0.
+template <bool MASKED>
+__device__ __forceinline__ void lookup_group(uint32_t (&e)[GRP], const uint4 q, uint32_t vm, uint32_t tab_s,
+                                             uint32_t H, const uint32_t* __restrict__ gtab) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
   for (int u = 0; u < GRP; ++u) {
     uint32_t c = (u & 1) ? (w[u >> 1] >> 16) : (w[u >> 1] & 0xFFFFu);
     if (MASKED) c = ((vm >> u) & 1u) ? c : 0u;
-    const uint32_t e = c < H ? lds_u32(tab_s + 4 * c) : __ldg(gtab + c);
+    e[u] = c < H ? lds_u32(tab_s + 4 * c) : __ldg(gtab + c);
+  }
+}
+
+// Apply stage: per used slot one x gather + FMA. xa = shared address of x at
+// the column of the next codeword (NT == 2: interleaved float2 pairs, 8 bytes
+// per column; entry fields are 4 * position).
+template <int NT>
+__device__ __forceinline__ void apply_group(const uint32_t (&e)[GRP], uint32_t& xa, float lmin, float lmax,
+                                            float (&acc)[3][NT]) {
+#pragma unroll
+  for (int u = 0; u < GRP; ++u) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const uint32_t f = __byte_perm(e, 0u, 0x4440u + j);
-      const float wv = ((e >> (24 + j)) & 1u) ? lmax : lmin;
+      const uint32_t f = __byte_perm(e[u], 0u, 0x4440u + j);
+      const float wv = ((e[u] >> (24 + j)) & 1u) ? lmax : lmin;
       if (f != 0x7Fu) {
         if (NT == 1) {
           const float xv = lds_f32(xa + f);
@@ -163,8 +186,90 @@ __device__ __forceinline__ void apply_group(const uint4 q, uint32_t vm, uint32_t
         }
       }
     }
-    xa += (e >> 28) << (NT == 1 ? 3 : 4);  // 2n columns
+    xa += (e[u] >> 28) << (NT == 1 ? 3 : 4);  // 2n columns
   }
+}
+
+__device__ __forceinline__ uint32_t seg_vm(int lo, int hi) {
+  const int l = max(0, lo), h = min(GRP, max(0, hi));
+  return ((1u << h) - 1u) & ~((1u << l) - 1u);
+}
+
+template <int NT>
+__device__ __forceinline__ void store_row(const SegParams& P, const Run& R, int row, const float (&sum)[NT]) {
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    if (q >= R.ntok) break;
+    const float v = bf16_round_dev(sum[q]);
+    const int64_t t = R.tok[q];
+    if (P.y_mode == QMOE_Y_RELU_BF16) {
+      reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+    } else if (P.y_mode == QMOE_Y_STORE_F32) {
+      reinterpret_cast<float*>(P.y)[t * P.ldy + row] = v + 0.f;  // == 0 + v
+    } else {
+      float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
+      *yp = *yp + v;
+    }
+  }
+}
+
+// PACKED layout task: 32 / G consecutive sorted rows x G segments of whole
+// groups; no masking (padding codewords decode to entry 0), lanes whose
+// segment is shorter than the warp's longest simply idle.
+template <int NT>
+__device__ __forceinline__ void run_task_packed(const SegParams& P, const Run& R, int task, uint32_t xs_s,
+                                                uint32_t tab_s) {
+  const int lane = threadIdx.x & 31;
+  const int lg = R.lg, G = 1 << lg;
+  const int i = R.row0 + (task << (5 - lg)) + (lane >> lg);
+  const int seg = lane & (G - 1);
+  int ga = 0, ng = 0, col = 0;
+  uint32_t mm = 0;
+  if (i < R.row1) {
+    const int gs = __ldg(R.ro + i), m = __ldg(R.ro + i + 1) - gs;
+    ga = gs + ((seg * m) >> lg);
+    ng = gs + (((seg + 1) * m) >> lg) - ga;
+    col = seg && ng ? (int)__ldg(R.ck + ga) : 0;
+    mm = __ldg(R.mm + i);
+  }
+  const int maxg = __reduce_max_sync(FULL_MASK, ng);
+  const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
+  uint32_t xa = xs_s + (uint32_t)col * (NT == 1 ? 4u : 8u);
+  float acc[3][NT];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int q = 0; q < NT; ++q) acc[j][q] = 0.f;
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t* gtab = P.gtab;
+  if (maxg > 0) {
+    // pipeline: group k+2 loading, group k+1 looked up, group k applied
+    const uint16_t* cw = R.cw;
+    const int glast = ga + max(ng, 1) - 1;
+    uint4 q1 = ld_group(cw, min(ga + 1, glast));
+    uint32_t ea[GRP], eb[GRP];
+    if (ng > 0) lookup_group<false>(ea, ld_group(cw, ga), 0xFFu, tab_s, H, gtab);
+    for (int k = 0;;) {
+      uint4 q2 = ld_group(cw, min(ga + k + 2, glast));
+      if (k + 1 < ng) lookup_group<false>(eb, q1, 0xFFu, tab_s, H, gtab);
+      if (k < ng) apply_group<NT>(ea, xa, lmin, lmax, acc);
+      if (++k >= maxg) break;
+      q1 = ld_group(cw, min(ga + k + 2, glast));
+      if (k + 1 < ng) lookup_group<false>(ea, q2, 0xFFu, tab_s, H, gtab);
+      if (k < ng) apply_group<NT>(eb, xa, lmin, lmax, acc);
+      if (++k >= maxg) break;
+    }
+  }
+  float sum[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    sum[q] = (acc[0][q] + acc[1][q]) + acc[2][q];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1)
+      if (d < G) sum[q] += __shfl_xor_sync(FULL_MASK, sum[q], d);
+  }
+  if (i >= R.row1 || seg != 0) return;
+  store_row<NT>(P, R, (int)__ldg(R.rid + i), sum);
 }
 
 template <int NT>
@@ -200,21 +305,37 @@ __device__ __forceinline__ void run_task(const SegParams& P, const Run& R, int t
   const uint32_t H = (uint32_t)P.H;
   const uint32_t* gtab = P.gtab;
   if (maxg > 0) {
+    // pipeline: group i+2 loading, group i+1 looked up, group i applied
     const uint16_t* cw = R.cw;
-    uint4 q0 = ld_group(cw, g0);
+    int lo = A - g0 * GRP, hi = B - g0 * GRP;  // segment in codewords relative to group i
     uint4 q1 = ld_group(cw, min(g0 + 1, glast));
-    int lo = A - g0 * GRP, hi = B - g0 * GRP;  // segment in codewords relative to the current group
-    for (int i = 0; i < maxg; ++i) {
+    uint32_t ea[GRP], eb[GRP];
+    {
+      const uint4 q0 = ld_group(cw, g0);
+      const uint32_t vm = seg_vm(lo, hi);
+      if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(ea, q0, vm, tab_s, H, gtab);
+      else lookup_group<true>(ea, q0, vm, tab_s, H, gtab);
+    }
+    for (int i = 0;;) {
       // groups past this lane's segment re-read its last group (mask 0)
-      const uint4 q2 = ld_group(cw, min(g0 + i + 2, glast));
-      const int l = max(0, lo), h = min(GRP, max(0, hi));
-      const uint32_t vm = ((1u << h) - 1u) & ~((1u << l) - 1u);
-      if (__all_sync(FULL_MASK, vm == 0xFFu))
-        apply_group<NT, false>(q0, vm, tab_s, H, gtab, xa, lmin, lmax, acc);
-      else
-        apply_group<NT, true>(q0, vm, tab_s, H, gtab, xa, lmin, lmax, acc);
-      q0 = q1;
-      q1 = q2;
+      uint4 q2 = ld_group(cw, min(g0 + i + 2, glast));
+      if (i + 1 < maxg) {
+        const uint32_t vm = seg_vm(lo - GRP, hi - GRP);
+        if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(eb, q1, vm, tab_s, H, gtab);
+        else lookup_group<true>(eb, q1, vm, tab_s, H, gtab);
+      }
+      apply_group<NT>(ea, xa, lmin, lmax, acc);
+      if (++i >= maxg) break;
+      lo -= GRP;
+      hi -= GRP;
+      q1 = ld_group(cw, min(g0 + i + 2, glast));
+      if (i + 1 < maxg) {
+        const uint32_t vm = seg_vm(lo - GRP, hi - GRP);
+        if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(ea, q2, vm, tab_s, H, gtab);
+        else lookup_group<true>(ea, q2, vm, tab_s, H, gtab);
+      }
+      apply_group<NT>(eb, xa, lmin, lmax, acc);
+      if (++i >= maxg) break;
       lo -= GRP;
       hi -= GRP;
     }
@@ -228,26 +349,13 @@ __device__ __forceinline__ void run_task(const SegParams& P, const Run& R, int t
       if (d < G) sum[q] += __shfl_xor_sync(FULL_MASK, sum[q], d);
   }
   if (r >= R.row1 || seg != 0) return;
-#pragma unroll
-  for (int q = 0; q < NT; ++q) {
-    if (q >= R.ntok) break;
-    const float v = bf16_round_dev(sum[q]);
-    const int64_t t = R.tok[q];
-    if (P.y_mode == QMOE_Y_RELU_BF16) {
-      reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
-    } else if (P.y_mode == QMOE_Y_STORE_F32) {
-      reinterpret_cast<float*>(P.y)[t * P.ldy + r] = v + 0.f;  // == 0 + v
-    } else {
-      float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + r;
-      *yp = *yp + v;
-    }
-  }
+  store_row<NT>(P, R, r, sum);
 }
 
+template <bool PACKED>
 __global__ void __launch_bounds__(THREADS, 1) seg_matvec_kernel(SegParams P) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
-  char* xs = reinterpret_cast<char*>(smem + (size_t)P.H * 4);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(seg_smem);
+  char* xs = reinterpret_cast<char*>(seg_smem + (size_t)P.H * 4);
   __shared__ int s_run;
 
   int n_runs, total;
@@ -302,10 +410,15 @@ __global__ void __launch_bounds__(THREADS, 1) seg_matvec_kernel(SegParams P) {
         x1[i] = i < R.cols ? load_x(P.x, P.x_bf16, (int64_t)R.tok[0] * P.ldx + i) : 0.f;
     }
     __syncthreads();
-    const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(xs), tab_s = (uint32_t)__cvta_generic_to_shared(tab);
+    const uint32_t tab_s = smem_base(), xs_s = tab_s + (uint32_t)P.H * 4;
     for (int k = a + warp; k < b; k += NWARPS) {
-      if (R.ntok > 1) run_task<2>(P, R, k - R.task0, xs_s, tab_s);
-      else run_task<1>(P, R, k - R.task0, xs_s, tab_s);
+      if (PACKED) {
+        if (R.ntok > 1) run_task_packed<2>(P, R, k - R.task0, xs_s, tab_s);
+        else run_task_packed<1>(P, R, k - R.task0, xs_s, tab_s);
+      } else {
+        if (R.ntok > 1) run_task<2>(P, R, k - R.task0, xs_s, tab_s);
+        else run_task<1>(P, R, k - R.task0, xs_s, tab_s);
+      }
     }
     t = b;
   }
@@ -323,7 +436,8 @@ int hot_override() {
   return v;
 }
 
-int launch_seg(const qmoe_dict* d, SegParams& P, int max_cols, int ntmax, int grid, int hot_want, cudaStream_t st) {
+int launch_seg(const qmoe_dict* d, SegParams& P, bool packed, int max_cols, int ntmax, int grid, int hot_want,
+               cudaStream_t st) {
   P.xcap = ((max_cols + 32 + 15) / 16) * 16;
   const size_t xbytes = (size_t)std::max(1, ntmax) * P.xcap * 4;
   const size_t static_smem = 64;
@@ -335,8 +449,13 @@ int launch_seg(const qmoe_dict* d, SegParams& P, int max_cols, int ntmax, int gr
   H = std::max(H & ~255, 256);
   P.H = H;
   const size_t smem = (size_t)H * 4 + xbytes;
-  CK(cudaFuncSetAttribute(seg_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-  seg_matvec_kernel<<<grid, THREADS, smem, st>>>(P);
+  if (packed) {
+    CK(cudaFuncSetAttribute(seg_matvec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    seg_matvec_kernel<true><<<grid, THREADS, smem, st>>>(P);
+  } else {
+    CK(cudaFuncSetAttribute(seg_matvec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    seg_matvec_kernel<false><<<grid, THREADS, smem, st>>>(P);
+  }
   CK(cudaGetLastError(), "seg_matvec_kernel launch");
   return QMOE_OK;
 }
@@ -488,7 +607,7 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
     // small launches stage a smaller hot table (the fill is per CTA)
     const int64_t est_cw = rows * cols / 24 + rows;
     const int want = (int)std::min<int64_t>(QMOE_DICT_SIZE, std::max<int64_t>(4096, est_cw / grid * 2));
-    const int rc = launch_seg(d, P, (int)cols, ntok > 1 ? 2 : 1, grid, want, S(stream));
+    const int rc = launch_seg(d, P, false, (int)cols, ntok > 1 ? 2 : 1, grid, want, S(stream));
     if (rc == QMOE_OK && d_bad) {
       // rows must have been validated (qmoe_validate_rows); nothing further to flag
     }
@@ -527,6 +646,8 @@ int qmoe_fused_matmat(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_
 int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work* d_work, const int32_t* d_n_work,
                         int32_t max_work, int32_t max_cols, int32_t max_ntok, const void* d_x, int x_dtype,
                         int64_t ldx, void* d_y, int y_mode, int64_t ldy, int32_t* d_bad, void* stream) {
+  const bool packed = (y_mode & QMOE_RUNS_PACKED) != 0;
+  y_mode &= ~QMOE_RUNS_PACKED;
   if (!d || !d->d_stab || !d_work || !d_n_work || max_work < 0 || max_cols <= 0 || max_ntok < 1 ||
       max_ntok > QMOE_NT_MAX || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16) ||
       (y_mode != QMOE_Y_ACCUM_F32 && y_mode != QMOE_Y_RELU_BF16 && y_mode != QMOE_Y_STORE_F32))
@@ -548,9 +669,9 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
     P.y = d_y;
     P.y_mode = y_mode;
     P.ldy = ldy;
-    return launch_seg(d, P, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
+    return launch_seg(d, P, packed, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
   }
-  if (d_table) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
+  if (d_table || packed) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks / packed runs need a <=3-non-zero dictionary");
   GeneralParams G{};
   G.words = d->d_words;
   G.work = d_work;

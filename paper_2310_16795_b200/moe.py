@@ -60,8 +60,15 @@ class CompressedMoELayer:
                 self.codebook.apply(mats)
             elif len({id(m.codebook) for m in mats}) == 1:
                 self.codebook = mats[0].codebook
-        for m in list(wi) + list(wo):  # row-segment checkpoints (kernel-private)
-            if m.ck is None and m.lg == 0:
+        import os
+
+        self.packed = (bool(dic.device_info(self.device.index)["sparse_path"])
+                       and os.environ.get("QMOE_LAYOUT", "raw") == "packed")
+        for m in list(wi) + list(wo):  # kernel-private PACKED layout (or row checkpoints)
+            if self.packed:
+                if m.packed is None:
+                    m.build_layout(dic)
+            elif m.ck is None and m.lg == 0:
                 m.build_checkpoints(dic)
         descs = (_lib.QmoeMatrix * (2 * self.E))()
         for e in range(self.E):
@@ -72,6 +79,9 @@ class CompressedMoELayer:
         self.tokens_per_unit = min(int(tokens_per_unit), _lib.NT_STREAM)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
                                      np.int64)
+        self.mean_groups = (float(np.mean([m.packed["mean_groups"] for m in wi])) if self.packed else 0.0,
+                            float(np.mean([m.packed["mean_groups"] for m in wo])) if self.packed else 0.0)
+        self._lanes = {}
         self._alloc(max_tokens)
 
     def _alloc(self, T: int) -> None:
@@ -96,12 +106,36 @@ class CompressedMoELayer:
                 and x.stride(1) == 1)
 
     # ------------------------------------------------------------------ device step
+    LANES = 148 * 768  # resident lanes of the streaming kernel on a B200 (1 CTA x 24 warps per SM)
+
+    def lanes_per_row(self, T: int) -> tuple[int, int]:
+        """log2 lanes per row (wi, wo) for a step of T tokens: enough lane
+        segments to fill the GPU about twice (expected distinct experts under
+        uniform routing), but segments of at least ~2 groups."""
+        if not self.packed:
+            return (-1, -1)
+        hit = self._lanes.get(T)
+        if hit is None:
+            runs = max(1.0, self.E * (1.0 - (1.0 - 1.0 / self.E) ** T))
+            out = []
+            for rows, mg in ((self.d_ff, self.mean_groups[0]), (self.d_model, self.mean_groups[1])):
+                lg = 0
+                while lg < 5 and runs * rows * (1 << lg) < 2 * self.LANES and mg / (1 << (lg + 1)) >= 2.0:
+                    lg += 1
+                out.append(lg)
+            hit = self._lanes[T] = tuple(out)
+        return hit
+
     def plan(self, assign, stream=None) -> None:
         T = assign.shape[0]
+        lg_wi, lg_wo = self.lanes_per_row(T)
         _lib.check(_lib.lib.qmoe_moe_plan(
-            _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit, self.max_units,
+            _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit, lg_wi, lg_wo, self.max_units,
             _lib.ptr(self.units_wi), _lib.ptr(self.units_wo),
             _lib.ptr(self.n_units), _lib.ptr(self.expert_count), _lib.ptr(self.order), _lib.stream_ptr(stream)))
+
+    def _flag(self) -> int:
+        return _lib.QMOE_RUNS_PACKED if self.packed else 0
 
     def _table(self) -> int:
         return self.codebook.table.data_ptr() if self.codebook is not None else 0
@@ -113,13 +147,13 @@ class CompressedMoELayer:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
             self.handle, self._table(), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
             self.d_model, self.tokens_per_unit, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h),
-            _lib.QMOE_Y_RELU_BF16, self.h.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
+            _lib.QMOE_Y_RELU_BF16 | self._flag(), self.h.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def pass_wo(self, out, stream=None) -> None:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
             self.handle, self._table(), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 8, self.max_units,
             self.d_ff, self.tokens_per_unit, _lib.ptr(self.h), _lib.QMOE_X_BF16, self.h.stride(0), _lib.ptr(out),
-            _lib.QMOE_Y_STORE_F32, out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
+            _lib.QMOE_Y_STORE_F32 | self._flag(), out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def forward_device(self, x, assign, out=None, stream=None):
         """x: (T, d_model) CUDA bf16/f32, assign: (T,) CUDA int32 expert ids.

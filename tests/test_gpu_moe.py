@@ -140,7 +140,7 @@ def test_moe_segmented_rows_vs_oracle(dic, odic, d_model, d_ff):
             pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
         host.append(tuple(pair))
     layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=8)
-    assert max(m.lg for m in wo) >= 1
+    assert layer.lanes_per_row(7)[1] >= 1 or max(m.lg for m in wo) >= 1  # several lanes per wo row
     x = q.bf16_round(rng.normal(size=(7, d_model)).astype(np.float32))
     assign = np.array([0, 1, 2, 0, 0, 2, 1], np.int32)
     y = layer.forward(x, assign)
