@@ -185,11 +185,15 @@ int qmoe_fused_matmat(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_r
  * own order, or a codebook from qmoe_codebook_table (streams re-indexed with
  * qmoe_remap; the codebook must map dictionary entry 0 to rank 0). Rows must
  * have been validated (qmoe_validate_rows); d_bad is used by the general
- * (> 3 non-zero) path only. */
+ * (> 3 non-zero) path only. hot_entries: entries of the table staged in
+ * shared memory per SM (0 = as many as fit); small launches should stage few.
+ * RAW runs: bits 0-7 of work.lg = lanes per row of the run (log2), bits 8-15 =
+ * the checkpoint granularity the matrix stores (0 = same); a run may use any
+ * lg <= the stored one (segment boundaries nest). */
 int qmoe_grouped_matvec(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_work* d_work,
                         const int32_t* d_n_work, int32_t max_work, int32_t max_cols,
                         int32_t max_ntok, const void* d_x, int x_dtype, int64_t ldx, void* d_y,
-                        int y_mode, int64_t ldy, int32_t* d_bad, void* stream);
+                        int y_mode, int64_t ldy, int32_t hot_entries, int32_t* d_bad, void* stream);
 
 /* ------------------------------------------------------- frequency codebook
  * Kernel-private re-indexing of the codeword streams of one model/layer by

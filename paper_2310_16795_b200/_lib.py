@@ -69,7 +69,7 @@ _SIGS = {
     "qmoe_fused_matvec": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, vp, vp, vp]),
     "qmoe_fused_matmat": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, vp, ctypes.c_int, i64, i64, vp, i64, vp, vp]),
     "qmoe_grouped_matvec": (ctypes.c_int, [vp, vp, vp, vp, i32, i32, i32, vp, ctypes.c_int, i64, vp,
-                                           ctypes.c_int, i64, vp, vp]),
+                                           ctypes.c_int, i64, i32, vp, vp]),
     "qmoe_histogram": (ctypes.c_int, [vp, i64, vp, vp]),
     "qmoe_codebook_table": (ctypes.c_int, [vp, vp, vp]),
     "qmoe_remap": (ctypes.c_int, [vp, i64, vp, vp, vp]),

@@ -393,8 +393,11 @@ __device__ __forceinline__ int4 block_scan_excl(int4 v, int4* wsum, int4* total)
   return make_int4(b.x + incl.x - v.x, b.y + incl.y - v.y, b.z + incl.z - v.z, b.w + incl.w - v.w);
 }
 
+// lanes per row of a run: the override, bounded (RAW) by the checkpoint
+// granularity the matrix stores (M.lg); PACKED matrices take any lg
 __device__ __forceinline__ int plan_lg(const qmoe_matrix& M, int lg_over) {
-  return (M.row_id && lg_over >= 0) ? lg_over : M.lg;
+  if (lg_over < 0) return M.lg;
+  return M.row_id ? lg_over : min(lg_over, M.lg);
 }
 
 __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restrict__ assign, int T, int E,
@@ -489,11 +492,12 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
       U.row_minmax = M.row_minmax;
       U.ck = M.ck;
       U.row_id = M.row_id;
-      U.lg = plan_lg(M, pass ? lg_wo : lg_wi);
+      const int rlg = plan_lg(M, pass ? lg_wo : lg_wi);
+      U.lg = M.row_id ? rlg : (rlg | (M.lg << 8));  // RAW: checkpoint stride in bits 8-15
       U.cols = M.cols;
       U.row0 = 0;
       U.row1 = M.rows;
-      U.task0 = (pass ? two[e] : twi[e]) + ch * run_tasks_dev(M.rows, U.lg);
+      U.task0 = (pass ? two[e] : twi[e]) + ch * run_tasks_dev(M.rows, rlg);
       (pass ? runs_wo : runs_wi)[i] = U;
     }
   }

@@ -65,6 +65,7 @@ struct SegParams {
   int y_mode;
   int64_t ldy;
   int xcap;                   // x elements staged per token
+  int xbytes;                 // x staging bytes (pipe kernel: several runs' slots)
 };
 
 struct Run {
@@ -73,7 +74,7 @@ struct Run {
   const uint32_t* mm;
   const uint16_t* ck;
   const uint16_t* rid;  // PACKED layout when non-null
-  int cols, row0, row1, lg, ntok, task0;
+  int cols, row0, row1, lg, cklg, ntok, task0;
   int tok[NT_STREAM];
 };
 
@@ -91,7 +92,8 @@ __device__ __forceinline__ Run get_run(const SegParams& P, int r) {
     R.cols = W.cols;
     R.row0 = W.row0;
     R.row1 = W.row1;
-    R.lg = W.lg;
+    R.lg = W.lg & 0xFF;                                        // lanes per row of this run
+    R.cklg = (W.lg >> 8) & 0xFF ? (W.lg >> 8) & 0xFF : R.lg;  // checkpoint stride of the matrix
     R.ntok = W.ntok;
     R.task0 = W.task0;
     R.tok[0] = W.tok[0];
@@ -106,6 +108,7 @@ __device__ __forceinline__ Run get_run(const SegParams& P, int r) {
     R.row0 = 0;
     R.row1 = P.single.rows;
     R.lg = 0;
+    R.cklg = 0;
     const int64_t t0 = (int64_t)r * NT_STREAM;
     R.ntok = (int)min((int64_t)NT_STREAM, P.ntok_single - t0);
     R.task0 = r * run_tasks(P.single.rows, 0);
@@ -285,7 +288,7 @@ __device__ __forceinline__ void run_task(const SegParams& P, const Run& R, int t
     const int n = e - s;
     A = s + ((seg * n) >> lg);
     B = s + (((seg + 1) * n) >> lg);
-    off = seg ? (int)__ldg(R.ck + (size_t)r * (G - 1) + seg - 1) : 0;
+    off = seg ? (int)__ldg(R.ck + (size_t)r * ((1 << R.cklg) - 1) + (seg << (R.cklg - lg)) - 1) : 0;
     mm = __ldg(R.mm + r);
   }
   const bool has = B > A;
@@ -424,6 +427,253 @@ __global__ void __launch_bounds__(THREADS, 1) seg_matvec_kernel(SegParams P) {
   }
 }
 
+// ----------------------------------------------------------------- pipelined raw kernel
+// pipe_matvec_kernel — the RAW-layout product path. Same decode/apply stages
+// as above, but each warp treats the lane segments of its successive tasks as
+// ONE continuous stream of codeword groups: the next task's row metadata is
+// loaded a whole task ahead, and its first groups are loaded and looked up
+// during the current task's last steps, so no task pays a dependent DRAM
+// round trip at its start. A CTA stages the x rows of every run of its task
+// range up front (a window of up to WIN_RUNS runs / the x budget), so there is
+// no barrier between runs inside a window.
+constexpr int WIN_RUNS = 16;
+
+struct WinRun {
+  const uint16_t* cw;
+  const int32_t* ro;
+  const uint32_t* mm;
+  const uint16_t* ck;
+  int cols, row0, row1, lg, cklg, ntok, task0, task1, xoff;
+  int tok[NT_STREAM];
+};
+
+struct Lane {  // one lane's segment of one task
+  int A, B, off, row;
+  uint32_t mm;
+};
+
+__device__ __forceinline__ Lane lane_task(const WinRun& W, int k) {
+  const int lane = threadIdx.x & 31;
+  const int lg = W.lg, G = 1 << lg;
+  const int r = W.row0 + ((k - W.task0) << (5 - lg)) + (lane >> lg);
+  const int seg = lane & (G - 1);
+  Lane L{0, 0, 0, -1, 0u};
+  if (r < W.row1) {
+    const int s = __ldg(W.ro + r), e = __ldg(W.ro + r + 1);
+    const int n = e - s;
+    L.A = s + ((seg * n) >> lg);
+    L.B = s + (((seg + 1) * n) >> lg);
+    L.off = seg ? (int)__ldg(W.ck + (size_t)r * ((1 << W.cklg) - 1) + (seg << (W.cklg - lg)) - 1) : 0;
+    L.mm = __ldg(W.mm + r);
+    L.row = r;
+  }
+  return L;
+}
+
+__device__ __forceinline__ int lane_groups(const Lane& L) { return L.B > L.A ? (L.B - 1) / GRP - L.A / GRP + 1 : 0; }
+
+__device__ __forceinline__ uint4 lane_load(const uint16_t* cw, const Lane& L, int i) {
+  if (L.B <= L.A) return make_uint4(0u, 0u, 0u, 0u);
+  const int g0 = L.A / GRP, gl = (L.B - 1) / GRP;
+  return ld_group(cw, min(g0 + i, gl));
+}
+
+__device__ __forceinline__ uint32_t lane_vm(const Lane& L, int i) {
+  const int base = (L.A / GRP + i) * GRP;
+  return seg_vm(L.A - base, L.B - base);
+}
+
+__device__ __forceinline__ void lookup_any(uint32_t (&e)[GRP], const uint4 q, uint32_t vm, uint32_t tab_s, uint32_t H,
+                                           const uint32_t* __restrict__ gtab) {
+  if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(e, q, vm, tab_s, H, gtab);
+  else lookup_group<true>(e, q, vm, tab_s, H, gtab);
+}
+
+__global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
+  uint32_t* tab = reinterpret_cast<uint32_t*>(seg_smem);
+  __shared__ WinRun win[WIN_RUNS];
+  __shared__ int s_run, s_nwin, s_wend;
+
+  int n_runs, total;
+  if (P.runs) {
+    n_runs = min(P.n_runs[0], P.max_runs);
+    total = P.n_runs[1];
+  } else {
+    n_runs = (int)((P.ntok_single + NT_STREAM - 1) / NT_STREAM);
+    total = n_runs * run_tasks(P.single.rows, 0);
+  }
+  if (n_runs <= 0) return;
+  const int t_begin = (int)((int64_t)total * blockIdx.x / gridDim.x);
+  const int t_end = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
+  if (t_begin >= t_end) return;
+  {  // hot table prefix: vectorised copy by all threads
+    const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
+    uint4* dst = reinterpret_cast<uint4*>(tab);
+    for (int i = threadIdx.x; i < P.H / 4; i += THREADS) dst[i] = __ldg(src + i);
+  }
+  if (threadIdx.x == 0) {  // run holding t_begin: last run with task0 <= t_begin
+    int lo = 0, hi = n_runs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (get_run(P, mid).task0 <= t_begin) lo = mid;
+      else hi = mid - 1;
+    }
+    s_run = lo;
+  }
+  const uint32_t tab_s = smem_base(), xs_s = tab_s + (uint32_t)P.H * 4;
+  char* xs = reinterpret_cast<char*>(seg_smem + (size_t)P.H * 4);
+  const int warp = threadIdx.x >> 5;
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t* gtab = P.gtab;
+  int t = t_begin;
+  while (t < t_end) {
+    __syncthreads();  // previous window done with xs / win (and s_run published)
+    if (threadIdx.x == 0) {  // next window: consecutive runs whose x slots fit the budget
+      int ri = s_run, nw = 0, xo = 0, wend = t;
+      while (ri < n_runs && nw < WIN_RUNS && wend < t_end) {
+        const Run R = get_run(P, ri);
+        const int r_end = R.task0 + run_tasks(R.row1 - R.row0, R.lg);
+        const int need = ((R.ntok > 1 ? 8 : 4) * (R.cols + 32) + 15) & ~15;
+        if (nw > 0 && xo + need > P.xbytes) break;
+        if (r_end > t) {
+          WinRun& W = win[nw++];
+          W.cw = R.cw; W.ro = R.ro; W.mm = R.mm; W.ck = R.ck;
+          W.cols = R.cols; W.row0 = R.row0; W.row1 = R.row1; W.lg = R.lg; W.cklg = R.cklg; W.ntok = R.ntok;
+          W.task0 = R.task0; W.task1 = r_end; W.xoff = xo;
+          W.tok[0] = R.tok[0]; W.tok[1] = R.tok[1];
+          xo += need;
+          wend = min(t_end, r_end);
+        }
+        if (r_end > t_end) break;
+        ++ri;
+      }
+      s_nwin = nw;
+      s_wend = wend;
+      s_run = ri;  // first run of the next window
+    }
+    __syncthreads();
+    const int nw = s_nwin, wend = s_wend;
+    for (int w = 0; w < nw; ++w) {  // stage x (fp32; two tokens interleaved)
+      const WinRun& W = win[w];
+      if (W.ntok > 1) {
+        float2* x2 = reinterpret_cast<float2*>(xs + W.xoff);
+        for (int i = threadIdx.x; i < W.cols + 32; i += THREADS) {
+          float v0 = 0.f, v1 = 0.f;
+          if (i < W.cols) {
+            v0 = load_x(P.x, P.x_bf16, (int64_t)W.tok[0] * P.ldx + i);
+            v1 = load_x(P.x, P.x_bf16, (int64_t)W.tok[1] * P.ldx + i);
+          }
+          x2[i] = make_float2(v0, v1);
+        }
+      } else {
+        float* x1 = reinterpret_cast<float*>(xs + W.xoff);
+        for (int i = threadIdx.x; i < W.cols + 32; i += THREADS)
+          x1[i] = i < W.cols ? load_x(P.x, P.x_bf16, (int64_t)W.tok[0] * P.ldx + i) : 0.f;
+      }
+    }
+    __syncthreads();
+    // ---- per-warp pipelined walk over tasks k = t + warp, + NWARPS, ... < wend
+    int k = t + warp;
+    if (k < wend) {
+      int wc = 0;
+      while (win[wc].task1 <= k) ++wc;
+      Lane c = lane_task(win[wc], k);
+      int wn = wc;
+      int kn = k + NWARPS;
+      bool has_n = kn < wend;
+      Lane n{0, 0, 0, -1, 0u};
+      if (has_n) {
+        while (win[wn].task1 <= kn) ++wn;
+        n = lane_task(win[wn], kn);
+      }
+      int maxgc = __reduce_max_sync(FULL_MASK, lane_groups(c));
+      int maxgn = 0;
+      bool nready = false;
+      uint32_t ea[GRP], eb[GRP];
+      uint4 q1;
+      {
+        const uint4 q0 = lane_load(win[wc].cw, c, 0);
+        if (maxgc >= 2) q1 = lane_load(win[wc].cw, c, 1);
+        else q1 = has_n ? lane_load(win[wn].cw, n, 0) : make_uint4(0u, 0u, 0u, 0u);
+        lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
+      }
+      for (;;) {
+        const WinRun& W = win[wc];
+        const int NTc = W.ntok > 1 ? 2 : 1;
+        const float lmin = __uint_as_float(c.mm << 16), lmax = __uint_as_float(c.mm & 0xFFFF0000u);
+        const uint32_t offb = (uint32_t)(c.off * 4) - (uint32_t)((c.A - (c.A / GRP) * GRP) * P.z_bytes);
+        uint32_t xa = xs_s + (uint32_t)W.xoff + (NTc == 1 ? offb : 2 * offb);
+        float acc[3][2];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) acc[j][0] = acc[j][1] = 0.f;
+        for (int i = 0; i < maxgc; ++i) {
+          // prefetch element i + 2 of the stream (this task, then the next)
+          uint4 q2 = make_uint4(0u, 0u, 0u, 0u);
+          if (i + 2 < maxgc) {
+            q2 = lane_load(W.cw, c, i + 2);
+          } else if (has_n) {
+            if (!nready) {
+              maxgn = __reduce_max_sync(FULL_MASK, lane_groups(n));
+              nready = true;
+            }
+            if (i + 2 - maxgc < maxgn) q2 = lane_load(win[wn].cw, n, i + 2 - maxgc);
+          }
+          // look element i + 1 up (raw in q1)
+          if (i + 1 < maxgc) lookup_any(eb, q1, lane_vm(c, i + 1), tab_s, H, gtab);
+          else if (has_n) lookup_any(eb, q1, lane_vm(n, 0), tab_s, H, gtab);
+          // apply element i
+          if (NTc == 1) {
+            float a1[3][1] = {{acc[0][0]}, {acc[1][0]}, {acc[2][0]}};
+            apply_group<1>(ea, xa, lmin, lmax, a1);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) acc[j][0] = a1[j][0];
+          } else {
+            apply_group<2>(ea, xa, lmin, lmax, acc);
+          }
+#pragma unroll
+          for (int u = 0; u < GRP; ++u) ea[u] = eb[u];
+          q1 = q2;
+        }
+        // row sums over the G lanes of a row (fixed order), bf16 epilogue
+        float sum[2];
+        const int G = 1 << W.lg;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          sum[q] = (acc[0][q] + acc[1][q]) + acc[2][q];
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1)
+            if (d < G) sum[q] += __shfl_xor_sync(FULL_MASK, sum[q], d);
+        }
+        if (c.row >= 0 && ((threadIdx.x & 31) & (G - 1)) == 0) {
+          Run R;
+          R.ntok = W.ntok;
+          R.tok[0] = W.tok[0];
+          R.tok[1] = W.tok[1];
+          store_row<2>(P, R, c.row, sum);
+        }
+        if (!has_n) break;
+        // advance: next becomes current; load the task after it
+        if (!nready) maxgn = __reduce_max_sync(FULL_MASK, lane_groups(n));
+        c = n;
+        wc = wn;
+        maxgc = maxgn;
+        k = kn;
+        kn = k + NWARPS;
+        has_n = kn < wend;
+        nready = false;
+        if (has_n) {
+          while (win[wn].task1 <= kn) ++wn;
+          n = lane_task(win[wn], kn);
+        }
+        // pipeline invariant: ea = entries(c, 0); q1 = raw(c, 1) if maxgc >= 2,
+        // else raw(next, 0) — not prefetched yet in that case
+        if (maxgc < 2) q1 = has_n ? lane_load(win[wn].cw, n, 0) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    t = wend;
+  }
+}
+
 // ----------------------------------------------------------------- host side
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -439,8 +689,11 @@ int hot_override() {
 int launch_seg(const qmoe_dict* d, SegParams& P, bool packed, int max_cols, int ntmax, int grid, int hot_want,
                cudaStream_t st) {
   P.xcap = ((max_cols + 32 + 15) / 16) * 16;
-  const size_t xbytes = (size_t)std::max(1, ntmax) * P.xcap * 4;
-  const size_t static_smem = 64;
+  const size_t slot = (size_t)std::max(1, ntmax) * P.xcap * 4;
+  // the pipelined kernel stages several runs' x at once (up to ~48 KB)
+  const size_t xbytes = packed || getenv("QMOE_SEG_V1") ? slot : std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
+  P.xbytes = (int)xbytes;
+  const size_t static_smem = 2048;  // kernels' static __shared__ (run window)
   if (xbytes + static_smem + 4096 > (size_t)d->max_smem_optin)
     return qmoe::fail(QMOE_EUNSUPPORTED, "cols too large for the shared-memory x staging buffer");
   int H = (int)((d->max_smem_optin - xbytes - static_smem - 256) / 4);
@@ -452,9 +705,12 @@ int launch_seg(const qmoe_dict* d, SegParams& P, bool packed, int max_cols, int 
   if (packed) {
     CK(cudaFuncSetAttribute(seg_matvec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
     seg_matvec_kernel<true><<<grid, THREADS, smem, st>>>(P);
-  } else {
+  } else if (getenv("QMOE_SEG_V1")) {
     CK(cudaFuncSetAttribute(seg_matvec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
     seg_matvec_kernel<false><<<grid, THREADS, smem, st>>>(P);
+  } else {
+    CK(cudaFuncSetAttribute(pipe_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    pipe_matvec_kernel<<<grid, THREADS, smem, st>>>(P);
   }
   CK(cudaGetLastError(), "seg_matvec_kernel launch");
   return QMOE_OK;
@@ -645,7 +901,8 @@ int qmoe_fused_matmat(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_
 
 int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work* d_work, const int32_t* d_n_work,
                         int32_t max_work, int32_t max_cols, int32_t max_ntok, const void* d_x, int x_dtype,
-                        int64_t ldx, void* d_y, int y_mode, int64_t ldy, int32_t* d_bad, void* stream) {
+                        int64_t ldx, void* d_y, int y_mode, int64_t ldy, int32_t hot_entries, int32_t* d_bad,
+                        void* stream) {
   const bool packed = (y_mode & QMOE_RUNS_PACKED) != 0;
   y_mode &= ~QMOE_RUNS_PACKED;
   if (!d || !d->d_stab || !d_work || !d_n_work || max_work < 0 || max_cols <= 0 || max_ntok < 1 ||
@@ -669,7 +926,8 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
     P.y = d_y;
     P.y_mode = y_mode;
     P.ldy = ldy;
-    return launch_seg(d, P, packed, max_cols, max_ntok, d->num_sms, QMOE_DICT_SIZE, S(stream));
+    return launch_seg(d, P, packed, max_cols, max_ntok, d->num_sms, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE,
+                      S(stream));
   }
   if (d_table || packed) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks / packed runs need a <=3-non-zero dictionary");
   GeneralParams G{};

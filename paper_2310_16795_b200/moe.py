@@ -64,12 +64,18 @@ class CompressedMoELayer:
 
         self.packed = (bool(dic.device_info(self.device.index)["sparse_path"])
                        and os.environ.get("QMOE_LAYOUT", "raw") == "packed")
-        for m in list(wi) + list(wo):  # kernel-private PACKED layout (or row checkpoints)
-            if self.packed:
-                if m.packed is None:
-                    m.build_layout(dic)
-            elif m.ck is None and m.lg == 0:
-                m.build_checkpoints(dic)
+        # mean 8-codeword groups per row (wi, wo): lane-segment sizing
+        self.mean_groups = tuple(float(np.mean([m.n_codewords / max(1, m.rows) / 8 for m in ms])) for ms in (wi, wo))
+        # most lanes per row a step may use: segments of >= ~2 groups
+        self.max_lg = tuple(max(0, min(self.MAX_LG, int(np.floor(np.log2(max(1.0, mg / 2)))))) for mg in self.mean_groups)
+        for kind, ms in enumerate((wi, wo)):  # kernel-private PACKED layout (or row checkpoints)
+            for m in ms:
+                if self.packed:
+                    if m.packed is None:
+                        m.build_layout(dic)
+                elif m.ck is None and m.lg == 0 and self.max_lg[kind] > 0:
+                    # checkpoints for 2^max_lg lanes per row; a run may use any 2^lg <= that
+                    m.build_checkpoints(dic, lg=self.max_lg[kind])
         descs = (_lib.QmoeMatrix * (2 * self.E))()
         for e in range(self.E):
             descs[2 * e] = _lib.QmoeMatrix(*wi[e].descriptor())
@@ -79,9 +85,8 @@ class CompressedMoELayer:
         self.tokens_per_unit = min(int(tokens_per_unit), _lib.NT_STREAM)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
                                      np.int64)
-        self.mean_groups = (float(np.mean([m.packed["mean_groups"] for m in wi])) if self.packed else 0.0,
-                            float(np.mean([m.packed["mean_groups"] for m in wo])) if self.packed else 0.0)
         self._lanes = {}
+        self._T = max_tokens
         self._alloc(max_tokens)
 
     def _alloc(self, T: int) -> None:
@@ -107,27 +112,42 @@ class CompressedMoELayer:
 
     # ------------------------------------------------------------------ device step
     LANES = 148 * 768  # resident lanes of the streaming kernel on a B200 (1 CTA x 24 warps per SM)
+    MAX_LG = 3  # RAW layout: checkpoints stored for 8 lanes per row (any 1/2/4/8 usable)
+
+    def _runs_est(self, T: int) -> float:
+        """expected distinct experts of a step under uniform top-1 routing"""
+        return max(1.0, self.E * (1.0 - (1.0 - 1.0 / self.E) ** T))
 
     def lanes_per_row(self, T: int) -> tuple[int, int]:
         """log2 lanes per row (wi, wo) for a step of T tokens: enough lane
-        segments to fill the GPU about twice (expected distinct experts under
-        uniform routing), but segments of at least ~2 groups."""
-        if not self.packed:
-            return (-1, -1)
+        segments to fill the GPU about twice, but segments of at least
+        ~2 groups (shorter ones waste their partial groups)."""
         hit = self._lanes.get(T)
         if hit is None:
-            runs = max(1.0, self.E * (1.0 - (1.0 - 1.0 / self.E) ** T))
+            runs = self._runs_est(T)
             out = []
-            for rows, mg in ((self.d_ff, self.mean_groups[0]), (self.d_model, self.mean_groups[1])):
+            for kind, (rows, mg) in enumerate(((self.d_ff, self.mean_groups[0]), (self.d_model, self.mean_groups[1]))):
+                cap = 5 if self.packed else max(m.lg for m in (self.wi if kind == 0 else self.wo))
                 lg = 0
-                while lg < 5 and runs * rows * (1 << lg) < 2 * self.LANES and mg / (1 << (lg + 1)) >= 2.0:
+                while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES and mg / (1 << (lg + 1)) >= 2.0:
                     lg += 1
                 out.append(lg)
             hit = self._lanes[T] = tuple(out)
         return hit
 
+    def hot_entries(self, T: int, wi: bool) -> int:
+        """table entries to stage per SM: ~4x the codewords one SM decodes in
+        the pass (small steps stage little: the fill is per CTA per launch)"""
+        cw = self._runs_est(T) * (self.d_ff if wi else self.d_model) * 8 * self.mean_groups[0 if wi else 1]
+        want = 4 * cw / 148
+        h = 4096
+        while h < want and h < 65536:
+            h *= 2
+        return h
+
     def plan(self, assign, stream=None) -> None:
         T = assign.shape[0]
+        self._T = T
         lg_wi, lg_wo = self.lanes_per_row(T)
         _lib.check(_lib.lib.qmoe_moe_plan(
             _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit, lg_wi, lg_wo, self.max_units,
@@ -147,13 +167,15 @@ class CompressedMoELayer:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
             self.handle, self._table(), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
             self.d_model, self.tokens_per_unit, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h),
-            _lib.QMOE_Y_RELU_BF16 | self._flag(), self.h.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
+            _lib.QMOE_Y_RELU_BF16 | self._flag(), self.h.stride(0), self.hot_entries(self._T, True),
+            _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def pass_wo(self, out, stream=None) -> None:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
             self.handle, self._table(), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 8, self.max_units,
             self.d_ff, self.tokens_per_unit, _lib.ptr(self.h), _lib.QMOE_X_BF16, self.h.stride(0), _lib.ptr(out),
-            _lib.QMOE_Y_STORE_F32 | self._flag(), out.stride(0), _lib.ptr(self.bad), _lib.stream_ptr(stream)))
+            _lib.QMOE_Y_STORE_F32 | self._flag(), out.stride(0), self.hot_entries(self._T, False),
+            _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def forward_device(self, x, assign, out=None, stream=None):
         """x: (T, d_model) CUDA bf16/f32, assign: (T,) CUDA int32 expert ids.
