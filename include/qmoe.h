@@ -276,6 +276,25 @@ int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matr
                   qmoe_work* d_runs_wo, int32_t* d_n, int32_t* d_expert_count, int32_t* d_order,
                   void* stream);
 
+/* One MoE layer step in ONE cooperative persistent launch (the fused form of
+ * qmoe_moe_plan + two qmoe_grouped_matvec passes): every CTA rebuilds the
+ * dispatcher plan of d_assign[T] in shared memory, runs its share of the wi
+ * tasks (h = relu(bf16(wi_e x_t)) stored bf16 in d_h rows of ldh), publishes
+ * per-run completion counters, and runs its share of the wo tasks, each wo run
+ * waiting only for its own wi run (d_y rows of ldy = bf16(wo_e h_t), f32).
+ * Experts: d_mats[2e] = wi_e (d_ff x d_model), d_mats[2e+1] = wo_e, RAW layout;
+ * lg_wi / lg_wo <= the checkpoint lg every wi / wo matrix stores.
+ * d_counters: int32[T + 1], zero before the first call; the kernel leaves it
+ * zeroed. d_order / d_expert_count (nullable) receive the plan as in
+ * qmoe_moe_plan. QMOE_EUNSUPPORTED when E and T do not fit the shared-memory
+ * plan (use the grouped path). */
+int qmoe_moe_step(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_assign, int32_t T,
+                  int32_t E, const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi,
+                  int32_t lg_wo, int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype,
+                  int64_t ldx, uint16_t* d_h, int64_t ldh, float* d_y, int64_t ldy,
+                  int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count,
+                  int32_t hot_entries, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -489,53 +489,68 @@ __device__ __forceinline__ void lookup_any(uint32_t (&e)[GRP], const uint4 q, ui
   else lookup_group<true>(e, q, vm, tab_s, H, gtab);
 }
 
-__global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
-  uint32_t* tab = reinterpret_cast<uint32_t*>(seg_smem);
-  __shared__ WinRun win[WIN_RUNS];
-  __shared__ int s_run, s_nwin, s_wend;
+// Run sources of pipe_range: the device run list of a grouped launch, or the
+// per-CTA shared-memory plan of the fused MoE step.
+struct ListRuns {
+  const SegParams* P;
+  int n;
+  __device__ __forceinline__ Run get(int r) const { return get_run(*P, r); }
+  __device__ __forceinline__ void wait(int) const {}
+};
 
-  int n_runs, total;
-  if (P.runs) {
-    n_runs = min(P.n_runs[0], P.max_runs);
-    total = P.n_runs[1];
-  } else {
-    n_runs = (int)((P.ntok_single + NT_STREAM - 1) / NT_STREAM);
-    total = n_runs * run_tasks(P.single.rows, 0);
+__device__ __forceinline__ float load_x_cg(const void* x, int bf16, int64_t i) {
+  // x written earlier in the same launch by other CTAs: bypass L1 / the
+  // non-coherent path
+  if (bf16) {
+    unsigned short b;
+    asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(b) : "l"(reinterpret_cast<const unsigned short*>(x) + i));
+    return __uint_as_float(uint32_t(b) << 16);
   }
-  if (n_runs <= 0) return;
-  const int t_begin = (int)((int64_t)total * blockIdx.x / gridDim.x);
-  const int t_end = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
-  if (t_begin >= t_end) return;
-  {  // hot table prefix: vectorised copy by all threads
-    const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
-    uint4* dst = reinterpret_cast<uint4*>(tab);
-    for (int i = threadIdx.x; i < P.H / 4; i += THREADS) dst[i] = __ldg(src + i);
-  }
-  if (threadIdx.x == 0) {  // run holding t_begin: last run with task0 <= t_begin
-    int lo = 0, hi = n_runs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (get_run(P, mid).task0 <= t_begin) lo = mid;
-      else hi = mid - 1;
-    }
-    s_run = lo;
-  }
-  const uint32_t tab_s = smem_base(), xs_s = tab_s + (uint32_t)P.H * 4;
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(reinterpret_cast<const float*>(x) + i));
+  return v;
+}
+
+struct PipeShared {
+  WinRun win[WIN_RUNS];
+  int run, nwin, wend;
+};
+
+// Walk global tasks [t_begin, t_end) of the runs `src` provides (task0
+// ascending): windows of runs whose x slots fit P.xbytes are staged at once,
+// then every warp walks its tasks with the cross-task pipeline.
+template <class Src, bool COHERENT_X>
+__device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, int t_begin, int t_end, PipeShared& S,
+                                           uint32_t tab_s) {
+  if (t_begin >= t_end || src.n <= 0) return;
+  const uint32_t xs_s = tab_s + (uint32_t)P.H * 4;
   char* xs = reinterpret_cast<char*>(seg_smem + (size_t)P.H * 4);
   const int warp = threadIdx.x >> 5;
   const uint32_t H = (uint32_t)P.H;
   const uint32_t* gtab = P.gtab;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // run holding t_begin: last run with task0 <= t_begin
+    int lo = 0, hi = src.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (src.get(mid).task0 <= t_begin) lo = mid;
+      else hi = mid - 1;
+    }
+    S.run = lo;
+  }
+  WinRun* win = S.win;
   int t = t_begin;
   while (t < t_end) {
-    __syncthreads();  // previous window done with xs / win (and s_run published)
+    __syncthreads();  // previous window done with xs / win (and S.run published)
     if (threadIdx.x == 0) {  // next window: consecutive runs whose x slots fit the budget
-      int ri = s_run, nw = 0, xo = 0, wend = t;
-      while (ri < n_runs && nw < WIN_RUNS && wend < t_end) {
-        const Run R = get_run(P, ri);
+      int ri = S.run, nw = 0, xo = 0, wend = t;
+      while (ri < src.n && nw < WIN_RUNS && wend < t_end) {
+        const Run R = src.get(ri);
         const int r_end = R.task0 + run_tasks(R.row1 - R.row0, R.lg);
         const int need = ((R.ntok > 1 ? 8 : 4) * (R.cols + 32) + 15) & ~15;
         if (nw > 0 && xo + need > P.xbytes) break;
         if (r_end > t) {
+          src.wait(ri);  // fused step: the run's x rows are ready
           WinRun& W = win[nw++];
           W.cw = R.cw; W.ro = R.ro; W.mm = R.mm; W.ck = R.ck;
           W.cols = R.cols; W.row0 = R.row0; W.row1 = R.row1; W.lg = R.lg; W.cklg = R.cklg; W.ntok = R.ntok;
@@ -547,12 +562,12 @@ __global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
         if (r_end > t_end) break;
         ++ri;
       }
-      s_nwin = nw;
-      s_wend = wend;
-      s_run = ri;  // first run of the next window
+      S.nwin = nw;
+      S.wend = wend;
+      S.run = ri;  // first run of the next window
     }
     __syncthreads();
-    const int nw = s_nwin, wend = s_wend;
+    const int nw = S.nwin, wend = S.wend;
     for (int w = 0; w < nw; ++w) {  // stage x (fp32; two tokens interleaved)
       const WinRun& W = win[w];
       if (W.ntok > 1) {
@@ -560,15 +575,18 @@ __global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
         for (int i = threadIdx.x; i < W.cols + 32; i += THREADS) {
           float v0 = 0.f, v1 = 0.f;
           if (i < W.cols) {
-            v0 = load_x(P.x, P.x_bf16, (int64_t)W.tok[0] * P.ldx + i);
-            v1 = load_x(P.x, P.x_bf16, (int64_t)W.tok[1] * P.ldx + i);
+            const int64_t i0 = (int64_t)W.tok[0] * P.ldx + i, i1 = (int64_t)W.tok[1] * P.ldx + i;
+            v0 = COHERENT_X ? load_x_cg(P.x, P.x_bf16, i0) : load_x(P.x, P.x_bf16, i0);
+            v1 = COHERENT_X ? load_x_cg(P.x, P.x_bf16, i1) : load_x(P.x, P.x_bf16, i1);
           }
           x2[i] = make_float2(v0, v1);
         }
       } else {
         float* x1 = reinterpret_cast<float*>(xs + W.xoff);
-        for (int i = threadIdx.x; i < W.cols + 32; i += THREADS)
-          x1[i] = i < W.cols ? load_x(P.x, P.x_bf16, (int64_t)W.tok[0] * P.ldx + i) : 0.f;
+        for (int i = threadIdx.x; i < W.cols + 32; i += THREADS) {
+          const int64_t i0 = (int64_t)W.tok[0] * P.ldx + i;
+          x1[i] = i < W.cols ? (COHERENT_X ? load_x_cg(P.x, P.x_bf16, i0) : load_x(P.x, P.x_bf16, i0)) : 0.f;
+        }
       }
     }
     __syncthreads();
@@ -671,6 +689,248 @@ __global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
       }
     }
     t = wend;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
+  __shared__ PipeShared S;
+  int n_runs, total;
+  if (P.runs) {
+    n_runs = min(P.n_runs[0], P.max_runs);
+    total = P.n_runs[1];
+  } else {
+    n_runs = (int)((P.ntok_single + NT_STREAM - 1) / NT_STREAM);
+    total = n_runs * run_tasks(P.single.rows, 0);
+  }
+  if (n_runs <= 0) return;
+  const int t_begin = (int)((int64_t)total * blockIdx.x / gridDim.x);
+  const int t_end = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
+  if (t_begin >= t_end) return;
+  {  // hot table prefix: vectorised copy by all threads
+    const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
+    uint4* dst = reinterpret_cast<uint4*>(seg_smem);
+    for (int i = threadIdx.x; i < P.H / 4; i += THREADS) dst[i] = __ldg(src + i);
+  }
+  ListRuns src{&P, n_runs};
+  pipe_range<ListRuns, false>(P, src, t_begin, t_end, S, smem_base());
+}
+
+// ----------------------------------------------------------------- fused MoE step
+// moe_step_kernel — one cooperative persistent launch per MoE layer step:
+//   1. every CTA recomputes the dispatcher plan in shared memory (stable
+//      counting sort of the top-1 ids, pipeline.py:86-90; one run per expert
+//      token chunk) — no plan kernel, no host sync;
+//   2. wi phase: the global wi task range split evenly over the CTAs, h =
+//      relu(bf16(wi_e x_t)) stored bf16; each CTA then publishes how many
+//      tasks of each run it finished (release: fence + atomic add);
+//   3. wo phase: before staging a run's h rows a CTA waits until all of that
+//      run's wi tasks are published (acquire), then y = bf16(wo_e h_t);
+//   4. the last CTA to finish re-zeroes the counters for the next step.
+// One table fill, no launch gaps, and the wi tail overlaps the wo start.
+struct PlanRuns {
+  const int* runs4;  // shared: per run {expert, ntok, tok0, tok1}
+  int n;
+  const qmoe_matrix* mats;
+  int pass, lg, tasks_per_run;
+  const int* counters;  // wo: counters[1 + r] reaches `need` when run r's wi tasks are done
+  int need;
+  __device__ __forceinline__ Run get(int r) const {
+    const int e = runs4[4 * r];
+    const qmoe_matrix& M = mats[2 * e + pass];
+    Run R;
+    R.cw = M.cw;
+    R.ro = M.row_off;
+    R.mm = M.row_minmax;
+    R.ck = M.ck;
+    R.rid = nullptr;
+    R.cols = M.cols;
+    R.row0 = 0;
+    R.row1 = M.rows;
+    R.lg = lg;
+    R.cklg = M.lg;
+    R.ntok = runs4[4 * r + 1];
+    R.task0 = r * tasks_per_run;
+    R.tok[0] = runs4[4 * r + 2];
+    R.tok[1] = runs4[4 * r + 3];
+    return R;
+  }
+  __device__ __forceinline__ void wait(int r) const {
+    if (!counters) return;
+    for (;;) {
+      int v;
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(counters + 1 + r));
+      if (v >= need) break;
+      __nanosleep(128);
+    }
+  }
+};
+
+struct StepParams {
+  SegParams wi, wo;  // per-phase x / y / modes; table fields from wi
+  const int32_t* assign;
+  int T, E, ntu;
+  const qmoe_matrix* mats;
+  int lg_wi, lg_wo, tasks_wi, tasks_wo;
+  int32_t* counters;  // int32[T + 1], zero at launch: [0] = CTAs done, [1 + r] = wi tasks done of run r
+  int32_t* order_out;
+  int32_t* count_out;
+  int plan_off;       // byte offset of the plan area in dynamic shared memory
+};
+
+__device__ __forceinline__ int block_excl_scan2(int v, int w, int& wtot, int2* wsum, int* tot) {
+  // exclusive scan of (v, w) pairs in thread order; returns v-prefix, w-prefix via wtot
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int iv = v, iw = w;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int a = __shfl_up_sync(FULL_MASK, iv, d), b = __shfl_up_sync(FULL_MASK, iw, d);
+    if (lane >= d) {
+      iv += a;
+      iw += b;
+    }
+  }
+  if (lane == 31) wsum[warp] = make_int2(iv, iw);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0, b = 0;
+    for (int k = 0; k < NWARPS; ++k) {
+      const int2 t = wsum[k];
+      wsum[k] = make_int2(a, b);
+      a += t.x;
+      b += t.y;
+    }
+    tot[0] = a;
+    tot[1] = b;
+  }
+  __syncthreads();
+  wtot = wsum[warp].y + iw - w;
+  return wsum[warp].x + iv - v;
+}
+
+__global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
+  __shared__ PipeShared PS;
+  __shared__ int2 wsum[NWARPS];
+  __shared__ int tot[2];
+  const int E = S.E, T = S.T, ntu = S.ntu;
+  int* cnt = reinterpret_cast<int*>(seg_smem + S.plan_off);  // E
+  int* start = cnt + E;                                        // E + 1
+  int* choff = start + E + 1;                                  // E + 1
+  int* order = choff + E + 1;                                  // T
+  int* runs4 = order + T;                                      // 4 T
+  const SegParams& PW = S.wi;
+  {  // hot table prefix
+    const uint4* src = reinterpret_cast<const uint4*>(PW.gtab);
+    uint4* dst = reinterpret_cast<uint4*>(seg_smem);
+    for (int i = threadIdx.x; i < PW.H / 4; i += THREADS) dst[i] = __ldg(src + i);
+  }
+  // ---- 1. plan
+  for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += THREADS) {
+    const int e = __ldg(S.assign + t);
+    if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);
+  }
+  __syncthreads();
+  {
+    const int per = (E + THREADS - 1) / THREADS;
+    const int e0 = min(E, (int)threadIdx.x * per), e1 = min(E, e0 + per);
+    int lv = 0, lw = 0;
+    for (int e = e0; e < e1; ++e) {
+      lv += cnt[e];
+      lw += (cnt[e] + ntu - 1) / ntu;
+    }
+    int bw;
+    int bv = block_excl_scan2(lv, lw, bw, wsum, tot);
+    for (int e = e0; e < e1; ++e) {
+      start[e] = bv;
+      choff[e] = bw;
+      bv += cnt[e];
+      bw += (cnt[e] + ntu - 1) / ntu;
+    }
+    if (threadIdx.x == 0) {
+      start[E] = tot[0];
+      choff[E] = tot[1];
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && S.count_out)
+    for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = cnt[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;  // fill cursor
+  __syncthreads();
+  if (threadIdx.x < 32) {  // stable placement in buffer order
+    const int lane = threadIdx.x;
+    for (int t0 = 0; t0 < T; t0 += 32) {
+      const int t = t0 + lane;
+      const int e = t < T ? __ldg(S.assign + t) : -1;
+      const bool ok = t < T && e >= 0 && e < E;
+      const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      const int leader = __ffs(peers) - 1;
+      int basev = 0;
+      if (ok && lane == leader) {
+        basev = cnt[e];
+        cnt[e] = basev + __popc(peers);
+      }
+      basev = __shfl_sync(FULL_MASK, basev, leader);
+      if (ok) order[start[e] + basev + rank] = t;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  const int nch = choff[E];
+  for (int i = threadIdx.x; i < nch; i += THREADS) {
+    int lo = 0, hi = E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (choff[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const int e = lo, ch = i - choff[e];
+    const int c = start[e + 1] - start[e];
+    const int nt = min(ntu, c - ch * ntu);
+    runs4[4 * i] = e;
+    runs4[4 * i + 1] = nt;
+    runs4[4 * i + 2] = order[start[e] + ch * ntu];
+    runs4[4 * i + 3] = order[start[e] + ch * ntu + (nt > 1 ? 1 : 0)];
+  }
+  if (blockIdx.x == 0 && S.order_out)
+    for (int t = threadIdx.x; t < start[E]; t += THREADS) S.order_out[t] = order[t];
+  __syncthreads();
+  const uint32_t tab_s = smem_base();
+  // ---- 2. wi phase
+  {
+    const int total = nch * S.tasks_wi;
+    const int tb = (int)((int64_t)total * blockIdx.x / gridDim.x);
+    const int te = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
+    PlanRuns src{runs4, nch, S.mats, 0, S.lg_wi, S.tasks_wi, nullptr, 0};
+    pipe_range<PlanRuns, false>(S.wi, src, tb, te, PS, tab_s);
+    __threadfence();  // this thread's h stores before the CTA's release below
+    __syncthreads();
+    if (threadIdx.x == 0 && tb < te) {
+      for (int r = tb / S.tasks_wi; r * S.tasks_wi < te; ++r) {
+        const int a = max(tb, r * S.tasks_wi), b = min(te, (r + 1) * S.tasks_wi);
+        atomicAdd(S.counters + 1 + r, b - a);
+      }
+    }
+  }
+  // ---- 3. wo phase
+  {
+    const int total = nch * S.tasks_wo;
+    const int tb = (int)((int64_t)total * blockIdx.x / gridDim.x);
+    const int te = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
+    PlanRuns src{runs4, nch, S.mats, 1, S.lg_wo, S.tasks_wo, S.counters, S.tasks_wi};
+    pipe_range<PlanRuns, true>(S.wo, src, tb, te, PS, tab_s);
+  }
+  // ---- 4. last CTA re-arms the counters
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(S.counters, 1) == (int)gridDim.x - 1) {
+      for (int r = 0; r < nch; ++r) S.counters[1 + r] = 0;
+      S.counters[0] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -897,6 +1157,80 @@ int qmoe_fused_matmat(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_
                       float* d_y, int64_t ldy, int32_t* d_bad, void* stream) {
   if (ldx < cols || ldy < rows) return qmoe::fail(QMOE_EINVAL, "leading dimension too small");
   return fused_common(d, d_cw, d_row_off, d_mm, rows, cols, d_x, x_dtype, ntok, ldx, d_y, ldy, d_bad, stream);
+}
+
+int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assign, int32_t T, int32_t E,
+                  const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo, int32_t d_model,
+                  int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h, int64_t ldh, float* d_y,
+                  int64_t ldy, int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count, int32_t hot_entries,
+                  void* stream) {
+  if (!d || !d->d_stab || !d_assign || T < 0 || E < 1 || !d_mats || tokens_per_run < 1 ||
+      tokens_per_run > NT_STREAM || lg_wi < 0 || lg_wi > 5 || lg_wo < 0 || lg_wo > 5 || d_model <= 0 ||
+      d_ff <= 0 || !d_h || !d_y || !d_counters || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16))
+    return qmoe::fail(QMOE_EINVAL, "bad argument");
+  if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "the fused step needs a <=3-non-zero dictionary");
+  const int esz = x_dtype == QMOE_X_BF16 ? 2 : 4;
+  if (!aligned16(d_x) || (ldx * esz) % 16 || !aligned16(d_h) || (ldh * 2) % 16)
+    return qmoe::fail(QMOE_EINVAL, "x / h rows must be 16-byte aligned");
+  if (T == 0) return QMOE_OK;
+  StepParams SP{};
+  SegParams P{};
+  P.gtab = seg_table(d, d_table);
+  P.z_bytes = entry0_bytes(d);
+  SP.wi = P;
+  SP.wi.x = d_x;
+  SP.wi.x_bf16 = x_dtype == QMOE_X_BF16;
+  SP.wi.ldx = ldx;
+  SP.wi.y = d_h;
+  SP.wi.y_mode = QMOE_Y_RELU_BF16;
+  SP.wi.ldy = ldh;
+  SP.wo = P;
+  SP.wo.x = d_h;
+  SP.wo.x_bf16 = 1;
+  SP.wo.ldx = ldh;
+  SP.wo.y = d_y;
+  SP.wo.y_mode = QMOE_Y_STORE_F32;
+  SP.wo.ldy = ldy;
+  SP.assign = d_assign;
+  SP.T = T;
+  SP.E = E;
+  SP.ntu = tokens_per_run;
+  SP.mats = d_mats;
+  SP.lg_wi = lg_wi;
+  SP.lg_wo = lg_wo;
+  SP.tasks_wi = ((d_ff << lg_wi) + 31) >> 5;
+  SP.tasks_wo = ((d_model << lg_wo) + 31) >> 5;
+  SP.counters = d_counters;
+  SP.order_out = d_order;
+  SP.count_out = d_expert_count;
+  const int maxc = std::max(d_model, d_ff);
+  const size_t slot = (size_t)2 * 4 * (((maxc + 32) + 3) & ~3);
+  const size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
+  const size_t plan = ((size_t)(3 * E + 2 + 5 * (size_t)T) * 4 + 15) & ~(size_t)15;
+  const size_t static_smem = 2048;
+  if (xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
+    return qmoe::fail(QMOE_EUNSUPPORTED, "step too large for the fused kernel's shared memory (use the grouped path)");
+  int H = (int)((d->max_smem_optin - xbytes - plan - static_smem - 256) / 4);
+  int want = hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE;
+  if (hot_override() >= 0) want = hot_override();
+  H = std::max(std::min(H, std::min(want, QMOE_DICT_SIZE)) & ~255, 256);
+  SP.wi.H = SP.wo.H = H;
+  SP.wi.xbytes = SP.wo.xbytes = (int)xbytes;
+  SP.plan_off = (int)((size_t)H * 4 + xbytes);
+  const size_t smem = (size_t)H * 4 + xbytes + plan;
+  CK(cudaFuncSetAttribute(moe_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(d->num_sms);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = S(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the wo phase waits on other CTAs
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, moe_step_kernel, SP), "moe_step_kernel launch");
+  return QMOE_OK;
 }
 
 int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work* d_work, const int32_t* d_n_work,

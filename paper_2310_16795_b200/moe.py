@@ -87,6 +87,9 @@ class CompressedMoELayer:
                                      np.int64)
         self._lanes = {}
         self._T = max_tokens
+        # one cooperative launch per step (sparse dictionaries, RAW layout)
+        self.fused = (not self.packed and bool(dic.device_info(self.device.index)["sparse_path"])
+                      and os.environ.get("QMOE_FUSED", "1") == "1")
         self._alloc(max_tokens)
 
     def _alloc(self, T: int) -> None:
@@ -103,6 +106,7 @@ class CompressedMoELayer:
         # FFN hidden: relu(bf16(wi @ x)) per token, bf16 rows (wo-pass x)
         self.h = _lib.padded_empty(max(1, T) * self.d_ff, torch.bfloat16, dev).view(max(1, T), self.d_ff)
         self.bad = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
+        self.counters = torch.zeros(max(1, T) + 1, dtype=torch.int32, device=dev)  # fused step (self-resetting)
 
     @staticmethod
     def _aligned_rows(x) -> bool:
@@ -194,10 +198,32 @@ class CompressedMoELayer:
             buf = _lib.padded_empty(T * self.d_model, x.dtype, x.device).view(T, self.d_model)
             buf.copy_(x)
             x = buf
-        self.plan(assign, stream)
-        self.pass_wi(x, stream)
-        self.pass_wo(out, stream)
+        if self.fused:
+            try:
+                self.step(x, assign, out, stream)
+                return out
+            except _lib.QmoeError as err:  # plan does not fit the fused kernel's shared memory
+                if err.status != _lib.QMOE_EUNSUPPORTED:
+                    raise
+        if True:
+            self.plan(assign, stream)
+            self.pass_wi(x, stream)
+            self.pass_wo(out, stream)
         return out
+
+    def step(self, x, assign, out, stream=None) -> None:
+        """The whole step as one cooperative launch (qmoe_moe_step)."""
+        import torch
+
+        T = assign.shape[0]
+        self._T = T
+        lg_wi, lg_wo = self.lanes_per_row(T)
+        xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
+        _lib.check(_lib.lib.qmoe_moe_step(
+            self.handle, self._table(), _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit,
+            lg_wi, lg_wo, self.d_model, self.d_ff, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h), self.h.stride(0),
+            _lib.ptr(out), out.stride(0), _lib.ptr(self.counters), _lib.ptr(self.order), _lib.ptr(self.expert_count),
+            max(self.hot_entries(T, True), self.hot_entries(T, False)), _lib.stream_ptr(stream)))
 
     def forward(self, x: np.ndarray, assign: np.ndarray) -> np.ndarray:
         """Host API: numpy tokens + expert ids in, numpy outputs back."""
