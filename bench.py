@@ -175,7 +175,8 @@ def reference_arm(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 codewords -> f32 accumulate",
         "data": "synthetic N(0,0.02^2) RTN ternary, oracle encode",
         "config": {"workload": args.workload, "experts": E, "d_model": d_model, "d_ff": d_ff,
-                   "tokens_per_step": sample_tokens, "routing": "RouterSim argmax seed 0"},
+                   "tokens_per_step": args.tokens, "sampled_tokens_per_step": sample_tokens,
+                   "routing": "top-1 RouterSim argmax seed 0", "parallelism": "cpu"},
         "tokens_per_s": ntok / sec,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
                          "sample": f"{args.steps} steps x {sample_tokens} tokens through the composed oracle "

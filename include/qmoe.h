@@ -295,6 +295,11 @@ int qmoe_moe_step(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_as
                   int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count,
                   int32_t hot_entries, void* stream);
 
+/* Debug hook: d_buf = u64[num_sms * 8] receives per-CTA %globaltimer stamps of
+ * qmoe_moe_step phases (0 start, 1 plan + table staged, 2 wi done, 3 wo
+ * done); NULL disables. Not for production use. */
+int qmoe_debug_step_trace(void* d_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -136,6 +136,41 @@ __device__ __forceinline__ uint32_t smem_base() {
   asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(b) : "l"(seg_smem));
   return b;
 }
+// Hot-table fill by the bulk-copy engine: one thread issues cp.async.bulk
+// copies (global -> this CTA's shared memory) completing on an mbarrier, the
+// CTA does other work (the dispatcher plan), and every thread waits on the
+// barrier before its first lookup.
+__device__ __forceinline__ void table_fill_async(const uint32_t* gtab, int H, uint64_t* mbar) {
+  if (threadIdx.x == 0) {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)H * 4;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    const uint32_t dst = smem_base();
+    constexpr uint32_t CHUNK = 32768;
+    for (uint32_t o = 0; o < bytes; o += CHUNK) {
+      const uint32_t n = min(CHUNK, bytes - o);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + o),
+          "l"(reinterpret_cast<const char*>(gtab) + o), "r"(n), "r"(mb)
+          : "memory");
+    }
+  }
+}
+
+__device__ __forceinline__ void table_fill_wait(uint64_t* mbar) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(mb)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -514,7 +549,14 @@ __device__ __forceinline__ float load_x_cg(const void* x, int bf16, int64_t i) {
 struct PipeShared {
   WinRun win[WIN_RUNS];
   int run, nwin, wend;
+  int next;  // next unclaimed task of the window (warps claim dynamically)
 };
+
+__device__ __forceinline__ int claim_task(int* next) {
+  int k = 0;
+  if ((threadIdx.x & 31) == 0) k = atomicAdd(next, 1);
+  return __shfl_sync(FULL_MASK, k, 0);
+}
 
 // Walk global tasks [t_begin, t_end) of the runs `src` provides (task0
 // ascending): windows of runs whose x slots fit P.xbytes are staged at once,
@@ -565,6 +607,7 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
       S.nwin = nw;
       S.wend = wend;
       S.run = ri;  // first run of the next window
+      S.next = t;
     }
     __syncthreads();
     const int nw = S.nwin, wend = S.wend;
@@ -590,14 +633,14 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
       }
     }
     __syncthreads();
-    // ---- per-warp pipelined walk over tasks k = t + warp, + NWARPS, ... < wend
-    int k = t + warp;
+    // ---- per-warp pipelined walk over dynamically claimed tasks (one claimed ahead)
+    int k = claim_task(&S.next);
     if (k < wend) {
       int wc = 0;
       while (win[wc].task1 <= k) ++wc;
       Lane c = lane_task(win[wc], k);
       int wn = wc;
-      int kn = k + NWARPS;
+      int kn = claim_task(&S.next);
       bool has_n = kn < wend;
       Lane n{0, 0, 0, -1, 0u};
       if (has_n) {
@@ -676,7 +719,7 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
         wc = wn;
         maxgc = maxgn;
         k = kn;
-        kn = k + NWARPS;
+        kn = claim_task(&S.next);
         has_n = kn < wend;
         nready = false;
         if (has_n) {
@@ -706,11 +749,10 @@ __global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
   const int t_begin = (int)((int64_t)total * blockIdx.x / gridDim.x);
   const int t_end = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
   if (t_begin >= t_end) return;
-  {  // hot table prefix: vectorised copy by all threads
-    const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
-    uint4* dst = reinterpret_cast<uint4*>(seg_smem);
-    for (int i = threadIdx.x; i < P.H / 4; i += THREADS) dst[i] = __ldg(src + i);
-  }
+  __shared__ __align__(8) uint64_t tab_bar;
+  table_fill_async(P.gtab, P.H, &tab_bar);
+  __syncthreads();  // barrier initialised before anyone waits on it
+  table_fill_wait(&tab_bar);
   ListRuns src{&P, n_runs};
   pipe_range<ListRuns, false>(P, src, t_begin, t_end, S, smem_base());
 }
@@ -765,6 +807,16 @@ struct PlanRuns {
   }
 };
 
+__device__ unsigned long long* g_step_trace = nullptr;  // qmoe_debug_step_trace: per-CTA phase stamps
+
+__device__ __forceinline__ void trace_stamp(int k) {
+  if (g_step_trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_step_trace[blockIdx.x * 8 + k] = t;
+  }
+}
+
 struct StepParams {
   SegParams wi, wo;  // per-phase x / y / modes; table fields from wi
   const int32_t* assign;
@@ -818,11 +870,9 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   int* order = choff + E + 1;                                  // T
   int* runs4 = order + T;                                      // 4 T
   const SegParams& PW = S.wi;
-  {  // hot table prefix
-    const uint4* src = reinterpret_cast<const uint4*>(PW.gtab);
-    uint4* dst = reinterpret_cast<uint4*>(seg_smem);
-    for (int i = threadIdx.x; i < PW.H / 4; i += THREADS) dst[i] = __ldg(src + i);
-  }
+  __shared__ __align__(8) uint64_t tab_bar;
+  trace_stamp(0);
+  table_fill_async(PW.gtab, PW.H, &tab_bar);  // overlaps the plan below
   // ---- 1. plan
   for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;
   __syncthreads();
@@ -897,6 +947,8 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   if (blockIdx.x == 0 && S.order_out)
     for (int t = threadIdx.x; t < start[E]; t += THREADS) S.order_out[t] = order[t];
   __syncthreads();
+  table_fill_wait(&tab_bar);
+  trace_stamp(1);
   const uint32_t tab_s = smem_base();
   // ---- 2. wi phase
   {
@@ -913,6 +965,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
         atomicAdd(S.counters + 1 + r, b - a);
       }
     }
+    trace_stamp(2);
   }
   // ---- 3. wo phase
   {
@@ -922,6 +975,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     PlanRuns src{runs4, nch, S.mats, 1, S.lg_wo, S.tasks_wo, S.counters, S.tasks_wi};
     pipe_range<PlanRuns, true>(S.wo, src, tb, te, PS, tab_s);
   }
+  trace_stamp(3);
   // ---- 4. last CTA re-arms the counters
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1159,6 +1213,13 @@ int qmoe_fused_matmat(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_
   return fused_common(d, d_cw, d_row_off, d_mm, rows, cols, d_x, x_dtype, ntok, ldx, d_y, ldy, d_bad, stream);
 }
 
+int qmoe_debug_step_trace(void* d_buf) {
+  // debug hook: per-CTA %globaltimer stamps of the fused step (8 u64 per CTA:
+  // start, plan done, wi done, wo done); NULL disables
+  CK(cudaMemcpyToSymbol(g_step_trace, &d_buf, sizeof(void*)), "trace symbol");
+  return QMOE_OK;
+}
+
 int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assign, int32_t T, int32_t E,
                   const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo, int32_t d_model,
                   int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h, int64_t ldh, float* d_y,
@@ -1228,7 +1289,7 @@ int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assig
   attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the wo phase waits on other CTAs
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = getenv("QMOE_NO_COOP") ? 0 : 1;
   CK(cudaLaunchKernelEx(&cfg, moe_step_kernel, SP), "moe_step_kernel launch");
   return QMOE_OK;
 }

@@ -21,6 +21,7 @@ wo matvec through moepack.codec.fused_matvec) up to the matvec tolerance.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -82,7 +83,7 @@ class CompressedMoELayer:
             descs[2 * e + 1] = _lib.QmoeMatrix(*wo[e].descriptor())
         raw = np.frombuffer(bytes(descs), dtype=np.uint8)
         self.mats = torch.from_numpy(raw.copy()).to(self.device)
-        self.tokens_per_unit = min(int(tokens_per_unit), _lib.NT_STREAM)
+        self.tokens_per_unit = min(int(os.environ.get("QMOE_NTU", tokens_per_unit)), _lib.NT_STREAM)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
                                      np.int64)
         self._lanes = {}
@@ -136,6 +137,9 @@ class CompressedMoELayer:
                 while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES and mg / (1 << (lg + 1)) >= 2.0:
                     lg += 1
                 out.append(lg)
+            for kind, key in enumerate(("QMOE_LG_WI", "QMOE_LG_WO")):  # experiment overrides
+                if key in os.environ:
+                    out[kind] = int(os.environ[key])
             hit = self._lanes[T] = tuple(out)
         return hit
 
