@@ -295,6 +295,21 @@ int qmoe_moe_step(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_as
                   int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count,
                   int32_t hot_entries, void* stream);
 
+/* Batched-token decode-then-MMA pass (many tokens per expert, e.g.
+ * Switch-large-128 with T in the thousands): for every expert e with tokens
+ * d_order[start_e .. start_e + d_expert_count[e]) (qmoe_moe_plan's outputs,
+ * start_e = exclusive prefix of the counts), y[t][r] (y_mode as
+ * qmoe_grouped_matvec) = bf16(sum_k W_e[r][k] x[t][k]) for all rows r of
+ * W_e = d_mats[2e + pass] (RAW layout, rows x cols). Each 512-row block of an
+ * expert is decoded once into shared memory per block of tokens_per_block
+ * (32 or 64) tokens and multiplied on the tensor cores (mma.sync bf16, fp32
+ * accumulate). */
+int qmoe_dense_moe_pass(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_matrix* d_mats,
+                        int32_t E, int32_t pass, const int32_t* d_expert_count,
+                        const int32_t* d_order, int32_t rows, int32_t cols, const void* d_x,
+                        int x_dtype, int64_t ldx, void* d_y, int y_mode, int64_t ldy,
+                        int32_t tokens_per_block, int32_t hot_entries, void* stream);
+
 /* Debug hook: d_buf = u64[num_sms * 8] receives per-CTA %globaltimer stamps of
  * qmoe_moe_step phases (0 start, 1 plan + table staged, 2 wi done, 3 wo
  * done); NULL disables. Not for production use. */

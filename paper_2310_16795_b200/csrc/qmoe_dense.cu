@@ -1,0 +1,338 @@
+// Batched-token decode-then-MMA MoE pass (BASELINE
+// configs[2]: Switch-large-128 with many tokens per expert).
+//
+// With t tokens per expert the streaming matvec re-decodes each expert matrix
+// ceil(t / 2) times; here every expert row block is decoded ONCE per step into
+// a dense bf16 tile in shared memory and multiplied on the tensor cores with
+// all of the expert's tokens (up to 64 per block).
+//
+//   work item   (expert e, 512-row block, token block of <= BN tokens); the
+//               persistent grid strides over the items; every CTA derives the
+//               item list from the dispatcher's expert counts (qmoe_moe_plan).
+//   decode      thread = row: the lane walks its row's codeword stream chunk
+//               by chunk (64 columns), zero-fills its 128-byte row of the W
+//               tile and stores the <= 3 non-zero bf16 levels of each codeword
+//               (entry table of the streaming kernel, hot prefix in shared
+//               memory). A codeword straddling the chunk end is revisited by
+//               the next chunk. Rows are XOR-swizzled by 16-byte chunk so the
+//               MMA operand loads are bank-conflict free.
+//   mma         warp w owns rows [32w, 32w+32) — exactly the rows its lanes
+//               decoded — x BN tokens: ldmatrix + mma.sync.m16n8k16 bf16 ->
+//               fp32 accumulators in registers; the token tile (bf16, from
+//               x rows of the expert's tokens) is double-buffered per chunk.
+//   epilogue    per (row, token): bf16 RNE once (codec.py:243), y mode as the
+//               streaming kernel (relu -> bf16 hidden, or f32 store / add).
+//
+// Numerics: bf16 x bf16 products are exact in fp32; the accumulation order
+// differs from the reference's sgemv (tolerance-level parity, as the
+// streaming kernel).
+#include <algorithm>
+#include <climits>
+
+#include "qmoe_device.cuh"
+
+using namespace qmoe_dev;
+
+namespace {
+
+constexpr int DTHREADS = 512;
+constexpr int DWARPS = DTHREADS / 32;
+constexpr int BM = DTHREADS;  // rows per item (thread = row)
+constexpr int BK = 64;        // columns per chunk (128-byte bf16 rows)
+
+extern __shared__ __align__(128) uint8_t dsm[];
+
+struct DenseParams {
+  const uint32_t* gtab;  // byte-field entry table (matvec variant 1)
+  int H;
+  const qmoe_matrix* mats;
+  int E, pass, rows, cols;
+  const int32_t* count;  // tokens per expert
+  const int32_t* order;  // expert-major token order (qmoe_moe_plan)
+  const void* x;
+  int x_bf16;
+  int64_t ldx;
+  void* y;
+  int y_mode;
+  int64_t ldy;
+  int w_off, x_off, plan_off;  // byte offsets in dynamic shared memory
+};
+
+__device__ __forceinline__ uint32_t sbase() {
+  uint32_t b;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(b) : "l"(dsm));
+  return b;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+}
+__device__ __forceinline__ void sts_zero16(uint32_t addr) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(addr), "r"(0u));
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ uint16_t x_bf16_bits(const void* x, int bf16, int64_t i) {
+  if (bf16) return __ldg(reinterpret_cast<const unsigned short*>(x) + i);
+  return (uint16_t)(__float_as_uint(__ldg(reinterpret_cast<const float*>(x) + i)) >> 16);  // x is bf16-valued
+}
+
+template <int BN>
+__global__ void __launch_bounds__(DTHREADS, 1) dense_moe_kernel(DenseParams P) {
+  __shared__ __align__(8) uint64_t tab_bar;
+  __shared__ int s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t base = sbase();
+  const uint32_t tab_s = base, w_s = base + P.w_off, x_s = base + P.x_off;
+  int* start = reinterpret_cast<int*>(dsm + P.plan_off);  // E + 1
+  int* ipre = start + P.E + 1;                              // E + 1: items before expert e
+  const int E = P.E;
+  const int nrb = (P.rows + BM - 1) / BM;
+  // ---- hot table (bulk copy, overlaps the item plan)
+  if (tid == 0) {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)P.H * 4;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    for (uint32_t o = 0; o < bytes; o += 32768u)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tab_s + o),
+          "l"(reinterpret_cast<const char*>(P.gtab) + o), "r"(min(32768u, bytes - o)), "r"(mb)
+          : "memory");
+    // ---- item plan (serial over experts; E <= a few thousand)
+    int a = 0, it = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = __ldg(P.count + e);
+      start[e] = a;
+      ipre[e] = it;
+      a += c;
+      it += nrb * ((c + BN - 1) / BN);
+    }
+    start[E] = a;
+    ipre[E] = it;
+    s_total = it;
+  }
+  __syncthreads();
+  {
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(mb)
+                   : "memory");
+  }
+  const int total = s_total;
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t rowb = w_s + (uint32_t)tid * 128u;  // my W-tile row
+  const uint32_t rx = (uint32_t)(tid & 7) << 4;      // its 16-byte-chunk swizzle
+  constexpr int NT8 = BN / 8;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    int lo = 0, hi = E - 1;  // expert of the item: last e with ipre[e] <= item
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ipre[mid] <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    const int e = lo, local = item - ipre[e];
+    const int rb = local % nrb, tb = local / nrb;
+    const int cnt = start[e + 1] - start[e];
+    const int nt = min(BN, cnt - tb * BN);
+    const int tok0 = start[e] + tb * BN;
+    const qmoe_matrix& M = P.mats[2 * e + P.pass];
+    const int r = rb * BM + tid;
+    const bool valid = r < P.rows;
+    int p = 0, pend = 0, col = 0;
+    uint32_t wlo = 0, whi = 0;
+    if (valid) {
+      p = __ldg(M.row_off + r);
+      pend = __ldg(M.row_off + r + 1);
+      const uint32_t mm = __ldg(M.row_minmax + r);
+      wlo = mm & 0xFFFFu;
+      whi = mm >> 16;
+    }
+    int gcur = -1;
+    uint4 g = make_uint4(0u, 0u, 0u, 0u);
+    float acc[2][NT8][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NT8; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[i][j][k] = 0.f;
+    int chunk = 0;
+    for (int k0 = 0; k0 < P.cols; k0 += BK, ++chunk) {
+      const int k1 = k0 + BK;
+      // ---- token tile (double-buffered): Xt[n][k] bf16, swizzled like W
+      const uint32_t xb = x_s + (uint32_t)(chunk & 1) * (BN * 128u);
+      for (int i = tid; i < BN * BK; i += DTHREADS) {
+        const int n = i / BK, k = i % BK;
+        uint32_t v = 0;
+        if (n < nt && k0 + k < P.cols) {
+          const int t = __ldg(P.order + tok0 + n);
+          v = x_bf16_bits(P.x, P.x_bf16, (int64_t)t * P.ldx + k0 + k);
+        }
+        sts_u16(xb + (uint32_t)n * 128u + (((uint32_t)k * 2u) ^ ((uint32_t)(n & 7) << 4)), v);
+      }
+      // ---- decode my row's columns [k0, k1) into the W tile
+#pragma unroll
+      for (int c16 = 0; c16 < 8; ++c16) sts_zero16(rowb + 16u * c16);
+      while (valid && p < pend && col < k1) {
+        const int grp = p >> 3;
+        if (grp != gcur) {
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+                       : "l"(M.cw + (size_t)grp * 8));
+          gcur = grp;
+        }
+        const uint32_t wd = (p & 4) ? ((p & 2) ? g.w : g.z) : ((p & 2) ? g.y : g.x);
+        const uint32_t c = (p & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+        const uint32_t en = c < H ? lds_u32(tab_s + 4 * c) : __ldg(P.gtab + c);
+        const int n2 = (int)(en >> 28) * 2;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
+          if (f != 0x7Fu) {
+            const int vk = col + (int)(f >> 2) - k0;  // column inside the chunk
+            if ((unsigned)vk < (unsigned)BK)
+              sts_u16(rowb + (((uint32_t)vk * 2u) ^ rx), ((en >> (24 + j)) & 1u) ? whi : wlo);
+          }
+        }
+        if (col + n2 > k1) break;  // straddles the chunk end: revisit next chunk
+        col += n2;
+        ++p;
+      }
+      __syncthreads();  // token tile staged (W rows: each warp reads only its own)
+      // ---- mma: rows [32 warp, +32) x BN tokens x 64 columns
+#pragma unroll
+      for (int ks = 0; ks < BK / 16; ++ks) {
+        uint32_t a[2][4];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int row = warp * 32 + mi * 16 + (lane & 15);
+          const uint32_t ch = (uint32_t)(ks * 2 + (lane >> 4));
+          ldsm_x4(w_s + (uint32_t)row * 128u + ((ch ^ (uint32_t)(row & 7)) << 4), a[mi][0], a[mi][1], a[mi][2],
+                  a[mi][3]);
+        }
+#pragma unroll
+        for (int nj = 0; nj < NT8; nj += 2) {
+          // four 8x8 matrices: (n-tile nj, k lo), (nj, k hi), (nj+1, k lo), (nj+1, k hi)
+          const int n = nj * 8 + (lane & 7) + ((lane >> 4) << 3);
+          const uint32_t ch = (uint32_t)(ks * 2 + ((lane >> 3) & 1));
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(xb + (uint32_t)n * 128u + ((ch ^ (uint32_t)(n & 7)) << 4), b0, b1, b2, b3);
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            mma16816(acc[mi][nj], a[mi], b0, b1);
+            mma16816(acc[mi][nj + 1], a[mi], b2, b3);
+          }
+        }
+      }
+      __syncwarp();  // this warp's W rows are rewritten by the next chunk's decode
+    }
+    // ---- epilogue: C fragment (row g, cols 2t, 2t+1) and (row g+8, ...)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+#pragma unroll
+      for (int nj = 0; nj < NT8; ++nj) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int row = rb * BM + warp * 32 + mi * 16 + (lane >> 2) + ((h & 2) ? 8 : 0);
+          const int n = nj * 8 + (lane & 3) * 2 + (h & 1);
+          if (row >= P.rows || n >= nt) continue;
+          const int64_t t = __ldg(P.order + tok0 + n);
+          const float v = bf16_round_dev(acc[mi][nj][h]);
+          if (P.y_mode == QMOE_Y_RELU_BF16) {
+            reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
+          } else if (P.y_mode == QMOE_Y_STORE_F32) {
+            reinterpret_cast<float*>(P.y)[t * P.ldy + row] = v + 0.f;
+          } else {
+            float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
+            *yp = *yp + v;
+          }
+        }
+      }
+    }
+    __syncthreads();  // token tile buffers reused by the next item
+  }
+}
+
+bool al16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matrix* d_mats, int32_t E, int32_t pass,
+                        const int32_t* d_expert_count, const int32_t* d_order, int32_t rows, int32_t cols,
+                        const void* d_x, int x_dtype, int64_t ldx, void* d_y, int y_mode, int64_t ldy,
+                        int32_t tokens_per_block, int32_t hot_entries, void* stream) {
+  if (!d || !d->d_stab || !d_mats || E < 1 || (pass != 0 && pass != 1) || !d_expert_count || !d_order || rows < 0 ||
+      cols < 0 || cols % 2 || !d_x || !d_y || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16) ||
+      (y_mode != QMOE_Y_ACCUM_F32 && y_mode != QMOE_Y_RELU_BF16 && y_mode != QMOE_Y_STORE_F32) ||
+      (tokens_per_block != 32 && tokens_per_block != 64))
+    return qmoe::fail(QMOE_EINVAL, "bad argument");
+  if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "the dense pass needs a <=3-non-zero dictionary");
+  if (rows == 0 || cols == 0) return QMOE_OK;
+  DenseParams P{};
+  P.gtab = (d_table ? d_table : d->d_mtab) + qmoe::MT_STRIDE;
+  P.mats = d_mats;
+  P.E = E;
+  P.pass = pass;
+  P.rows = rows;
+  P.cols = cols;
+  P.count = d_expert_count;
+  P.order = d_order;
+  P.x = d_x;
+  P.x_bf16 = x_dtype == QMOE_X_BF16;
+  P.ldx = ldx;
+  P.y = d_y;
+  P.y_mode = y_mode;
+  P.ldy = ldy;
+  const int BN = tokens_per_block;
+  const size_t wbytes = (size_t)BM * 128, xbytes = (size_t)2 * BN * 128;
+  const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
+  const size_t static_smem = 1024;
+  if (wbytes + xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
+    return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts for the dense pass");
+  int H = (int)((d->max_smem_optin - wbytes - xbytes - plan - static_smem) / 4);
+  H = std::min(H, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE) & ~255;
+  H = std::max(H, 256);
+  P.H = H;
+  P.w_off = H * 4;
+  P.x_off = P.w_off + (int)wbytes;
+  P.plan_off = P.x_off + (int)xbytes;
+  const size_t smem = (size_t)P.plan_off + plan;
+  const int grid = d->num_sms;
+  if (BN == 64) {
+    CK(cudaFuncSetAttribute(dense_moe_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    dense_moe_kernel<64><<<grid, DTHREADS, smem, S(stream)>>>(P);
+  } else {
+    CK(cudaFuncSetAttribute(dense_moe_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    dense_moe_kernel<32><<<grid, DTHREADS, smem, S(stream)>>>(P);
+  }
+  CK(cudaGetLastError(), "dense_moe_kernel launch");
+  (void)al16;
+  return QMOE_OK;
+}
+
+}  // extern "C"

@@ -105,7 +105,8 @@ class CompressedMoELayer:
         self.expert_count = torch.zeros(self.E, dtype=torch.int32, device=dev)
         self.order = torch.zeros(max(1, T), dtype=torch.int32, device=dev)
         # FFN hidden: relu(bf16(wi @ x)) per token, bf16 rows (wo-pass x)
-        self.h = _lib.padded_empty(max(1, T) * self.d_ff, torch.bfloat16, dev).view(max(1, T), self.d_ff)
+        ldh = (self.d_ff + 7) // 8 * 8  # 16-byte aligned hidden rows (bulk staging)
+        self.h = _lib.padded_empty(max(1, T) * ldh, torch.bfloat16, dev).view(max(1, T), ldh)[:, : self.d_ff]
         self.bad = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
         self.counters = torch.zeros(max(1, T) + 1, dtype=torch.int32, device=dev)  # fused step (self-resetting)
 
@@ -202,6 +203,11 @@ class CompressedMoELayer:
             buf = _lib.padded_empty(T * self.d_model, x.dtype, x.device).view(T, self.d_model)
             buf.copy_(x)
             x = buf
+        if self.use_dense(T):
+            self.plan(assign, stream)
+            self.pass_dense(x, 0, self.h, _lib.QMOE_Y_RELU_BF16, stream)
+            self.pass_dense(self.h, 1, out, _lib.QMOE_Y_STORE_F32, stream)
+            return out
         if self.fused:
             try:
                 self.step(x, assign, out, stream)
@@ -214,6 +220,30 @@ class CompressedMoELayer:
             self.pass_wi(x, stream)
             self.pass_wo(out, stream)
         return out
+
+    DENSE_MIN_TOKENS = 6.0  # tokens per touched expert above which decode-then-MMA wins
+
+    def use_dense(self, T: int) -> bool:
+        """Batched regime: each expert block decoded once and multiplied with
+        all its tokens on the tensor cores (qmoe_dense_moe_pass)."""
+        if self.packed or not bool(self.dic.device_info(self.device.index)["sparse_path"]):
+            return False
+        mode = os.environ.get("QMOE_DENSE", "auto")
+        if mode in ("0", "1"):
+            return mode == "1"
+        return T / self._runs_est(T) >= self.DENSE_MIN_TOKENS
+
+    def pass_dense(self, x, which: int, y, y_mode: int, stream=None) -> None:
+        import torch
+
+        T = self._T
+        bn = 64 if T / self._runs_est(T) > 24 else 32
+        rows, cols = (self.d_ff, self.d_model) if which == 0 else (self.d_model, self.d_ff)
+        xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
+        _lib.check(_lib.lib.qmoe_dense_moe_pass(
+            self.handle, self._table(), _lib.ptr(self.mats), self.E, which, _lib.ptr(self.expert_count),
+            _lib.ptr(self.order), rows, cols, _lib.ptr(x), xt, x.stride(0), _lib.ptr(y), y_mode, y.stride(0), bn,
+            0, _lib.stream_ptr(stream)))
 
     def step(self, x, assign, out, stream=None) -> None:
         """The whole step as one cooperative launch (qmoe_moe_step)."""

@@ -148,3 +148,42 @@ def test_moe_segmented_rows_vs_oracle(dic, odic, d_model, d_ff):
     d = bf16_ulp_diff(y, y_ref)
     assert d.max() <= 2
     assert np.mean(d == 0) >= 0.99
+
+
+@pytest.mark.parametrize("T", [40, 200])
+def test_moe_dense_decode_then_mma_vs_oracle(dic, odic, T):
+    """Batched regime: decode-then-MMA passes (qmoe_dense_moe_pass) — several
+    row blocks, K chunks with straddling codewords, experts with 0, < 32 and
+    > 64 tokens — against the composed oracle and the streaming path."""
+    import os
+
+    rng = np.random.default_rng(T + 7)
+    E, d_model, d_ff = 4, 320, 1100  # 1100 rows: 3 row blocks (last partial); 320 cols: 5 chunks
+    wi, wo, host = [], [], []
+    for e in range(E):
+        pair = []
+        for rows, cols, lst in ((d_ff, d_model, wi), (d_model, d_ff, wo)):
+            w = (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+            t = q.rtn_quantize(w, q.make_grid(w))
+            c = q.encode(t, dic)
+            lst.append(c.to_device(dic))
+            pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
+        host.append(tuple(pair))
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+    x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
+    assign = np.where(np.arange(T) % 5 == 0, 1, rng.integers(0, 3, size=T)).astype(np.int32)  # expert 3: no tokens
+    os.environ["QMOE_DENSE"] = "1"
+    try:
+        y = layer.forward(x, assign)
+    finally:
+        os.environ.pop("QMOE_DENSE")
+    y_ref = O.moe_layer(x, assign, host, odic)
+    d = bf16_ulp_diff(y, y_ref)
+    assert d.max() <= 2, d.max()
+    assert np.mean(d == 0) >= 0.99
+    os.environ["QMOE_DENSE"] = "0"
+    try:
+        y_stream = layer.forward(x, assign)
+    finally:
+        os.environ.pop("QMOE_DENSE")
+    assert bf16_ulp_diff(y, y_stream).max() <= 2
