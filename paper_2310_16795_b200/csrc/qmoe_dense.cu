@@ -170,39 +170,63 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_moe_kernel(DenseParams P) {
       wlo = mm & 0xFFFFu;
       whi = mm >> 16;
     }
-    int gcur = -1;
-    uint4 g = make_uint4(0u, 0u, 0u, 0u);
+    // token ids of the item (shared), then the first chunk's token tile in registers
+    __shared__ int s_tok[64];
+    if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
+    __syncthreads();
+    constexpr int XPT = BN * BK / DTHREADS;  // token-tile elements per thread
+    uint16_t xr[XPT];
+    auto load_x_chunk = [&](int k0) {
+#pragma unroll
+      for (int u = 0; u < XPT; ++u) {
+        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
+        xr[u] = (n < nt && k0 + k < P.cols) ? x_bf16_bits(P.x, P.x_bf16, (int64_t)s_tok[n] * P.ldx + k0 + k)
+                                            : (uint16_t)0;
+      }
+    };
+    load_x_chunk(0);
+    // codeword groups: current + one prefetched
+    int gcur = valid && p < pend ? (p >> 3) : -1;
+    uint4 g = make_uint4(0u, 0u, 0u, 0u), gn = g;
+    if (gcur >= 0) {
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+                   : "l"(M.cw + (size_t)gcur * 8));
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
+                   : "l"(M.cw + (size_t)(gcur + 1) * 8));
+    }
+    const int glast = valid && pend > 0 ? (pend - 1) >> 3 : 0;
     float acc[2][NT8][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
-      for (int j = 0; j < NT8; ++j)
+      for (int j2 = 0; j2 < NT8; ++j2)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[i][j][k] = 0.f;
+        for (int k2 = 0; k2 < 4; ++k2) acc[i2][j2][k2] = 0.f;
     int chunk = 0;
     for (int k0 = 0; k0 < P.cols; k0 += BK, ++chunk) {
       const int k1 = k0 + BK;
-      // ---- token tile (double-buffered): Xt[n][k] bf16, swizzled like W
+      // ---- token tile of this chunk (double-buffered): registers -> Xt[n][k] bf16, swizzled like W
       const uint32_t xb = x_s + (uint32_t)(chunk & 1) * (BN * 128u);
-      for (int i = tid; i < BN * BK; i += DTHREADS) {
-        const int n = i / BK, k = i % BK;
-        uint32_t v = 0;
-        if (n < nt && k0 + k < P.cols) {
-          const int t = __ldg(P.order + tok0 + n);
-          v = x_bf16_bits(P.x, P.x_bf16, (int64_t)t * P.ldx + k0 + k);
-        }
-        sts_u16(xb + (uint32_t)n * 128u + (((uint32_t)k * 2u) ^ ((uint32_t)(n & 7) << 4)), v);
-      }
-      // ---- decode my row's columns [k0, k1) into the W tile
 #pragma unroll
-      for (int c16 = 0; c16 < 8; ++c16) sts_zero16(rowb + 16u * c16);
+      for (int u = 0; u < XPT; ++u) {
+        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
+        sts_u16(xb + (uint32_t)n * 128u + (((uint32_t)k * 2u) ^ ((uint32_t)(n & 7) << 4)), xr[u]);
+      }
+      if (k1 < P.cols) load_x_chunk(k1);  // next chunk's tile in flight during decode + mma
+      // ---- decode my row's columns [k0, k1) into the W tile (zero-fill: lanes
+      // start at different 16-byte chunks, so the 8 stores are conflict-free)
+#pragma unroll
+      for (int c16 = 0; c16 < 8; ++c16) sts_zero16(rowb + 16u * (uint32_t)((c16 + lane) & 7));
       while (valid && p < pend && col < k1) {
         const int grp = p >> 3;
-        if (grp != gcur) {
-          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
-                       : "l"(M.cw + (size_t)grp * 8));
+        if (grp != gcur) {  // advance to the prefetched group, prefetch the one after
+          g = gn;
           gcur = grp;
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
+                       : "l"(M.cw + (size_t)min(grp + 1, glast) * 8));
         }
         const uint32_t wd = (p & 4) ? ((p & 2) ? g.w : g.z) : ((p & 2) ? g.y : g.x);
         const uint32_t c = (p & 1) ? (wd >> 16) : (wd & 0xFFFFu);
@@ -259,7 +283,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_moe_kernel(DenseParams P) {
           const int row = rb * BM + warp * 32 + mi * 16 + (lane >> 2) + ((h & 2) ? 8 : 0);
           const int n = nj * 8 + (lane & 3) * 2 + (h & 1);
           if (row >= P.rows || n >= nt) continue;
-          const int64_t t = __ldg(P.order + tok0 + n);
+          const int64_t t = s_tok[n];
           const float v = bf16_round_dev(acc[mi][nj][h]);
           if (P.y_mode == QMOE_Y_RELU_BF16) {
             reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
@@ -274,6 +298,268 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_moe_kernel(DenseParams P) {
     }
     __syncthreads();  // token tile buffers reused by the next item
   }
+}
+
+// ------------------------------------------------------------------ tcgen05 variant
+// Same decode; the MMA runs on the 5th-generation tensor cores: one elected
+// thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128 rows, N = BN
+// tokens, K = 16) from shared-memory descriptors over the SW128 K-major tiles
+// (the decode's XOR swizzle IS the canonical 128-byte swizzle), accumulating
+// in TMEM (4 row blocks x BN fp32 columns); tcgen05.commit signals an
+// mbarrier before the tiles are overwritten. Warp w's TMEM lane quarter holds
+// exactly the 32 rows its lanes decoded, read back with tcgen05.ld.32x32b.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  // start >> 4 [0,14) | LBO (unused for swizzled K-major) = 1 [16,30) |
+  // SBO = 1024 B between 8-row groups [32,46) | version 1 [46,48) | SWIZZLE_128B = 2 [61,64)
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+template <int BN>
+__device__ __forceinline__ uint32_t idesc_bf16_f32() {
+  // c F32 [4,6) | a BF16 [7,10) | b BF16 [10,13) | K-major A, B | N >> 3 [17,23) | M >> 4 [24,29)
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(mb), "r"(parity)
+                 : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
+  __shared__ __align__(8) uint64_t tab_bar, mma_bar;
+  __shared__ int s_total;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_tok[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t base = sbase();
+  const uint32_t tab_s = base;
+  // operand tiles 1024-byte aligned in the shared window (SW128 atoms)
+  const uint32_t w_s = (base + P.w_off + 1023u) & ~1023u, x_s = w_s + (uint32_t)BM * 128u;
+  int* start = reinterpret_cast<int*>(dsm + P.plan_off);
+  int* ipre = start + P.E + 1;
+  const int E = P.E;
+  const int nrb = (P.rows + BM - 1) / BM;
+  constexpr uint32_t TMEM_COLS = 4 * BN;  // 4 row blocks x BN fp32 columns (128 or 256)
+  const uint32_t tb_mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
+  const uint32_t mma_mb = (uint32_t)__cvta_generic_to_shared(&mma_bar);
+  if (warp == 0) {  // TMEM accumulators (warp-wide alloc)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_mb));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma_mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)P.H * 4;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tb_mb), "r"(bytes) : "memory");
+    for (uint32_t o = 0; o < bytes; o += 32768u)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tab_s + o),
+          "l"(reinterpret_cast<const char*>(P.gtab) + o), "r"(min(32768u, bytes - o)), "r"(tb_mb)
+          : "memory");
+    int a = 0, it = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = __ldg(P.count + e);
+      start[e] = a;
+      ipre[e] = it;
+      a += c;
+      it += nrb * ((c + BN - 1) / BN);
+    }
+    start[E] = a;
+    ipre[E] = it;
+    s_total = it;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  mbar_wait(tb_mb, 0);
+  const uint32_t tmem = s_tmem;
+  const int total = s_total;
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t rowb = w_s + (uint32_t)tid * 128u;
+  const uint32_t rx = (uint32_t)(tid & 7) << 4;
+  const uint32_t idesc = idesc_bf16_f32<BN>();
+  uint32_t mma_phase = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    int lo = 0, hi = E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ipre[mid] <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    const int e = lo, local = item - ipre[e];
+    const int rb = local % nrb, tb = local / nrb;
+    const int cnt = start[e + 1] - start[e];
+    const int nt = min(BN, cnt - tb * BN);
+    const int tok0 = start[e] + tb * BN;
+    const qmoe_matrix& M = P.mats[2 * e + P.pass];
+    const int r = rb * BM + tid;
+    const bool valid = r < P.rows;
+    int p = 0, pend = 0, col = 0;
+    uint32_t wlo = 0, whi = 0;
+    if (valid) {
+      p = __ldg(M.row_off + r);
+      pend = __ldg(M.row_off + r + 1);
+      const uint32_t mm = __ldg(M.row_minmax + r);
+      wlo = mm & 0xFFFFu;
+      whi = mm >> 16;
+    }
+    if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
+    __syncthreads();
+    constexpr int XPT = BN * BK / DTHREADS;
+    uint16_t xr[XPT];
+    auto load_x_chunk = [&](int k0) {
+#pragma unroll
+      for (int u = 0; u < XPT; ++u) {
+        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
+        xr[u] = (n < nt && k0 + k < P.cols) ? x_bf16_bits(P.x, P.x_bf16, (int64_t)s_tok[n] * P.ldx + k0 + k)
+                                            : (uint16_t)0;
+      }
+    };
+    load_x_chunk(0);
+    int gcur = valid && p < pend ? (p >> 3) : -1;
+    uint4 g = make_uint4(0u, 0u, 0u, 0u), gn = g;
+    if (gcur >= 0) {
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+                   : "l"(M.cw + (size_t)gcur * 8));
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
+                   : "l"(M.cw + (size_t)(gcur + 1) * 8));
+    }
+    const int glast = valid && pend > 0 ? (pend - 1) >> 3 : 0;
+    int chunk = 0;
+    for (int k0 = 0; k0 < P.cols; k0 += BK, ++chunk) {
+      const int k1 = k0 + BK;
+      if (chunk > 0) {  // previous chunk's MMAs must be done reading the W / X tiles
+        mbar_wait(mma_mb, mma_phase);
+        mma_phase ^= 1u;
+      }
+      const uint32_t xb = x_s + (uint32_t)(chunk & 1) * (BN * 128u);
+#pragma unroll
+      for (int u = 0; u < XPT; ++u) {
+        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
+        sts_u16(xb + (uint32_t)n * 128u + (((uint32_t)k * 2u) ^ ((uint32_t)(n & 7) << 4)), xr[u]);
+      }
+      if (k1 < P.cols) load_x_chunk(k1);
+#pragma unroll
+      for (int c16 = 0; c16 < 8; ++c16) sts_zero16(rowb + 16u * (uint32_t)((c16 + lane) & 7));
+      while (valid && p < pend && col < k1) {
+        const int grp = p >> 3;
+        if (grp != gcur) {
+          g = gn;
+          gcur = grp;
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
+                       : "l"(M.cw + (size_t)min(grp + 1, glast) * 8));
+        }
+        const uint32_t wd = (p & 4) ? ((p & 2) ? g.w : g.z) : ((p & 2) ? g.y : g.x);
+        const uint32_t c = (p & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+        const uint32_t en = c < H ? lds_u32(tab_s + 4 * c) : __ldg(P.gtab + c);
+        const int n2 = (int)(en >> 28) * 2;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
+          if (f != 0x7Fu) {
+            const int vk = col + (int)(f >> 2) - k0;
+            if ((unsigned)vk < (unsigned)BK)
+              sts_u16(rowb + (((uint32_t)vk * 2u) ^ rx), ((en >> (24 + j)) & 1u) ? whi : wlo);
+          }
+        }
+        if (col + n2 > k1) break;
+        col += n2;
+        ++p;
+      }
+      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int mb = 0; mb < BM / 128; ++mb) {
+#pragma unroll
+          for (int ks = 0; ks < BK / 16; ++ks) {
+            const uint64_t da = sw128_desc(w_s + (uint32_t)mb * 128u * 128u + (uint32_t)ks * 32u);
+            const uint64_t db = sw128_desc(xb + (uint32_t)ks * 32u);
+            const uint32_t acc = (chunk > 0 || ks > 0) ? 1u : 0u;
+            asm volatile(
+                "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+                    tmem + (uint32_t)mb * BN),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mma_mb)
+                     : "memory");
+      }
+    }
+    mbar_wait(mma_mb, mma_phase);  // last chunk's MMAs: accumulators final
+    mma_phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- epilogue: warp w reads TMEM lanes 32(w%4).. = rows 32w.. of the item, columns of block w/4
+    {
+      uint32_t v[BN];
+      const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * BN;
+      if (BN == 64) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,"
+            "%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32 % BN]), "=r"(v[33 % BN]), "=r"(v[34 % BN]),
+              "=r"(v[35 % BN]), "=r"(v[36 % BN]), "=r"(v[37 % BN]), "=r"(v[38 % BN]), "=r"(v[39 % BN]),
+              "=r"(v[40 % BN]), "=r"(v[41 % BN]), "=r"(v[42 % BN]), "=r"(v[43 % BN]), "=r"(v[44 % BN]),
+              "=r"(v[45 % BN]), "=r"(v[46 % BN]), "=r"(v[47 % BN]), "=r"(v[48 % BN]), "=r"(v[49 % BN]),
+              "=r"(v[50 % BN]), "=r"(v[51 % BN]), "=r"(v[52 % BN]), "=r"(v[53 % BN]), "=r"(v[54 % BN]),
+              "=r"(v[55 % BN]), "=r"(v[56 % BN]), "=r"(v[57 % BN]), "=r"(v[58 % BN]), "=r"(v[59 % BN]),
+              "=r"(v[60 % BN]), "=r"(v[61 % BN]), "=r"(v[62 % BN]), "=r"(v[63 % BN])
+            : "r"(ta));
+      } else {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(ta));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (valid) {
+#pragma unroll
+        for (int n = 0; n < BN; ++n) {
+          if (n >= nt) break;
+          const int64_t t = s_tok[n];
+          const float vv = bf16_round_dev(__uint_as_float(v[n]));
+          if (P.y_mode == QMOE_Y_RELU_BF16) {
+            reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(vv, 0.f)) >> 16);
+          } else if (P.y_mode == QMOE_Y_STORE_F32) {
+            reinterpret_cast<float*>(P.y)[t * P.ldy + r] = vv + 0.f;
+          } else {
+            float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + r;
+            *yp = *yp + vv;
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // TMEM read before the next item's first MMA; token ids reused
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
 bool al16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
@@ -309,7 +595,7 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.y_mode = y_mode;
   P.ldy = ldy;
   const int BN = tokens_per_block;
-  const size_t wbytes = (size_t)BM * 128, xbytes = (size_t)2 * BN * 128;
+  const size_t wbytes = (size_t)BM * 128 + 1024, xbytes = (size_t)2 * BN * 128;  // + 1 KB: SW128 alignment
   const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
   const size_t static_smem = 1024;
   if (wbytes + xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
@@ -323,7 +609,15 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.plan_off = P.x_off + (int)xbytes;
   const size_t smem = (size_t)P.plan_off + plan;
   const int grid = d->num_sms;
-  if (BN == 64) {
+  if (!getenv("QMOE_DENSE_HMMA")) {  // tcgen05 (default) vs the legacy mma.sync variant
+    if (BN == 64) {
+      CK(cudaFuncSetAttribute(dense_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+      dense_tc_kernel<64><<<grid, DTHREADS, smem, S(stream)>>>(P);
+    } else {
+      CK(cudaFuncSetAttribute(dense_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+      dense_tc_kernel<32><<<grid, DTHREADS, smem, S(stream)>>>(P);
+    }
+  } else if (BN == 64) {
     CK(cudaFuncSetAttribute(dense_moe_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
     dense_moe_kernel<64><<<grid, DTHREADS, smem, S(stream)>>>(P);
   } else {
