@@ -56,26 +56,13 @@ struct DenseParams {
   int y_mode;
   int64_t ldy;
   int w_off, x_off, plan_off;  // byte offsets in dynamic shared memory
+  int dbg;                     // experiment switches (QMOE_DENSE_DBG): 1 skip mma, 2 skip decode
 };
 
 __device__ __forceinline__ uint32_t sbase() {
   uint32_t b;
   asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(b) : "l"(dsm));
   return b;
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 __device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
@@ -93,211 +80,6 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 __device__ __forceinline__ uint16_t x_bf16_bits(const void* x, int bf16, int64_t i) {
   if (bf16) return __ldg(reinterpret_cast<const unsigned short*>(x) + i);
   return (uint16_t)(__float_as_uint(__ldg(reinterpret_cast<const float*>(x) + i)) >> 16);  // x is bf16-valued
-}
-
-template <int BN>
-__global__ void __launch_bounds__(DTHREADS, 1) dense_moe_kernel(DenseParams P) {
-  __shared__ __align__(8) uint64_t tab_bar;
-  __shared__ int s_total;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t base = sbase();
-  const uint32_t tab_s = base, w_s = base + P.w_off, x_s = base + P.x_off;
-  int* start = reinterpret_cast<int*>(dsm + P.plan_off);  // E + 1
-  int* ipre = start + P.E + 1;                              // E + 1: items before expert e
-  const int E = P.E;
-  const int nrb = (P.rows + BM - 1) / BM;
-  // ---- hot table (bulk copy, overlaps the item plan)
-  if (tid == 0) {
-    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t bytes = (uint32_t)P.H * 4;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-    for (uint32_t o = 0; o < bytes; o += 32768u)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tab_s + o),
-          "l"(reinterpret_cast<const char*>(P.gtab) + o), "r"(min(32768u, bytes - o)), "r"(mb)
-          : "memory");
-    // ---- item plan (serial over experts; E <= a few thousand)
-    int a = 0, it = 0;
-    for (int e = 0; e < E; ++e) {
-      const int c = __ldg(P.count + e);
-      start[e] = a;
-      ipre[e] = it;
-      a += c;
-      it += nrb * ((c + BN - 1) / BN);
-    }
-    start[E] = a;
-    ipre[E] = it;
-    s_total = it;
-  }
-  __syncthreads();
-  {
-    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
-    uint32_t done = 0;
-    while (!done)
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done)
-                   : "r"(mb)
-                   : "memory");
-  }
-  const int total = s_total;
-  const uint32_t H = (uint32_t)P.H;
-  const uint32_t rowb = w_s + (uint32_t)tid * 128u;  // my W-tile row
-  const uint32_t rx = (uint32_t)(tid & 7) << 4;      // its 16-byte-chunk swizzle
-  constexpr int NT8 = BN / 8;
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    int lo = 0, hi = E - 1;  // expert of the item: last e with ipre[e] <= item
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (ipre[mid] <= item) lo = mid;
-      else hi = mid - 1;
-    }
-    const int e = lo, local = item - ipre[e];
-    const int rb = local % nrb, tb = local / nrb;
-    const int cnt = start[e + 1] - start[e];
-    const int nt = min(BN, cnt - tb * BN);
-    const int tok0 = start[e] + tb * BN;
-    const qmoe_matrix& M = P.mats[2 * e + P.pass];
-    const int r = rb * BM + tid;
-    const bool valid = r < P.rows;
-    int p = 0, pend = 0, col = 0;
-    uint32_t wlo = 0, whi = 0;
-    if (valid) {
-      p = __ldg(M.row_off + r);
-      pend = __ldg(M.row_off + r + 1);
-      const uint32_t mm = __ldg(M.row_minmax + r);
-      wlo = mm & 0xFFFFu;
-      whi = mm >> 16;
-    }
-    // token ids of the item (shared), then the first chunk's token tile in registers
-    __shared__ int s_tok[64];
-    if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
-    __syncthreads();
-    constexpr int XPT = BN * BK / DTHREADS;  // token-tile elements per thread
-    uint16_t xr[XPT];
-    auto load_x_chunk = [&](int k0) {
-#pragma unroll
-      for (int u = 0; u < XPT; ++u) {
-        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
-        xr[u] = (n < nt && k0 + k < P.cols) ? x_bf16_bits(P.x, P.x_bf16, (int64_t)s_tok[n] * P.ldx + k0 + k)
-                                            : (uint16_t)0;
-      }
-    };
-    load_x_chunk(0);
-    // codeword groups: current + one prefetched
-    int gcur = valid && p < pend ? (p >> 3) : -1;
-    uint4 g = make_uint4(0u, 0u, 0u, 0u), gn = g;
-    if (gcur >= 0) {
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
-                   : "l"(M.cw + (size_t)gcur * 8));
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
-                   : "l"(M.cw + (size_t)(gcur + 1) * 8));
-    }
-    const int glast = valid && pend > 0 ? (pend - 1) >> 3 : 0;
-    float acc[2][NT8][4];
-#pragma unroll
-    for (int i2 = 0; i2 < 2; ++i2)
-#pragma unroll
-      for (int j2 = 0; j2 < NT8; ++j2)
-#pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) acc[i2][j2][k2] = 0.f;
-    int chunk = 0;
-    for (int k0 = 0; k0 < P.cols; k0 += BK, ++chunk) {
-      const int k1 = k0 + BK;
-      // ---- token tile of this chunk (double-buffered): registers -> Xt[n][k] bf16, swizzled like W
-      const uint32_t xb = x_s + (uint32_t)(chunk & 1) * (BN * 128u);
-#pragma unroll
-      for (int u = 0; u < XPT; ++u) {
-        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
-        sts_u16(xb + (uint32_t)n * 128u + (((uint32_t)k * 2u) ^ ((uint32_t)(n & 7) << 4)), xr[u]);
-      }
-      if (k1 < P.cols) load_x_chunk(k1);  // next chunk's tile in flight during decode + mma
-      // ---- decode my row's columns [k0, k1) into the W tile (zero-fill: lanes
-      // start at different 16-byte chunks, so the 8 stores are conflict-free)
-#pragma unroll
-      for (int c16 = 0; c16 < 8; ++c16) sts_zero16(rowb + 16u * (uint32_t)((c16 + lane) & 7));
-      while (valid && p < pend && col < k1) {
-        const int grp = p >> 3;
-        if (grp != gcur) {  // advance to the prefetched group, prefetch the one after
-          g = gn;
-          gcur = grp;
-          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
-                       : "l"(M.cw + (size_t)min(grp + 1, glast) * 8));
-        }
-        const uint32_t wd = (p & 4) ? ((p & 2) ? g.w : g.z) : ((p & 2) ? g.y : g.x);
-        const uint32_t c = (p & 1) ? (wd >> 16) : (wd & 0xFFFFu);
-        const uint32_t en = c < H ? lds_u32(tab_s + 4 * c) : __ldg(P.gtab + c);
-        const int n2 = (int)(en >> 28) * 2;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
-          if (f != 0x7Fu) {
-            const int vk = col + (int)(f >> 2) - k0;  // column inside the chunk
-            if ((unsigned)vk < (unsigned)BK)
-              sts_u16(rowb + (((uint32_t)vk * 2u) ^ rx), ((en >> (24 + j)) & 1u) ? whi : wlo);
-          }
-        }
-        if (col + n2 > k1) break;  // straddles the chunk end: revisit next chunk
-        col += n2;
-        ++p;
-      }
-      __syncthreads();  // token tile staged (W rows: each warp reads only its own)
-      // ---- mma: rows [32 warp, +32) x BN tokens x 64 columns
-#pragma unroll
-      for (int ks = 0; ks < BK / 16; ++ks) {
-        uint32_t a[2][4];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          const int row = warp * 32 + mi * 16 + (lane & 15);
-          const uint32_t ch = (uint32_t)(ks * 2 + (lane >> 4));
-          ldsm_x4(w_s + (uint32_t)row * 128u + ((ch ^ (uint32_t)(row & 7)) << 4), a[mi][0], a[mi][1], a[mi][2],
-                  a[mi][3]);
-        }
-#pragma unroll
-        for (int nj = 0; nj < NT8; nj += 2) {
-          // four 8x8 matrices: (n-tile nj, k lo), (nj, k hi), (nj+1, k lo), (nj+1, k hi)
-          const int n = nj * 8 + (lane & 7) + ((lane >> 4) << 3);
-          const uint32_t ch = (uint32_t)(ks * 2 + ((lane >> 3) & 1));
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(xb + (uint32_t)n * 128u + ((ch ^ (uint32_t)(n & 7)) << 4), b0, b1, b2, b3);
-#pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
-            mma16816(acc[mi][nj], a[mi], b0, b1);
-            mma16816(acc[mi][nj + 1], a[mi], b2, b3);
-          }
-        }
-      }
-      __syncwarp();  // this warp's W rows are rewritten by the next chunk's decode
-    }
-    // ---- epilogue: C fragment (row g, cols 2t, 2t+1) and (row g+8, ...)
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-#pragma unroll
-      for (int nj = 0; nj < NT8; ++nj) {
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int row = rb * BM + warp * 32 + mi * 16 + (lane >> 2) + ((h & 2) ? 8 : 0);
-          const int n = nj * 8 + (lane & 3) * 2 + (h & 1);
-          if (row >= P.rows || n >= nt) continue;
-          const int64_t t = s_tok[n];
-          const float v = bf16_round_dev(acc[mi][nj][h]);
-          if (P.y_mode == QMOE_Y_RELU_BF16) {
-            reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
-          } else if (P.y_mode == QMOE_Y_STORE_F32) {
-            reinterpret_cast<float*>(P.y)[t * P.ldy + row] = v + 0.f;
-          } else {
-            float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
-            *yp = *yp + v;
-          }
-        }
-      }
-    }
-    __syncthreads();  // token tile buffers reused by the next item
-  }
 }
 
 // ------------------------------------------------------------------ tcgen05 variant
@@ -425,17 +207,19 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
       }
     };
     load_x_chunk(0);
-    int gcur = valid && p < pend ? (p >> 3) : -1;
-    uint4 g = make_uint4(0u, 0u, 0u, 0u), gn = g;
-    if (gcur >= 0) {
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
-                   : "l"(M.cw + (size_t)gcur * 8));
+    // codeword groups: the current group's 8 entries stay looked up across
+    // chunks; the next group is prefetched
+    const uint16_t* cwp = M.cw;
+    const int glast = valid && pend > 0 ? (pend - 1) >> 3 : 0;
+    int gcur = -1;
+    uint4 gn = make_uint4(0u, 0u, 0u, 0u);
+    uint32_t ent[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ent[u] = 0x007F7F7Fu;
+    if (valid && p < pend)
       asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                    : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
-                   : "l"(M.cw + (size_t)(gcur + 1) * 8));
-    }
-    const int glast = valid && pend > 0 ? (pend - 1) >> 3 : 0;
+                   : "l"(cwp + (size_t)(p >> 3) * 8));
     int chunk = 0;
     for (int k0 = 0; k0 < P.cols; k0 += BK, ++chunk) {
       const int k1 = k0 + BK;
@@ -452,36 +236,56 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
       if (k1 < P.cols) load_x_chunk(k1);
 #pragma unroll
       for (int c16 = 0; c16 < 8; ++c16) sts_zero16(rowb + 16u * (uint32_t)((c16 + lane) & 7));
-      while (valid && p < pend && col < k1) {
+      bool go = valid && p < pend && col < k1 && !(P.dbg & 2);
+      while (go) {
         const int grp = p >> 3;
-        if (grp != gcur) {
-          g = gn;
+        if (grp != gcur) {  // new group: take the prefetched words, look all 8 up, prefetch the next
+          const uint4 g = gn;
           gcur = grp;
           asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                        : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
-                       : "l"(M.cw + (size_t)min(grp + 1, glast) * 8));
-        }
-        const uint32_t wd = (p & 4) ? ((p & 2) ? g.w : g.z) : ((p & 2) ? g.y : g.x);
-        const uint32_t c = (p & 1) ? (wd >> 16) : (wd & 0xFFFFu);
-        const uint32_t en = c < H ? lds_u32(tab_s + 4 * c) : __ldg(P.gtab + c);
-        const int n2 = (int)(en >> 28) * 2;
+                       : "l"(cwp + (size_t)min(grp + 1, glast) * 8));
+          const uint32_t w4[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
-          if (f != 0x7Fu) {
-            const int vk = col + (int)(f >> 2) - k0;
-            if ((unsigned)vk < (unsigned)BK)
-              sts_u16(rowb + (((uint32_t)vk * 2u) ^ rx), ((en >> (24 + j)) & 1u) ? whi : wlo);
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t c = (u & 1) ? (w4[u >> 1] >> 16) : (w4[u >> 1] & 0xFFFFu);
+            ent[u] = c < H ? lds_u32(tab_s + 4 * c) : __ldg(P.gtab + c);
           }
         }
-        if (col + n2 > k1) break;
-        col += n2;
-        ++p;
+        // walk the group's codewords from p: only the column add is in the chain
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = grp * 8 + u;
+          if (go && q >= p) {
+            if (q >= pend || col >= k1) {
+              go = false;
+            } else {
+              const uint32_t en = ent[u];
+#pragma unroll
+              for (int j = 0; j < 3; ++j) {
+                const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
+                const int vk = col + (int)(f >> 2) - k0;  // column inside the chunk (f = 0x7F: unused slot)
+                if (f != 0x7Fu && (unsigned)vk < (unsigned)BK)
+                  sts_u16(rowb + (((uint32_t)vk * 2u) ^ rx), ((en >> (24 + j)) & 1u) ? whi : wlo);
+              }
+              const int n2 = (int)(en >> 28) * 2;
+              if (col + n2 > k1) {
+                go = false;  // straddles the chunk end: revisit next chunk
+              } else {
+                col += n2;
+                p = q + 1;
+              }
+            }
+          }
+        }
+        go = go && p < pend && col < k1;
       }
       // generic-proxy smem writes -> visible to the tensor core (async proxy)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
-      if (tid == 0) {
+      if (tid == 0 && (P.dbg & 1)) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mma_mb) : "memory");
+      } else if (tid == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
         for (int mb = 0; mb < BM / 128; ++mb) {
@@ -595,6 +399,7 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.y_mode = y_mode;
   P.ldy = ldy;
   const int BN = tokens_per_block;
+  P.dbg = getenv("QMOE_DENSE_DBG") ? atoi(getenv("QMOE_DENSE_DBG")) : 0;
   const size_t wbytes = (size_t)BM * 128 + 1024, xbytes = (size_t)2 * BN * 128;  // + 1 KB: SW128 alignment
   const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
   const size_t static_smem = 1024;
@@ -609,20 +414,12 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.plan_off = P.x_off + (int)xbytes;
   const size_t smem = (size_t)P.plan_off + plan;
   const int grid = d->num_sms;
-  if (!getenv("QMOE_DENSE_HMMA")) {  // tcgen05 (default) vs the legacy mma.sync variant
-    if (BN == 64) {
-      CK(cudaFuncSetAttribute(dense_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-      dense_tc_kernel<64><<<grid, DTHREADS, smem, S(stream)>>>(P);
-    } else {
-      CK(cudaFuncSetAttribute(dense_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-      dense_tc_kernel<32><<<grid, DTHREADS, smem, S(stream)>>>(P);
-    }
-  } else if (BN == 64) {
-    CK(cudaFuncSetAttribute(dense_moe_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    dense_moe_kernel<64><<<grid, DTHREADS, smem, S(stream)>>>(P);
+  if (BN == 64) {
+    CK(cudaFuncSetAttribute(dense_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    dense_tc_kernel<64><<<grid, DTHREADS, smem, S(stream)>>>(P);
   } else {
-    CK(cudaFuncSetAttribute(dense_moe_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    dense_moe_kernel<32><<<grid, DTHREADS, smem, S(stream)>>>(P);
+    CK(cudaFuncSetAttribute(dense_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    dense_tc_kernel<32><<<grid, DTHREADS, smem, S(stream)>>>(P);
   }
   CK(cudaGetLastError(), "dense_moe_kernel launch");
   (void)al16;

@@ -221,7 +221,7 @@ class CompressedMoELayer:
             self.pass_wo(out, stream)
         return out
 
-    DENSE_MIN_TOKENS = 6.0  # tokens per touched expert above which decode-then-MMA wins
+    DENSE_MIN_TOKENS = 12.0  # tokens per touched expert above which decode-then-MMA wins (measured)
 
     def use_dense(self, T: int) -> bool:
         """Batched regime: each expert block decoded once and multiplied with
