@@ -314,6 +314,9 @@ int qmoe_dense_moe_pass(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_ma
  * qmoe_moe_step phases (0 start, 1 plan + table staged, 2 wi done, 3 wo
  * done); NULL disables. Not for production use. */
 int qmoe_debug_step_trace(void* d_buf);
+/* Debug hook: an empty kernel of num_sms CTAs x threads with smem_bytes of
+ * dynamic shared memory (launch-floor measurements). */
+int qmoe_debug_empty_launch(int32_t smem_bytes, int32_t threads, void* stream);
 
 #ifdef __cplusplus
 }

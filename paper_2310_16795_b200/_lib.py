@@ -83,6 +83,7 @@ _SIGS = {
     "qmoe_moe_step": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, ctypes.c_int, i64, vp,
                                      i64, vp, i64, vp, vp, vp, i32, vp]),
     "qmoe_debug_step_trace": (ctypes.c_int, [vp]),
+    "qmoe_debug_empty_launch": (ctypes.c_int, [i32, i32, vp]),
     "qmoe_dense_moe_pass": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, i32, i32, vp, ctypes.c_int, i64, vp,
                                            ctypes.c_int, i64, i32, i32, vp]),
     "qmoe_pack": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -478,7 +478,7 @@ struct WinRun {
   const int32_t* ro;
   const uint32_t* mm;
   const uint16_t* ck;
-  int cols, row0, row1, lg, cklg, ntok, task0, task1, xoff;
+  int cols, row0, row1, lg, cklg, ntok, task0, task1, xoff, ri;
   int tok[NT_STREAM];
 };
 
@@ -592,8 +592,8 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
         const int need = ((R.ntok > 1 ? 8 : 4) * (R.cols + 32) + 15) & ~15;
         if (nw > 0 && xo + need > P.xbytes) break;
         if (r_end > t) {
-          src.wait(ri);  // fused step: the run's x rows are ready
           WinRun& W = win[nw++];
+          W.ri = ri;
           W.cw = R.cw; W.ro = R.ro; W.mm = R.mm; W.ck = R.ck;
           W.cols = R.cols; W.row0 = R.row0; W.row1 = R.row1; W.lg = R.lg; W.cklg = R.cklg; W.ntok = R.ntok;
           W.task0 = R.task0; W.task1 = r_end; W.xoff = xo;
@@ -611,53 +611,63 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     }
     __syncthreads();
     const int nw = S.nwin, wend = S.wend;
-    for (int w = 0; w < nw; ++w) {  // stage x (fp32; two tokens interleaved)
-      const WinRun& W = win[w];
-      if (W.ntok > 1) {
-        float2* x2 = reinterpret_cast<float2*>(xs + W.xoff);
-        for (int i = threadIdx.x; i < W.cols + 32; i += THREADS) {
-          float v0 = 0.f, v1 = 0.f;
-          if (i < W.cols) {
-            const int64_t i0 = (int64_t)W.tok[0] * P.ldx + i, i1 = (int64_t)W.tok[1] * P.ldx + i;
-            v0 = COHERENT_X ? load_x_cg(P.x, P.x_bf16, i0) : load_x(P.x, P.x_bf16, i0);
-            v1 = COHERENT_X ? load_x_cg(P.x, P.x_bf16, i1) : load_x(P.x, P.x_bf16, i1);
+    auto stage_x = [&]() {
+      for (int w = 0; w < nw; ++w) {  // stage x (fp32; two tokens interleaved)
+        const WinRun& W = win[w];
+        if (W.ntok > 1) {
+          float2* x2 = reinterpret_cast<float2*>(xs + W.xoff);
+          for (int i = threadIdx.x; i < W.cols + 32; i += THREADS) {
+            float v0 = 0.f, v1 = 0.f;
+            if (i < W.cols) {
+              const int64_t i0 = (int64_t)W.tok[0] * P.ldx + i, i1 = (int64_t)W.tok[1] * P.ldx + i;
+              v0 = COHERENT_X ? load_x_cg(P.x, P.x_bf16, i0) : load_x(P.x, P.x_bf16, i0);
+              v1 = COHERENT_X ? load_x_cg(P.x, P.x_bf16, i1) : load_x(P.x, P.x_bf16, i1);
+            }
+            x2[i] = make_float2(v0, v1);
           }
-          x2[i] = make_float2(v0, v1);
-        }
-      } else {
-        float* x1 = reinterpret_cast<float*>(xs + W.xoff);
-        for (int i = threadIdx.x; i < W.cols + 32; i += THREADS) {
-          const int64_t i0 = (int64_t)W.tok[0] * P.ldx + i;
-          x1[i] = i < W.cols ? (COHERENT_X ? load_x_cg(P.x, P.x_bf16, i0) : load_x(P.x, P.x_bf16, i0)) : 0.f;
+        } else {
+          float* x1 = reinterpret_cast<float*>(xs + W.xoff);
+          for (int i = threadIdx.x; i < W.cols + 32; i += THREADS) {
+            const int64_t i0 = (int64_t)W.tok[0] * P.ldx + i;
+            x1[i] = i < W.cols ? (COHERENT_X ? load_x_cg(P.x, P.x_bf16, i0) : load_x(P.x, P.x_bf16, i0)) : 0.f;
+          }
         }
       }
-    }
-    __syncthreads();
+    };
     // ---- per-warp pipelined walk over dynamically claimed tasks (one claimed ahead)
     int k = claim_task(&S.next);
-    if (k < wend) {
-      int wc = 0;
+    const bool active = k < wend;
+    int wc = 0, wn = 0, kn = 0, maxgc = 0, maxgn = 0;
+    bool has_n = false, nready = false;
+    Lane c{0, 0, 0, -1, 0u}, n{0, 0, 0, -1, 0u};
+    uint32_t ea[GRP], eb[GRP];
+    uint4 q1 = make_uint4(0u, 0u, 0u, 0u);
+    if (active) {  // first tasks' metadata, groups and entries: needs no x
       while (win[wc].task1 <= k) ++wc;
-      Lane c = lane_task(win[wc], k);
-      int wn = wc;
-      int kn = claim_task(&S.next);
-      bool has_n = kn < wend;
-      Lane n{0, 0, 0, -1, 0u};
+      c = lane_task(win[wc], k);
+      wn = wc;
+      kn = claim_task(&S.next);
+      has_n = kn < wend;
       if (has_n) {
         while (win[wn].task1 <= kn) ++wn;
         n = lane_task(win[wn], kn);
       }
-      int maxgc = __reduce_max_sync(FULL_MASK, lane_groups(c));
-      int maxgn = 0;
-      bool nready = false;
-      uint32_t ea[GRP], eb[GRP];
-      uint4 q1;
-      {
-        const uint4 q0 = lane_load(win[wc].cw, c, 0);
-        if (maxgc >= 2) q1 = lane_load(win[wc].cw, c, 1);
-        else q1 = has_n ? lane_load(win[wn].cw, n, 0) : make_uint4(0u, 0u, 0u, 0u);
-        lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
-      }
+      maxgc = __reduce_max_sync(FULL_MASK, lane_groups(c));
+      const uint4 q0 = lane_load(win[wc].cw, c, 0);
+      if (maxgc >= 2) q1 = lane_load(win[wc].cw, c, 1);
+      else q1 = has_n ? lane_load(win[wn].cw, n, 0) : make_uint4(0u, 0u, 0u, 0u);
+      lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
+    }
+    // x staging after the first loads are in flight (fused wo phase: the x
+    // rows are other CTAs' h — wait for their runs first)
+    if (COHERENT_X) {
+      if (threadIdx.x == 0)
+        for (int w = 0; w < nw; ++w) src.wait(win[w].ri);
+      __syncthreads();
+    }
+    stage_x();
+    __syncthreads();
+    if (active) {
       for (;;) {
         const WinRun& W = win[wc];
         const int NTc = W.ntok > 1 ? 2 : 1;
@@ -874,79 +884,128 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   trace_stamp(0);
   table_fill_async(PW.gtab, PW.H, &tab_bar);  // overlaps the plan below
   // ---- 1. plan
-  for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;
-  __syncthreads();
-  for (int t = threadIdx.x; t < T; t += THREADS) {
-    const int e = __ldg(S.assign + t);
-    if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);
-  }
-  __syncthreads();
-  {
-    const int per = (E + THREADS - 1) / THREADS;
-    const int e0 = min(E, (int)threadIdx.x * per), e1 = min(E, e0 + per);
-    int lv = 0, lw = 0;
-    for (int e = e0; e < e1; ++e) {
-      lv += cnt[e];
-      lw += (cnt[e] + ntu - 1) / ntu;
-    }
-    int bw;
-    int bv = block_excl_scan2(lv, lw, bw, wsum, tot);
-    for (int e = e0; e < e1; ++e) {
-      start[e] = bv;
-      choff[e] = bw;
-      bv += cnt[e];
-      bw += (cnt[e] + ntu - 1) / ntu;
-    }
-    if (threadIdx.x == 0) {
-      start[E] = tot[0];
-      choff[E] = tot[1];
-    }
-  }
-  __syncthreads();
-  if (blockIdx.x == 0 && S.count_out)
-    for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = cnt[e];
-  __syncthreads();
-  for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;  // fill cursor
-  __syncthreads();
-  if (threadIdx.x < 32) {  // stable placement in buffer order
-    const int lane = threadIdx.x;
-    for (int t0 = 0; t0 < T; t0 += 32) {
-      const int t = t0 + lane;
-      const int e = t < T ? __ldg(S.assign + t) : -1;
-      const bool ok = t < T && e >= 0 && e < E;
+  if (T <= 32) {
+    // small step: one warp, no block barriers. Lane t holds token t; experts
+    // are the match_any groups, ordered by id; buffer order within an expert.
+    if (blockIdx.x == 0 && S.count_out)
+      for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = 0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int e = lane < T ? __ldg(S.assign + lane) : -1;
+      const bool ok = lane < T && e >= 0 && e < E;
       const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
-      const int rank = __popc(peers & ((1u << lane) - 1u));
-      const int leader = __ffs(peers) - 1;
-      int basev = 0;
-      if (ok && lane == leader) {
-        basev = cnt[e];
-        cnt[e] = basev + __popc(peers);
+      const int c = __popc(peers), rank = __popc(peers & ((1u << lane) - 1u));
+      const bool leader = ok && (__ffs(peers) - 1) == lane;
+      const unsigned L = __ballot_sync(FULL_MASK, leader);
+      int st = 0, co = 0, tot_t = 0, tot_c = 0;
+      for (unsigned m = L; m; m &= m - 1) {  // over distinct experts
+        const int b = __ffs(m) - 1;
+        const int eb = __shfl_sync(FULL_MASK, e, b), cb = __shfl_sync(FULL_MASK, c, b);
+        if (eb < e) {
+          st += cb;
+          co += (cb + ntu - 1) / ntu;
+        }
+        tot_t += cb;
+        tot_c += (cb + ntu - 1) / ntu;
       }
-      basev = __shfl_sync(FULL_MASK, basev, leader);
-      if (ok) order[start[e] + basev + rank] = t;
+      const int my_start = __shfl_sync(FULL_MASK, st, __ffs(peers) - 1);
+      if (ok) order[my_start + rank] = lane;
       __syncwarp();
+      if (leader) {
+        if (blockIdx.x == 0 && S.count_out) S.count_out[e] = c;
+        for (int ch = 0; ch * ntu < c; ++ch) {
+          const int nt = min(ntu, c - ch * ntu);
+          runs4[4 * (co + ch)] = e;
+          runs4[4 * (co + ch) + 1] = nt;
+          runs4[4 * (co + ch) + 2] = order[st + ch * ntu];
+          runs4[4 * (co + ch) + 3] = order[st + ch * ntu + (nt > 1 ? 1 : 0)];
+        }
+      }
+      if (lane == 0) {
+        start[E] = tot_t;
+        choff[E] = tot_c;
+      }
     }
+    __syncthreads();
+    if (blockIdx.x == 0 && S.order_out && threadIdx.x < start[E]) S.order_out[threadIdx.x] = order[threadIdx.x];
+  } else {
+    for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < T; t += THREADS) {
+      const int e = __ldg(S.assign + t);
+      if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);
+    }
+    __syncthreads();
+    {
+      const int per = (E + THREADS - 1) / THREADS;
+      const int e0 = min(E, (int)threadIdx.x * per), e1 = min(E, e0 + per);
+      int lv = 0, lw = 0;
+      for (int e = e0; e < e1; ++e) {
+        lv += cnt[e];
+        lw += (cnt[e] + ntu - 1) / ntu;
+      }
+      int bw;
+      int bv = block_excl_scan2(lv, lw, bw, wsum, tot);
+      for (int e = e0; e < e1; ++e) {
+        start[e] = bv;
+        choff[e] = bw;
+        bv += cnt[e];
+        bw += (cnt[e] + ntu - 1) / ntu;
+      }
+      if (threadIdx.x == 0) {
+        start[E] = tot[0];
+        choff[E] = tot[1];
+      }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && S.count_out)
+      for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = cnt[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;  // fill cursor
+    __syncthreads();
+    if (threadIdx.x < 32) {  // stable placement in buffer order
+      const int lane = threadIdx.x;
+      for (int t0 = 0; t0 < T; t0 += 32) {
+        const int t = t0 + lane;
+        const int e = t < T ? __ldg(S.assign + t) : -1;
+        const bool ok = t < T && e >= 0 && e < E;
+        const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        const int leader = __ffs(peers) - 1;
+        int basev = 0;
+        if (ok && lane == leader) {
+          basev = cnt[e];
+          cnt[e] = basev + __popc(peers);
+        }
+        basev = __shfl_sync(FULL_MASK, basev, leader);
+        if (ok) order[start[e] + basev + rank] = t;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    const int nchp = choff[E];
+    for (int i = threadIdx.x; i < nchp; i += THREADS) {
+      int lo = 0, hi = E - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (choff[mid] <= i) lo = mid;
+        else hi = mid - 1;
+      }
+      const int e = lo, ch = i - choff[e];
+      const int c = start[e + 1] - start[e];
+      const int nt = min(ntu, c - ch * ntu);
+      runs4[4 * i] = e;
+      runs4[4 * i + 1] = nt;
+      runs4[4 * i + 2] = order[start[e] + ch * ntu];
+      runs4[4 * i + 3] = order[start[e] + ch * ntu + (nt > 1 ? 1 : 0)];
+    }
+    if (blockIdx.x == 0 && S.order_out)
+      for (int t = threadIdx.x; t < start[E]; t += THREADS) S.order_out[t] = order[t];
+
   }
   __syncthreads();
   const int nch = choff[E];
-  for (int i = threadIdx.x; i < nch; i += THREADS) {
-    int lo = 0, hi = E - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (choff[mid] <= i) lo = mid;
-      else hi = mid - 1;
-    }
-    const int e = lo, ch = i - choff[e];
-    const int c = start[e + 1] - start[e];
-    const int nt = min(ntu, c - ch * ntu);
-    runs4[4 * i] = e;
-    runs4[4 * i + 1] = nt;
-    runs4[4 * i + 2] = order[start[e] + ch * ntu];
-    runs4[4 * i + 3] = order[start[e] + ch * ntu + (nt > 1 ? 1 : 0)];
-  }
-  if (blockIdx.x == 0 && S.order_out)
-    for (int t = threadIdx.x; t < start[E]; t += THREADS) S.order_out[t] = order[t];
-  __syncthreads();
   table_fill_wait(&tab_bar);
   trace_stamp(1);
   const uint32_t tab_s = smem_base();
@@ -975,9 +1034,9 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     PlanRuns src{runs4, nch, S.mats, 1, S.lg_wo, S.tasks_wo, S.counters, S.tasks_wi};
     pipe_range<PlanRuns, true>(S.wo, src, tb, te, PS, tab_s);
   }
-  trace_stamp(3);
   // ---- 4. last CTA re-arms the counters
   __syncthreads();
+  trace_stamp(3);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(S.counters, 1) == (int)gridDim.x - 1) {
@@ -1211,6 +1270,21 @@ int qmoe_fused_matmat(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_
                       float* d_y, int64_t ldy, int32_t* d_bad, void* stream) {
   if (ldx < cols || ldy < rows) return qmoe::fail(QMOE_EINVAL, "leading dimension too small");
   return fused_common(d, d_cw, d_row_off, d_mm, rows, cols, d_x, x_dtype, ntok, ldx, d_y, ldy, d_bad, stream);
+}
+
+__global__ void empty_kernel(int* sink) {
+  if (sink && threadIdx.x == 0 && blockIdx.x == 0) *sink = 1;
+}
+
+int qmoe_debug_empty_launch(int32_t smem_bytes, int32_t threads, void* stream) {
+  // debug hook: an empty kernel with the fused step's launch shape, to measure
+  // the launch floor of 1 CTA x `threads` x `smem_bytes` per SM
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  CK(cudaFuncSetAttribute(empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes), "attr");
+  empty_kernel<<<nsm, threads, smem_bytes, S(stream)>>>(nullptr);
+  CK(cudaGetLastError(), "empty launch");
+  return QMOE_OK;
 }
 
 int qmoe_debug_step_trace(void* d_buf) {
