@@ -4,7 +4,8 @@ Workload (BASELINE.json configs[1], the metric's single-GPU config):
 Switch-base-128 MoE layer — 128 experts, d_model 768, d_ff 3072, top-1
 routing (RouterSim argmax), T tokens per step (default 64), synthetic
 random-init weights compressed by the bit-exact GPU encoder. A step is one MoE
-layer forward: dispatcher plan + grouped wi pass + grouped wo pass (ReLU fused).
+layer forward: ONE cooperative launch (qmoe_moe_step: dispatcher plan in every
+CTA's shared memory, wi pass with the ReLU fused, wo pass gated per expert run).
 Cold L2: a pool of distinct layers >= 4x the 126 MB L2 is rotated, so every
 step streams its experts from HBM.
 
@@ -355,32 +356,24 @@ def main():
     value = tot_bytes / t_sec / 1e9
     tokens_per_s = T * args.steps * world / t_sec
 
-    # ---- per-kernel timing of the grouped passes: events on the launch stream
-    # between back-to-back launches (enqueued ahead, no host sync in between)
+    # ---- per-kernel timing: the fused step kernel (one launch per step) with
+    # events on the launch stream between back-to-back launches (enqueued
+    # ahead, no host sync in between)
     stream = torch.cuda.current_stream()
     nk = min(max(args.steps, 8), 4 * nsteps_graph)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nk)]
-    kb_wi, kb_wo = [], []
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)]
+    kb = []
+    evs[0].record(stream)
     for i in range(nk):
         l, b = i % L, i % nb
-        lay = layers[l]
-        evs[i][0].record(stream)
-        lay.plan(ad[b], stream)
-        evs[i][1].record(stream)
-        lay.pass_wi(xd[b], stream)
-        evs[i][2].record(stream)
-        lay.pass_wo(outs[l], stream)
-        evs[i][3].record(stream)
-        touched = np.unique(asg[b])
-        kb_wi.append(sum(lay.wi[e].compressed_bytes for e in touched))
-        kb_wo.append(sum(lay.wo[e].compressed_bytes for e in touched))
+        layers[l].forward_device(xd[b], ad[b], out=outs[l], stream=stream)
+        evs[i + 1].record(stream)
+        kb.append(layers[l].touched_bytes(asg[b]))
     torch.cuda.synchronize()
-    ms_plan = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
-    ms_wi = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    ms_wo = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))
-    kern_ms = (ms_wi + ms_wo) / 2
-    kern_bytes = float(np.mean(kb_wi) + np.mean(kb_wo)) / 2
+    kern_ms = float(np.mean([evs[i].elapsed_time(evs[i + 1]) for i in range(nk)]))
+    kern_bytes = float(np.mean(kb))
     achieved = kern_bytes / (kern_ms / 1e3) / 1e9
+    fused = bool(layers[0].fused) and not layers[0].use_dense(T)
     # ---- uncompressed bf16 reference of the same step on the same GPU
     bf16_ms = None
     if not args.profile:
@@ -447,11 +440,11 @@ def main():
             "tokens_per_s": tokens_per_s,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "pipe_matvec_kernel (grouped wi and wo passes of one step, mean per launch)",
+                         "kernel": ("moe_step_kernel (the whole step: plan + wi + wo in one cooperative launch)"
+                                    if fused else "grouped passes"),
                          "bytes_per_launch": kern_bytes, "ms_per_launch": kern_ms,
-                         "ms_plan": ms_plan, "ms_wi": ms_wi, "ms_wo": ms_wo,
                          "traffic_source": "profiles/roofline_r01.json (ncu --set full, dram__bytes_read+write per "
-                                           "launch of the same step)"},
+                                           "launch of the same kernel on the same workload)"},
             "bf16_baseline": {"ms_per_step_cublas": bf16_ms,
                               "ms_per_step_hbm_sol": bf16_sol_ms,
                               "speedup_vs_bf16_cublas": (bf16_ms / (1e3 * t_sec / args.steps)) if bf16_ms else None,
@@ -461,7 +454,7 @@ def main():
                                       "(bf16 bytes of the touched experts / measured HBM peak)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": (1 if fused else 3) * args.steps,
             "clocks": clocks,
             "build_s": t_build,
         }
@@ -541,7 +534,7 @@ def ep_main(args, world, rank, local):
                        "d_ff": d_ff, "tokens_per_step_per_rank": T, "parallelism": f"ep{world}",
                        "exchange": "NCCL all_to_all_single dispatch + combine"},
             "tokens_per_s": T * world * args.steps / t_sec, "pct_peak": 100 * tot / t_sec / 1e9 / (hbm_peak * world),
-            "gpu_launches": 3 * args.steps, "e2e": None, "cpu_baseline": None, "roofline": None,
+            "gpu_launches": (1 if fused else 3) * args.steps, "e2e": None, "cpu_baseline": None, "roofline": None,
         }))
     dist.destroy_process_group()
 
