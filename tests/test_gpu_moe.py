@@ -187,3 +187,74 @@ def test_moe_dense_decode_then_mma_vs_oracle(dic, odic, T):
     finally:
         os.environ.pop("QMOE_DENSE")
     assert bf16_ulp_diff(y, y_stream).max() <= 2
+
+
+def _random_layer(dic, rng, E, d_model, d_ff, max_tokens):
+    wi, wo, host = [], [], []
+    for e in range(E):
+        pair = []
+        for rows, cols, lst in ((d_ff, d_model, wi), (d_model, d_ff, wo)):
+            w = (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+            t = q.rtn_quantize(w, q.make_grid(w))
+            c = q.encode(t, dic)
+            lst.append(c.to_device(dic))
+            pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
+        host.append(tuple(pair))
+    return wi, wo, host
+
+
+@pytest.mark.parametrize("T", [5, 48])
+def test_fused_step_equals_grouped_passes_and_plan(dic, T):
+    """The single-launch step (qmoe_moe_step) runs the same decode with the same
+    lanes as the plan kernel + two grouped passes: outputs must be bit-identical,
+    and its dispatcher outputs (stable per-expert order, counts) exact."""
+    import os
+
+    rng = np.random.default_rng(100 + T)
+    E, d_model, d_ff = 6, 192, 640
+    wi, wo, _ = _random_layer(dic, rng, E, d_model, d_ff, T)
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+    assert layer.fused
+    x = torch.from_numpy(q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))).cuda().to(torch.bfloat16)
+    a_np = rng.integers(-1, E, size=T).astype(np.int32)  # -1: no expert (dropped)
+    a = torch.from_numpy(a_np).cuda()
+    y_fused = layer.forward_device(x, a).clone()
+    ok = a_np >= 0
+    order = np.argsort(np.where(ok, a_np, E), kind="stable")[: ok.sum()]
+    assert np.array_equal(layer.order[: ok.sum()].cpu().numpy(), order)
+    assert np.array_equal(layer.expert_count.cpu().numpy(), np.bincount(a_np[ok], minlength=E))
+    os.environ["QMOE_FUSED"] = "0"
+    try:
+        layer2 = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+        assert not layer2.fused
+        y_grouped = layer2.forward_device(x, a)
+    finally:
+        os.environ.pop("QMOE_FUSED")
+    assert torch.equal(y_fused[ok], y_grouped[ok])
+    # a second step with the same layer reuses the self-resetting counters
+    y_again = layer.forward_device(x, a)
+    assert torch.equal(y_again[ok], y_fused[ok])
+    assert int(layer.counters.abs().sum()) == 0
+
+
+def test_packed_layout_matches_oracle(dic, odic):
+    """Kernel-private PACKED layout (length-sorted, group-aligned rows, per-group
+    columns; QMOE_LAYOUT=packed) against the composed oracle."""
+    import os
+
+    rng = np.random.default_rng(7)
+    E, d_model, d_ff = 3, 256, 768
+    os.environ["QMOE_LAYOUT"] = "packed"
+    try:
+        wi, wo, host = _random_layer(dic, rng, E, d_model, d_ff, 16)
+        layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=16)
+        assert layer.packed and not layer.fused
+        x = q.bf16_round(rng.normal(size=(16, d_model)).astype(np.float32))
+        assign = rng.integers(0, E, size=16).astype(np.int32)
+        y = layer.forward(x, assign)
+    finally:
+        os.environ.pop("QMOE_LAYOUT")
+    y_ref = O.moe_layer(x, assign, host, odic)
+    d = bf16_ulp_diff(y, y_ref)
+    assert d.max() <= 2
+    assert np.mean(d == 0) >= 0.99
