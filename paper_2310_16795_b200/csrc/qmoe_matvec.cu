@@ -1403,7 +1403,12 @@ int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assig
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = getenv("QMOE_NO_COOP") ? 0 : 1;
-  CK(cudaLaunchKernelEx(&cfg, moe_step_kernel, SP), "moe_step_kernel launch");
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, moe_step_kernel, SP);
+  if (le == cudaErrorCooperativeLaunchTooLarge) {  // SMs not all available: caller falls back
+    (void)cudaGetLastError();
+    return qmoe::fail(QMOE_EUNSUPPORTED, "fused step needs every SM co-resident (cooperative launch too large)");
+  }
+  CK(le, "moe_step_kernel launch");
   return QMOE_OK;
 }
 
