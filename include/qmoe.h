@@ -69,7 +69,9 @@ typedef struct qmoe_dict* qmoe_dict_t;
  *      row_minmax uint32[rows]         bf16 (min, max) of sorted row i
  *      ck         uint16[G_total]      column at which group g starts in its row
  *      row_id     uint16[rows]         original row of sorted row i
- *    lg is then only a default: the lanes per row are chosen per run. */
+ *    lg is then only a default: the lanes per row are chosen per run.
+ * colpts (RAW, optional): column points for the decode-then-MMA pass
+ *    (qmoe_colpoints, 256-column chunks). */
 typedef struct qmoe_matrix {
   const uint16_t* cw;
   const int32_t* row_off;
@@ -80,6 +82,7 @@ typedef struct qmoe_matrix {
   int32_t n_cw;
   int32_t lg;
   const uint16_t* row_id;
+  const uint32_t* colpts;
 } qmoe_matrix;
 
 /* One RUN of a grouped launch (self-contained, 80 bytes): rows [row0, row1)
@@ -217,6 +220,16 @@ int qmoe_checkpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* 
                      const int32_t* d_row_off, int64_t rows, int64_t cols, int lg, uint16_t* d_ck,
                      int32_t* d_bad, void* stream);
 
+/* Column points of one RAW matrix (kernel-private, built once): for every
+ * row r and chunk boundary column c = k * 2^chunk_log2 (k = 1 .. nb, nb =
+ * ceil(cols / 2^chunk_log2) - 1), d_cp[r * nb + k - 1] = (index in the row of
+ * the codeword holding column c) << 16 | (the column that codeword starts at).
+ * Lets several lanes decode one column chunk of a row (qmoe_dense_moe_pass
+ * uses 256-column chunks, chunk_log2 = 8). */
+int qmoe_colpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d_cw,
+                   const int32_t* d_row_off, int64_t rows, int64_t cols, int chunk_log2,
+                   uint32_t* d_cp, void* stream);
+
 /* PACKED layout of one RAW matrix (see qmoe_matrix), built once on the device.
  * d_order: int32[rows], the sorted row order (row of sorted row i; e.g. a
  * stable descending sort of the rows' codeword counts); d_gstart:
@@ -300,10 +313,11 @@ int qmoe_moe_step(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_as
  * d_order[start_e .. start_e + d_expert_count[e]) (qmoe_moe_plan's outputs,
  * start_e = exclusive prefix of the counts), y[t][r] (y_mode as
  * qmoe_grouped_matvec) = bf16(sum_k W_e[r][k] x[t][k]) for all rows r of
- * W_e = d_mats[2e + pass] (RAW layout, rows x cols). Each 512-row block of an
- * expert is decoded once into shared memory per block of tokens_per_block
- * (32 or 64) tokens and multiplied on the tensor cores (mma.sync bf16, fp32
- * accumulate). */
+ * W_e = d_mats[2e + pass] (RAW layout, rows x cols, colpts built with
+ * chunk_log2 = 7 when cols > 128). Each 128-row block of an expert is decoded
+ * once per block of tokens_per_block (32 or 64) tokens, 256 columns at a time,
+ * into shared memory and multiplied on the tensor cores (tcgen05.mma, bf16 in,
+ * fp32 accumulate in TMEM). */
 int qmoe_dense_moe_pass(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_matrix* d_mats,
                         int32_t E, int32_t pass, const int32_t* d_expert_count,
                         const int32_t* d_order, int32_t rows, int32_t cols, const void* d_x,

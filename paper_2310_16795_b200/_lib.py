@@ -38,7 +38,7 @@ i32 = ctypes.c_int32
 
 class QmoeMatrix(ctypes.Structure):
     _fields_ = [("cw", vp), ("row_off", vp), ("row_minmax", vp), ("ck", vp), ("rows", i32), ("cols", i32),
-                ("n_cw", i32), ("lg", i32), ("row_id", vp)]
+                ("n_cw", i32), ("lg", i32), ("row_id", vp), ("colpts", vp)]
 
 
 class QmoeWork(ctypes.Structure):
@@ -86,6 +86,7 @@ _SIGS = {
     "qmoe_debug_empty_launch": (ctypes.c_int, [i32, i32, vp]),
     "qmoe_dense_moe_pass": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, i32, i32, vp, ctypes.c_int, i64, vp,
                                            ctypes.c_int, i64, i32, i32, vp]),
+    "qmoe_colpoints": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, ctypes.c_int, vp, vp]),
     "qmoe_pack": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
 

@@ -6,20 +6,17 @@
 // a dense bf16 tile in shared memory and multiplied on the tensor cores with
 // all of the expert's tokens (up to 64 per block).
 //
-//   work item   (expert e, 512-row block, token block of <= BN tokens); the
+//   work item   (expert e, 128-row block, token block of <= BN tokens); the
 //               persistent grid strides over the items; every CTA derives the
 //               item list from the dispatcher's expert counts (qmoe_moe_plan).
-//   decode      thread = row: the lane walks its row's codeword stream chunk
-//               by chunk (64 columns), zero-fills its 128-byte row of the W
-//               tile and stores the <= 3 non-zero bf16 levels of each codeword
-//               (entry table of the streaming kernel, hot prefix in shared
-//               memory). A codeword straddling the chunk end is revisited by
-//               the next chunk. Rows are XOR-swizzled by 16-byte chunk so the
-//               MMA operand loads are bank-conflict free.
-//   mma         warp w owns rows [32w, 32w+32) — exactly the rows its lanes
-//               decoded — x BN tokens: ldmatrix + mma.sync.m16n8k16 bf16 ->
-//               fp32 accumulators in registers; the token tile (bf16, from
-//               x rows of the expert's tokens) is double-buffered per chunk.
+//   decode      per 256-column chunk, 4 lanes per row split the chunk's
+//               codeword range of the row evenly (kernel-private column points),
+//               sum lengths, scan, and store the <= 3 non-zero bf16 levels of
+//               each codeword into a zero-filled tile whose 16-byte chunks are
+//               XOR-swizzled by row: the canonical SW128 K-major UMMA layout.
+//   mma         one thread issues tcgen05.mma (M 128, N BN, K 16) from shared
+//               memory descriptors into a TMEM accumulator, tcgen05.commit on
+//               an mbarrier; the token tile (bf16) is staged per chunk.
 //   epilogue    per (row, token): bf16 RNE once (codec.py:243), y mode as the
 //               streaming kernel (relu -> bf16 hidden, or f32 store / add).
 //
@@ -28,6 +25,7 @@
 // streaming kernel).
 #include <algorithm>
 #include <climits>
+#include <string>
 
 #include "qmoe_device.cuh"
 
@@ -56,6 +54,7 @@ struct DenseParams {
   int y_mode;
   int64_t ldy;
   int w_off, x_off, plan_off;  // byte offsets in dynamic shared memory
+  int cp_log2;                 // column-point granularity the matrices store (qmoe_colpoints)
   int dbg;                     // experiment switches (QMOE_DENSE_DBG): 1 skip mma, 2 skip decode
 };
 
@@ -82,25 +81,35 @@ __device__ __forceinline__ uint16_t x_bf16_bits(const void* x, int bf16, int64_t
   return (uint16_t)(__float_as_uint(__ldg(reinterpret_cast<const float*>(x) + i)) >> 16);  // x is bf16-valued
 }
 
-// ------------------------------------------------------------------ tcgen05 variant
-// Same decode; the MMA runs on the 5th-generation tensor cores: one elected
-// thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128 rows, N = BN
-// tokens, K = 16) from shared-memory descriptors over the SW128 K-major tiles
-// (the decode's XOR swizzle IS the canonical 128-byte swizzle), accumulating
-// in TMEM (4 row blocks x BN fp32 columns); tcgen05.commit signals an
-// mbarrier before the tiles are overwritten. Warp w's TMEM lane quarter holds
-// exactly the 32 rows its lanes decoded, read back with tcgen05.ld.32x32b.
+// ------------------------------------------------------------------ tcgen05 kernel
+// Item = (expert e, 128-row block, <= BN-token block). For every 256-column
+// chunk of the rows:
+//   x tile   the chunk's columns of the item's token rows, bf16, staged as 4
+//            SW128 K-major blocks [BN rows x 128 B] (registers prefetched a
+//            chunk ahead, 16-byte loads);
+//   decode   4 lanes per row split the chunk's codeword range of their row
+//            evenly (column points give its first codeword and start column):
+//            pass 1 sums the entries' lengths, a 4-lane shuffle scan gives each
+//            lane its start column, pass 2 writes the <= 3 non-zero bf16 levels
+//            per codeword into the zero-filled W tile (4 SW128 blocks [128 rows
+//            x 128 B]) — equal work per lane, no divergent column walks;
+//   mma      one thread issues 16 tcgen05.mma (M 128, N BN, K 16) into the
+//            TMEM accumulator and commits to an mbarrier, awaited before the
+//            tiles are rewritten.
+// Epilogue: warps w, w+4, w+8, w+12 share TMEM lane quarter w%4 (rows) and read
+// BN/4 columns (tokens) each with tcgen05.ld.32x32b.
+
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  // start >> 4 [0,14) | LBO (unused for swizzled K-major) = 1 [16,30) |
-  // SBO = 1024 B between 8-row groups [32,46) | version 1 [46,48) | SWIZZLE_128B = 2 [61,64)
+  // start >> 4 [0,14) | LBO 1 (unused, swizzled K-major) [16,30) | SBO 1024 B [32,46) |
+  // version 1 [46,48) | SWIZZLE_128B = 2 [61,64)
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
 template <int BN>
 __device__ __forceinline__ uint32_t idesc_bf16_f32() {
-  // c F32 [4,6) | a BF16 [7,10) | b BF16 [10,13) | K-major A, B | N >> 3 [17,23) | M >> 4 [24,29)
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  // c F32 [4,6) | a BF16 [7,10) | b BF16 [10,13) | K-major A, B | N >> 3 [17,23) | M = 128: 8 [24,29)
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (8u << 24);
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
@@ -112,8 +121,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
                  : "memory");
 }
 
-template <int BN>
+__device__ __forceinline__ uint4 x_chunk8(const void* x, int bf16, int64_t i) {
+  // 8 consecutive x values as bf16 (x is bf16-valued: f32 -> bf16 truncation is exact)
+  if (bf16) return __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + i));
+  const float4 a = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + i));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + i) + 1);
+  auto pk = [](float lo, float hi) { return (__float_as_uint(lo) >> 16) | (__float_as_uint(hi) & 0xFFFF0000u); };
+  return make_uint4(pk(a.x, a.y), pk(a.z, a.w), pk(b.x, b.y), pk(b.z, b.w));
+}
+
+// ROWS rows per item (ROWS / 128 UMMA row blocks, DTHREADS / ROWS lanes per
+// row), KC columns per chunk (KC / 64 SW128 blocks).
+template <int BN, int ROWS, int KC>
 __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
+  constexpr int DT_ROWS = ROWS, DT_KC = KC, DT_LPR = DTHREADS / ROWS, MB = ROWS / 128, KB = KC / 64;
   __shared__ __align__(8) uint64_t tab_bar, mma_bar;
   __shared__ int s_total;
   __shared__ uint32_t s_tmem;
@@ -121,16 +142,19 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t base = sbase();
   const uint32_t tab_s = base;
-  // operand tiles 1024-byte aligned in the shared window (SW128 atoms)
-  const uint32_t w_s = (base + P.w_off + 1023u) & ~1023u, x_s = w_s + (uint32_t)BM * 128u;
+  const uint32_t w_s = (base + P.w_off + 1023u) & ~1023u;   // 4 blocks x 16 KB, 1 KB aligned
+  const uint32_t x_s = w_s + (uint32_t)KB * DT_ROWS * 128u;  // KB blocks x BN x 128 B
   int* start = reinterpret_cast<int*>(dsm + P.plan_off);
   int* ipre = start + P.E + 1;
   const int E = P.E;
-  const int nrb = (P.rows + BM - 1) / BM;
-  constexpr uint32_t TMEM_COLS = 4 * BN;  // 4 row blocks x BN fp32 columns (128 or 256)
+  const int nrb = (P.rows + DT_ROWS - 1) / DT_ROWS;
+  const int nk = (P.cols + DT_KC - 1) / DT_KC;  // chunks
+  const int nb = ((P.cols + (1 << P.cp_log2) - 1) >> P.cp_log2) - 1;  // stored column points per row
+  const int cps = DT_KC >> P.cp_log2;  // stored points per chunk
+  constexpr uint32_t TMEM_COLS = MB * BN < 32 ? 32 : MB * BN;
   const uint32_t tb_mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
   const uint32_t mma_mb = (uint32_t)__cvta_generic_to_shared(&mma_bar);
-  if (warp == 0) {  // TMEM accumulators (warp-wide alloc)
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&s_tmem)),
                  "n"(TMEM_COLS));
@@ -166,10 +190,11 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
   const uint32_t tmem = s_tmem;
   const int total = s_total;
   const uint32_t H = (uint32_t)P.H;
-  const uint32_t rowb = w_s + (uint32_t)tid * 128u;
-  const uint32_t rx = (uint32_t)(tid & 7) << 4;
+  const int rr = tid / DT_LPR, q = tid % DT_LPR;  // my row in the item, my quarter of its chunk
+  const uint32_t rx = (uint32_t)(rr & 7) << 4;    // SW128 chunk swizzle of my row
   const uint32_t idesc = idesc_bf16_f32<BN>();
   uint32_t mma_phase = 0;
+  constexpr int XV = BN * (DT_KC / 8) / DTHREADS;  // 16-byte x pieces per thread per chunk
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     int lo = 0, hi = E - 1;
     while (lo < hi) {
@@ -183,175 +208,192 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
     const int nt = min(BN, cnt - tb * BN);
     const int tok0 = start[e] + tb * BN;
     const qmoe_matrix& M = P.mats[2 * e + P.pass];
-    const int r = rb * BM + tid;
+    const uint16_t* cwp = M.cw;
+    const uint32_t* cpp = M.colpts;
+    const int r = rb * DT_ROWS + rr;
     const bool valid = r < P.rows;
-    int p = 0, pend = 0, col = 0;
+    int s = 0, n = 0;
     uint32_t wlo = 0, whi = 0;
     if (valid) {
-      p = __ldg(M.row_off + r);
-      pend = __ldg(M.row_off + r + 1);
+      s = __ldg(M.row_off + r);
+      n = __ldg(M.row_off + r + 1) - s;
       const uint32_t mm = __ldg(M.row_minmax + r);
       wlo = mm & 0xFFFFu;
       whi = mm >> 16;
     }
     if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
     __syncthreads();
-    constexpr int XPT = BN * BK / DTHREADS;
-    uint16_t xr[XPT];
-    auto load_x_chunk = [&](int k0) {
+    uint4 xr[XV];
+    auto load_x = [&](int k0) {
 #pragma unroll
-      for (int u = 0; u < XPT; ++u) {
-        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
-        xr[u] = (n < nt && k0 + k < P.cols) ? x_bf16_bits(P.x, P.x_bf16, (int64_t)s_tok[n] * P.ldx + k0 + k)
-                                            : (uint16_t)0;
+      for (int u = 0; u < XV; ++u) {
+        const int i = tid + u * DTHREADS, nn = i / (DT_KC / 8), c8 = i % (DT_KC / 8);
+        xr[u] = (nn < nt && k0 + c8 * 8 < P.cols)
+                    ? x_chunk8(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8)
+                    : make_uint4(0u, 0u, 0u, 0u);
       }
     };
-    load_x_chunk(0);
-    // codeword groups: the current group's 8 entries stay looked up across
-    // chunks; the next group is prefetched
-    const uint16_t* cwp = M.cw;
-    const int glast = valid && pend > 0 ? (pend - 1) >> 3 : 0;
-    int gcur = -1;
-    uint4 gn = make_uint4(0u, 0u, 0u, 0u);
-    uint32_t ent[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) ent[u] = 0x007F7F7Fu;
-    if (valid && p < pend)
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
-                   : "l"(cwp + (size_t)(p >> 3) * 8));
-    int chunk = 0;
-    for (int k0 = 0; k0 < P.cols; k0 += BK, ++chunk) {
-      const int k1 = k0 + BK;
-      if (chunk > 0) {  // previous chunk's MMAs must be done reading the W / X tiles
+    load_x(0);
+    for (int k = 0; k < nk; ++k) {
+      const int k0 = k * DT_KC;
+      if (k > 0) {  // the previous chunk's MMAs must be done reading W / X (the last chunk's are awaited below)
         mbar_wait(mma_mb, mma_phase);
         mma_phase ^= 1u;
       }
-      const uint32_t xb = x_s + (uint32_t)(chunk & 1) * (BN * 128u);
+      // ---- x tile
 #pragma unroll
-      for (int u = 0; u < XPT; ++u) {
-        const int i = tid + u * DTHREADS, n = i / BK, k = i % BK;
-        sts_u16(xb + (uint32_t)n * 128u + (((uint32_t)k * 2u) ^ ((uint32_t)(n & 7) << 4)), xr[u]);
+      for (int u = 0; u < XV; ++u) {
+        const int i = tid + u * DTHREADS, nn = i / (DT_KC / 8), c8 = i % (DT_KC / 8);
+        const uint32_t a = x_s + (uint32_t)(c8 >> 3) * (BN * 128u) + (uint32_t)nn * 128u +
+                           ((uint32_t)((c8 & 7) ^ (nn & 7)) << 4);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(xr[u].x), "r"(xr[u].y), "r"(xr[u].z),
+                     "r"(xr[u].w));
       }
-      if (k1 < P.cols) load_x_chunk(k1);
+      if (k + 1 < nk) load_x(k0 + DT_KC);
+      // ---- W tile: zero my 128-byte slice (block q of my row), rotated so the
+      // lanes of a warp hit different banks
 #pragma unroll
-      for (int c16 = 0; c16 < 8; ++c16) sts_zero16(rowb + 16u * (uint32_t)((c16 + lane) & 7));
-      bool go = valid && p < pend && col < k1 && !(P.dbg & 2);
-      while (go) {
-        const int grp = p >> 3;
-        if (grp != gcur) {  // new group: take the prefetched words, look all 8 up, prefetch the next
-          const uint4 g = gn;
-          gcur = grp;
-          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(gn.x), "=r"(gn.y), "=r"(gn.z), "=r"(gn.w)
-                       : "l"(cwp + (size_t)min(grp + 1, glast) * 8));
-          const uint32_t w4[4] = {g.x, g.y, g.z, g.w};
+      for (int b = q; b < KB; b += DT_LPR) {
+        const uint32_t wrow = w_s + (uint32_t)b * (DT_ROWS * 128u) + (uint32_t)rr * 128u;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t c = (u & 1) ? (w4[u >> 1] >> 16) : (w4[u >> 1] & 0xFFFFu);
-            ent[u] = c < H ? lds_u32(tab_s + 4 * c) : __ldg(P.gtab + c);
-          }
+        for (int c16 = 0; c16 < 8; ++c16) sts_zero16(wrow + 16u * (uint32_t)((c16 + lane) & 7));
+      }
+      // ---- my share of the row's codewords for this chunk
+      int ia = 0, ca = 0, ib = n;
+      if (valid) {
+        if (k > 0) {
+          const uint32_t pa = __ldg(cpp + (size_t)r * nb + k * cps - 1);
+          ia = (int)(pa >> 16);
+          ca = (int)(pa & 0xFFFFu);
         }
-        // walk the group's codewords from p: only the column add is in the chain
+        if (k + 1 < nk) ib = min(n, (int)(__ldg(cpp + (size_t)r * nb + (k + 1) * cps - 1) >> 16) + 1);
+      }
+      const int len = max(0, ib - ia);
+      const int p0 = ia + (q * len) / DT_LPR, p1 = ia + ((q + 1) * len) / DT_LPR;
+      // pass 1: lengths, in blocks of 8 independent loads + lookups; the first
+      // block's entries stay in registers for pass 2
+      uint32_t e0[8];
+      int sum = 0;
+      for (int pb = p0; pb < p1; pb += 8) {
+        uint32_t cc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cc[u] = pb + u < p1 ? (uint32_t)__ldg(cwp + s + pb + u) : 0u;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const int q = grp * 8 + u;
-          if (go && q >= p) {
-            if (q >= pend || col >= k1) {
-              go = false;
-            } else {
-              const uint32_t en = ent[u];
-#pragma unroll
-              for (int j = 0; j < 3; ++j) {
-                const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
-                const int vk = col + (int)(f >> 2) - k0;  // column inside the chunk (f = 0x7F: unused slot)
-                if (f != 0x7Fu && (unsigned)vk < (unsigned)BK)
-                  sts_u16(rowb + (((uint32_t)vk * 2u) ^ rx), ((en >> (24 + j)) & 1u) ? whi : wlo);
-              }
-              const int n2 = (int)(en >> 28) * 2;
-              if (col + n2 > k1) {
-                go = false;  // straddles the chunk end: revisit next chunk
-              } else {
-                col += n2;
-                p = q + 1;
-              }
-            }
-          }
+          const uint32_t en = pb + u < p1 ? (cc[u] < H ? lds_u32(tab_s + 4 * cc[u]) : __ldg(P.gtab + cc[u])) : 0u;
+          if (pb == p0) e0[u] = en;
+          sum += (int)(en >> 28) * 2;
         }
-        go = go && p < pend && col < k1;
       }
-      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      int incl = sum;  // 4-lane inclusive scan (the lanes of a row are consecutive)
+#pragma unroll
+      for (int d = 1; d < DT_LPR; d <<= 1) {
+        const int v = __shfl_up_sync(FULL_MASK, incl, d, DT_LPR);
+        if (q >= d) incl += v;
+      }
+      int col = ca + incl - sum - k0;  // chunk-relative start column of my first codeword
+      // pass 2: the non-zero values
+      for (int pb = p0; pb < p1; pb += 8) {
+        uint32_t ee[8];
+        if (pb == p0) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) ee[u] = e0[u];
+        } else {
+          uint32_t cc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cc[u] = pb + u < p1 ? (uint32_t)__ldg(cwp + s + pb + u) : 0u;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            ee[u] = pb + u < p1 ? (cc[u] < H ? lds_u32(tab_s + 4 * cc[u]) : __ldg(P.gtab + cc[u])) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t en = ee[u];  // 0 past the part: no value, length 0
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
+            const int vk = col + (int)(f >> 2);
+            if (en != 0u && f != 0x7Fu && (unsigned)vk < (unsigned)DT_KC)
+              sts_u16(w_s + (uint32_t)(vk >> 6) * (DT_ROWS * 128u) + (uint32_t)rr * 128u +
+                          ((((uint32_t)vk & 63u) * 2u) ^ rx),
+                      ((en >> (24 + j)) & 1u) ? whi : wlo);
+          }
+          col += (int)(en >> 28) * 2;
+        }
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
-      if (tid == 0 && (P.dbg & 1)) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mma_mb) : "memory");
-      } else if (tid == 0) {
+      if (tid == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-        for (int mb = 0; mb < BM / 128; ++mb) {
+        for (int mb = 0; mb < MB; ++mb) {
 #pragma unroll
-          for (int ks = 0; ks < BK / 16; ++ks) {
-            const uint64_t da = sw128_desc(w_s + (uint32_t)mb * 128u * 128u + (uint32_t)ks * 32u);
-            const uint64_t db = sw128_desc(xb + (uint32_t)ks * 32u);
-            const uint32_t acc = (chunk > 0 || ks > 0) ? 1u : 0u;
-            asm volatile(
-                "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
-                    tmem + (uint32_t)mb * BN),
-                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          for (int kb = 0; kb < KB; ++kb) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint64_t da =
+                  sw128_desc(w_s + (uint32_t)kb * (DT_ROWS * 128u) + (uint32_t)mb * (128u * 128u) + (uint32_t)ks * 32u);
+              const uint64_t db = sw128_desc(x_s + (uint32_t)kb * (BN * 128u) + (uint32_t)ks * 32u);
+              const uint32_t accf = (k > 0 || kb > 0 || ks > 0) ? 1u : 0u;
+              asm volatile(
+                  "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+                      tmem + (uint32_t)mb * BN),
+                  "l"(da), "l"(db), "r"(idesc), "r"(accf));
+            }
           }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mma_mb)
                      : "memory");
       }
     }
-    mbar_wait(mma_mb, mma_phase);  // last chunk's MMAs: accumulators final
+    mbar_wait(mma_mb, mma_phase);  // the item's last MMAs: accumulators final
     mma_phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // ---- epilogue: warp w reads TMEM lanes 32(w%4).. = rows 32w.. of the item, columns of block w/4
-    {
-      uint32_t v[BN];
-      const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * BN;
-      if (BN == 64) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,"
-            "%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-              "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32 % BN]), "=r"(v[33 % BN]), "=r"(v[34 % BN]),
-              "=r"(v[35 % BN]), "=r"(v[36 % BN]), "=r"(v[37 % BN]), "=r"(v[38 % BN]), "=r"(v[39 % BN]),
-              "=r"(v[40 % BN]), "=r"(v[41 % BN]), "=r"(v[42 % BN]), "=r"(v[43 % BN]), "=r"(v[44 % BN]),
-              "=r"(v[45 % BN]), "=r"(v[46 % BN]), "=r"(v[47 % BN]), "=r"(v[48 % BN]), "=r"(v[49 % BN]),
-              "=r"(v[50 % BN]), "=r"(v[51 % BN]), "=r"(v[52 % BN]), "=r"(v[53 % BN]), "=r"(v[54 % BN]),
-              "=r"(v[55 % BN]), "=r"(v[56 % BN]), "=r"(v[57 % BN]), "=r"(v[58 % BN]), "=r"(v[59 % BN]),
-              "=r"(v[60 % BN]), "=r"(v[61 % BN]), "=r"(v[62 % BN]), "=r"(v[63 % BN])
-            : "r"(ta));
-      } else {
+    {  // epilogue: warp -> (TMEM lane quarter = 32 rows, row block, column slice of tokens)
+      constexpr int SPL = 4 / MB;  // column slices per (row block, quarter)
+      constexpr int CW = BN / SPL;
+      uint32_t v[CW];
+      const int quarter = warp & 3, mbk = (warp >> 2) % MB, slice = (warp >> 2) / MB;
+      const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)mbk * BN + (uint32_t)slice * CW;
+      if (CW == 32) {
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
             "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              "=r"(v[8 % CW]), "=r"(v[9 % CW]), "=r"(v[10 % CW]), "=r"(v[11 % CW]), "=r"(v[12 % CW]),
+              "=r"(v[13 % CW]), "=r"(v[14 % CW]), "=r"(v[15 % CW]), "=r"(v[16 % CW]), "=r"(v[17 % CW]),
+              "=r"(v[18 % CW]), "=r"(v[19 % CW]), "=r"(v[20 % CW]), "=r"(v[21 % CW]), "=r"(v[22 % CW]),
+              "=r"(v[23 % CW]), "=r"(v[24 % CW]), "=r"(v[25 % CW]), "=r"(v[26 % CW]), "=r"(v[27 % CW]),
+              "=r"(v[28 % CW]), "=r"(v[29 % CW]), "=r"(v[30 % CW]), "=r"(v[31 % CW])
             : "r"(ta));
+      } else if (CW == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8 % CW]), "=r"(v[9 % CW]), "=r"(v[10 % CW]), "=r"(v[11 % CW]), "=r"(v[12 % CW]),
+              "=r"(v[13 % CW]), "=r"(v[14 % CW]), "=r"(v[15 % CW])
+            : "r"(ta));
+      } else {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                       "=r"(v[7])
+                     : "r"(ta));
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (valid) {
+      const int row = rb * DT_ROWS + mbk * 128 + 32 * quarter + lane;
+      if (row < P.rows) {
 #pragma unroll
-        for (int n = 0; n < BN; ++n) {
-          if (n >= nt) break;
-          const int64_t t = s_tok[n];
-          const float vv = bf16_round_dev(__uint_as_float(v[n]));
+        for (int j = 0; j < CW; ++j) {
+          const int nn = slice * CW + j;
+          if (nn >= nt) break;
+          const int64_t t = s_tok[nn];
+          const float vv = bf16_round_dev(__uint_as_float(v[j]));
           if (P.y_mode == QMOE_Y_RELU_BF16) {
-            reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + r] = (uint16_t)(__float_as_uint(fmaxf(vv, 0.f)) >> 16);
+            reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(vv, 0.f)) >> 16);
           } else if (P.y_mode == QMOE_Y_STORE_F32) {
-            reinterpret_cast<float*>(P.y)[t * P.ldy + r] = vv + 0.f;
+            reinterpret_cast<float*>(P.y)[t * P.ldy + row] = vv + 0.f;
           } else {
-            float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + r;
+            float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
             *yp = *yp + vv;
           }
         }
@@ -399,8 +441,12 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.y_mode = y_mode;
   P.ldy = ldy;
   const int BN = tokens_per_block;
+  P.cp_log2 = 7;  // DeviceMatrix.build_colpoints: 128-column points
   P.dbg = getenv("QMOE_DENSE_DBG") ? atoi(getenv("QMOE_DENSE_DBG")) : 0;
-  const size_t wbytes = (size_t)BM * 128 + 1024, xbytes = (size_t)2 * BN * 128;  // + 1 KB: SW128 alignment
+  // item shape: 128 rows x 256-column chunks (default, 4 lanes per row) or 256 x 128 (QMOE_DENSE_SHAPE)
+  const bool tall = getenv("QMOE_DENSE_SHAPE") && std::string(getenv("QMOE_DENSE_SHAPE")) == "256x128";
+  const int R = tall ? 256 : 128, KC = tall ? 128 : 256;  // rows per item x columns per chunk
+  const size_t wbytes = (size_t)R * KC * 2 + 1024, xbytes = (size_t)(KC / 64) * BN * 128;  // + 1 KB: SW128 alignment
   const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
   const size_t static_smem = 1024;
   if (wbytes + xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
@@ -414,13 +460,20 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.plan_off = P.x_off + (int)xbytes;
   const size_t smem = (size_t)P.plan_off + plan;
   const int grid = d->num_sms;
-  if (BN == 64) {
-    CK(cudaFuncSetAttribute(dense_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    dense_tc_kernel<64><<<grid, DTHREADS, smem, S(stream)>>>(P);
+#define QMOE_DENSE_LAUNCH(BNv, Rv, KCv)                                                                      \
+  do {                                                                                                     \
+    CK(cudaFuncSetAttribute(dense_tc_kernel<BNv, Rv, KCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
+       "attr");                                                                                            \
+    dense_tc_kernel<BNv, Rv, KCv><<<grid, DTHREADS, smem, S(stream)>>>(P);                                 \
+  } while (0)
+  if (tall) {
+    if (BN == 64) QMOE_DENSE_LAUNCH(64, 256, 128);
+    else QMOE_DENSE_LAUNCH(32, 256, 128);
   } else {
-    CK(cudaFuncSetAttribute(dense_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    dense_tc_kernel<32><<<grid, DTHREADS, smem, S(stream)>>>(P);
+    if (BN == 64) QMOE_DENSE_LAUNCH(64, 128, 256);
+    else QMOE_DENSE_LAUNCH(32, 128, 256);
   }
+#undef QMOE_DENSE_LAUNCH
   CK(cudaGetLastError(), "dense_moe_kernel launch");
   (void)al16;
   return QMOE_OK;

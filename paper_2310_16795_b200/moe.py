@@ -77,12 +77,8 @@ class CompressedMoELayer:
                 elif m.ck is None and m.lg == 0 and self.max_lg[kind] > 0:
                     # checkpoints for 2^max_lg lanes per row; a run may use any 2^lg <= that
                     m.build_checkpoints(dic, lg=self.max_lg[kind])
-        descs = (_lib.QmoeMatrix * (2 * self.E))()
-        for e in range(self.E):
-            descs[2 * e] = _lib.QmoeMatrix(*wi[e].descriptor())
-            descs[2 * e + 1] = _lib.QmoeMatrix(*wo[e].descriptor())
-        raw = np.frombuffer(bytes(descs), dtype=np.uint8)
-        self.mats = torch.from_numpy(raw.copy()).to(self.device)
+        self._colpts_ready = all(m.colpts is not None for m in list(wi) + list(wo))
+        self._write_descriptors()
         self.tokens_per_unit = min(int(os.environ.get("QMOE_NTU", tokens_per_unit)), _lib.NT_STREAM)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
                                      np.int64)
@@ -109,6 +105,17 @@ class CompressedMoELayer:
         self.h = _lib.padded_empty(max(1, T) * ldh, torch.bfloat16, dev).view(max(1, T), ldh)[:, : self.d_ff]
         self.bad = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
         self.counters = torch.zeros(max(1, T) + 1, dtype=torch.int32, device=dev)  # fused step (self-resetting)
+
+    def _write_descriptors(self) -> None:
+        """Device array of qmoe_matrix descriptors (wi_e = 2e, wo_e = 2e + 1)."""
+        import torch
+
+        descs = (_lib.QmoeMatrix * (2 * self.E))()
+        for e in range(self.E):
+            descs[2 * e] = _lib.QmoeMatrix(*self.wi[e].descriptor())
+            descs[2 * e + 1] = _lib.QmoeMatrix(*self.wo[e].descriptor())
+        raw = np.frombuffer(bytes(descs), dtype=np.uint8)
+        self.mats = torch.from_numpy(raw.copy()).to(self.device)
 
     @staticmethod
     def _aligned_rows(x) -> bool:
@@ -225,19 +232,31 @@ class CompressedMoELayer:
 
     def use_dense(self, T: int) -> bool:
         """Batched regime: each expert block decoded once and multiplied with
-        all its tokens on the tensor cores (qmoe_dense_moe_pass)."""
+        all its tokens on the tensor cores (qmoe_dense_moe_pass). Needs the
+        kernel-private column points, built on first use (not during a CUDA
+        graph capture: a capture before the first batched step keeps the
+        streaming path)."""
+        import torch
+
         if self.packed or not bool(self.dic.device_info(self.device.index)["sparse_path"]):
             return False
         mode = os.environ.get("QMOE_DENSE", "auto")
-        if mode in ("0", "1"):
-            return mode == "1"
-        return T / self._runs_est(T) >= self.DENSE_MIN_TOKENS
+        want = mode == "1" if mode in ("0", "1") else T / self._runs_est(T) >= self.DENSE_MIN_TOKENS
+        if want and not self._colpts_ready:
+            if torch.cuda.is_current_stream_capturing():
+                return False
+            for m in list(self.wi) + list(self.wo):
+                if m.colpts is None:
+                    m.build_colpoints(self.dic)
+            self._write_descriptors()
+            self._colpts_ready = True
+        return want
 
     def pass_dense(self, x, which: int, y, y_mode: int, stream=None) -> None:
         import torch
 
         T = self._T
-        bn = 64 if T / self._runs_est(T) > 24 else 32
+        bn = int(os.environ.get("QMOE_DENSE_BN", 64 if T / self._runs_est(T) > 24 else 32))
         rows, cols = (self.d_ff, self.d_model) if which == 0 else (self.d_model, self.d_ff)
         xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
         _lib.check(_lib.lib.qmoe_dense_moe_pass(

@@ -37,7 +37,7 @@ def test_struct_layouts_match_header():
     import ctypes
 
     assert ctypes.sizeof(_lib.QmoeWork) == 80
-    assert ctypes.sizeof(_lib.QmoeMatrix) == 56
+    assert ctypes.sizeof(_lib.QmoeMatrix) == 64
 
 
 def test_error_mapping():

@@ -28,7 +28,7 @@ Wo = torch.randn((E, d_model, d_ff), device=dev, dtype=torch.bfloat16) * 0.02
 
 
 def timed(fn, n):
-    for i in range(3):
+    for i in range(max(3, n)):  # every pooled layer once before capture (lazy per-layer setup)
         fn(i)
     torch.cuda.synchronize()
     graphs = []
