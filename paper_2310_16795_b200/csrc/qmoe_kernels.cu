@@ -404,19 +404,22 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
                                                         const qmoe_matrix* __restrict__ mats, int ntu, int lg_wi,
                                                         int lg_wo, int max_runs,
                                                         qmoe_work* runs_wi, qmoe_work* runs_wo, int32_t* n_out,
-                                                        int32_t* cnt_out, int32_t* order) {
+                                                        int32_t* cnt_out, int32_t* order, int stage_ids) {
   extern __shared__ int32_t sh[];
   int32_t* cnt = sh;             // E: tokens per expert (then fill cursor)
   int32_t* start = sh + E;       // E: first slot of expert e in order[]
   int32_t* choff = sh + 2 * E;   // E + 1: token chunks before expert e
   int32_t* twi = sh + 3 * E + 1; // E: wi tasks before expert e
   int32_t* two = sh + 4 * E + 1; // E: wo tasks before expert e
+  int32_t* ids = sh + 5 * E + 1;  // T (when staged): the ids, read once from global
   __shared__ int4 wsum[32];
   __shared__ int4 total;
+  const bool staged = stage_ids != 0;
   for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
   __syncthreads();
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     const int e = assign[t];
+    if (staged) ids[t] = e;
     if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);
   }
   __syncthreads();
@@ -456,7 +459,7 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
     const int lane = threadIdx.x;
     for (int t0 = 0; t0 < T; t0 += 32) {
       const int t = t0 + lane;
-      const int e = t < T ? assign[t] : -1;
+      const int e = t < T ? (staged ? ids[t] : assign[t]) : -1;
       const bool ok = t < T && e >= 0 && e < E;
       const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
       const int rank = __popc(peers & ((1u << lane) - 1u));
@@ -764,12 +767,14 @@ int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matr
                   int32_t* d_expert_count, int32_t* d_order, void* stream) {
   if (T < 0 || E < 1 || !d_mats || max_runs < T || ntu < 1 || ntu > QMOE_NT_MAX || !d_n || lg_wi > 5 || lg_wo > 5)
     return qmoe::fail(QMOE_EINVAL, "bad argument (max_runs must be >= T)");
-  const size_t smem = (size_t)(5 * E + 1) * 4;
+  size_t smem = (size_t)(5 * E + 1) * 4;
   if (smem > 200 * 1024) return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts");
+  const int stage = smem + (size_t)T * 4 <= 200 * 1024 ? 1 : 0;  // ids in shared memory for the ordered walk
+  if (stage) smem += (size_t)T * 4;
   CK(cudaFuncSetAttribute(moe_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
   moe_plan_kernel<<<1, 1024, smem, S(stream)>>>(d_assign, T, E, d_mats, ntu, lg_wi, lg_wo, max_runs, d_runs_wi,
                                                  d_runs_wo, d_n,
-                                                 d_expert_count, d_order);
+                                                 d_expert_count, d_order, stage);
   CK(cudaGetLastError(), "moe_plan_kernel");
   return QMOE_OK;
 }
