@@ -242,6 +242,59 @@ def bf16_baseline(E, d_model, d_ff, xs_dev, asg, steps, warmup, dev):
     return ms
 
 
+def matvec_at_scale(dic, dev, hbm_peak, rows=768, cols=3072, lg=2, iters=20):
+    """Streaming decode + matvec throughput at scale: ONE grouped launch over
+    E distinct compressed matrices (a pool > 4x L2, so weights come from HBM),
+    one token; codewords/s, weights/s and compressed GB/s (stats bytes)."""
+    import torch
+
+    import paper_2310_16795_b200 as q
+    from paper_2310_16795_b200 import _lib
+    from paper_2310_16795_b200.codebook import Codebook
+    from paper_2310_16795_b200.synth import _stacked
+
+    per = 2 * rows * cols // 24 + 8 * rows
+    E = int(4.5 * L2_BYTES / per)
+    mats = _stacked(E, rows, cols, seed=4242, dic=dic, device=dev)
+    cb = Codebook(dic, mats)
+    cb.apply(mats)
+    recs = (_lib.QmoeWork * E)()
+    t = 0
+    for i, m in enumerate(mats):
+        m.build_checkpoints(dic, lg)
+        d = m.descriptor()
+        recs[i] = _lib.QmoeWork(d[0], d[1], d[2], d[3], cols, 0, rows, lg | (lg << 8), 1, t, 0, (0, 0, 0, 0))
+        t += ((rows << lg) + 31) >> 5
+    raw = torch.from_numpy(np.frombuffer(bytes(recs), dtype=np.uint8).copy()).to(dev)
+    n = torch.tensor([E, t], dtype=torch.int32, device=dev)
+    x = torch.randn(1, cols, device=dev).to(torch.bfloat16)
+    y = torch.zeros(1, rows, device=dev)
+    h = dic.device_handle(dev.index)
+
+    def launch():
+        _lib.check(_lib.lib.qmoe_grouped_matvec(h, _lib.ptr(cb.table), _lib.ptr(raw), _lib.ptr(n), E, cols, 1,
+                                                 _lib.ptr(x), _lib.QMOE_X_BF16, x.stride(0), _lib.ptr(y),
+                                                 _lib.QMOE_Y_STORE_F32, y.stride(0), 0, 0, _lib.stream_ptr()))
+    launch()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        launch()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    nbytes = sum(m.compressed_bytes for m in mats)
+    ncw = sum(m.n_codewords for m in mats)
+    out = {"kernel": "pipe_matvec_kernel (one grouped launch)", "shape": f"{rows}x{cols}", "matrices": E,
+           "ms_per_launch": ms, "codewords_per_s": ncw / ms * 1e3, "weights_per_s": E * rows * cols / ms * 1e3,
+           "GBps": nbytes / ms / 1e6, "frac_of_hbm": nbytes / ms / 1e6 / hbm_peak,
+           "bf16_sol_weights_per_s": hbm_peak * 1e9 / 2}
+    del mats, cb, raw
+    torch.cuda.empty_cache()
+    return out
+
+
 def profiled_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu
     capture (profiles/roofline_r01.json), or None."""
@@ -433,6 +486,13 @@ def main():
                "sample": f"{sample_steps} steps x {sample_T} tokens of layer 0 through the composed CPU oracle "
                          f"(numpy restatement of moepack.codec.fused_matvec, workers={cores})"}
 
+    # ---- the decode + matvec kernel at scale (first half of the metric): one
+    # grouped launch over a pool (> 4x L2) of distinct 768x3072 matrices
+    # (Switch-base wo shape, 4 lanes per row), 1 token, cold
+    at_scale = None
+    if not args.profile:
+        at_scale = matvec_at_scale(dic, dev, hbm_peak)
+
     traffic, _ = profiled_traffic()
     if rank == 0:
         clocks = cs.summary() if cs else None
@@ -461,6 +521,7 @@ def main():
                               "what": "same routed MoE step with uncompressed bf16 weights: measured with cuBLAS "
                                       "GEMMs per touched expert in a CUDA graph, and its HBM speed-of-light "
                                       "(bf16 bytes of the touched experts / measured HBM peak)"},
+            "kernel_at_scale": at_scale,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": (1 if fused else 3) * args.steps,
