@@ -526,10 +526,34 @@ __device__ __forceinline__ void lookup_any(uint32_t (&e)[GRP], const uint4 q, ui
 
 // Run sources of pipe_range: the device run list of a grouped launch, or the
 // per-CTA shared-memory plan of the fused MoE step.
+// What the (serial) window builder needs of a run; the pointers are filled
+// afterwards, one thread per run of the window, so their loads overlap.
+struct RunMeta {
+  int task0, task1, ntok, cols;
+};
+
+__device__ __forceinline__ void fill_win(WinRun& W, const Run& R) {
+  W.cw = R.cw;
+  W.ro = R.ro;
+  W.mm = R.mm;
+  W.ck = R.ck;
+  W.row0 = R.row0;
+  W.row1 = R.row1;
+  W.lg = R.lg;
+  W.cklg = R.cklg;
+  W.tok[0] = R.tok[0];
+  W.tok[1] = R.tok[1];
+}
+
 struct ListRuns {
   const SegParams* P;
   int n;
   __device__ __forceinline__ Run get(int r) const { return get_run(*P, r); }
+  __device__ __forceinline__ RunMeta meta(int r) const {
+    const Run R = get_run(*P, r);
+    return RunMeta{R.task0, R.task0 + run_tasks(R.row1 - R.row0, R.lg), R.ntok, R.cols};
+  }
+  __device__ __forceinline__ void fill(WinRun& W, int r) const { fill_win(W, get_run(*P, r)); }
   __device__ __forceinline__ void wait(int) const {}
 };
 
@@ -575,7 +599,7 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     int lo = 0, hi = src.n - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (src.get(mid).task0 <= t_begin) lo = mid;
+      if (src.meta(mid).task0 <= t_begin) lo = mid;
       else hi = mid - 1;
     }
     S.run = lo;
@@ -587,17 +611,18 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     if (threadIdx.x == 0) {  // next window: consecutive runs whose x slots fit the budget
       int ri = S.run, nw = 0, xo = 0, wend = t;
       while (ri < src.n && nw < WIN_RUNS && wend < t_end) {
-        const Run R = src.get(ri);
-        const int r_end = R.task0 + run_tasks(R.row1 - R.row0, R.lg);
+        const RunMeta R = src.meta(ri);
+        const int r_end = R.task1;
         const int need = ((R.ntok > 1 ? 8 : 4) * (R.cols + 32) + 15) & ~15;
         if (nw > 0 && xo + need > P.xbytes) break;
         if (r_end > t) {
           WinRun& W = win[nw++];
           W.ri = ri;
-          W.cw = R.cw; W.ro = R.ro; W.mm = R.mm; W.ck = R.ck;
-          W.cols = R.cols; W.row0 = R.row0; W.row1 = R.row1; W.lg = R.lg; W.cklg = R.cklg; W.ntok = R.ntok;
-          W.task0 = R.task0; W.task1 = r_end; W.xoff = xo;
-          W.tok[0] = R.tok[0]; W.tok[1] = R.tok[1];
+          W.cols = R.cols;
+          W.ntok = R.ntok;
+          W.task0 = R.task0;
+          W.task1 = r_end;
+          W.xoff = xo;
           xo += need;
           wend = min(t_end, r_end);
         }
@@ -611,6 +636,8 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     }
     __syncthreads();
     const int nw = S.nwin, wend = S.wend;
+    if ((int)threadIdx.x < nw) src.fill(win[threadIdx.x], win[threadIdx.x].ri);  // pointers, in parallel
+    __syncthreads();
     auto stage_x = [&]() {
       for (int w = 0; w < nw; ++w) {  // stage x (fp32; two tokens interleaved)
         const WinRun& W = win[w];
@@ -786,6 +813,7 @@ struct PlanRuns {
   int pass, lg, tasks_per_run;
   const int* counters;  // wo: counters[1 + r] reaches `need` when run r's wi tasks are done
   int need;
+  int cols;  // columns of every matrix of this pass
   __device__ __forceinline__ Run get(int r) const {
     const int e = runs4[4 * r];
     const qmoe_matrix& M = mats[2 * e + pass];
@@ -806,6 +834,10 @@ struct PlanRuns {
     R.tok[1] = runs4[4 * r + 3];
     return R;
   }
+  __device__ __forceinline__ RunMeta meta(int r) const {
+    return RunMeta{r * tasks_per_run, (r + 1) * tasks_per_run, runs4[4 * r + 1], cols};
+  }
+  __device__ __forceinline__ void fill(WinRun& W, int r) const { fill_win(W, get(r)); }
   __device__ __forceinline__ void wait(int r) const {
     if (!counters) return;
     for (;;) {
@@ -833,6 +865,7 @@ struct StepParams {
   int T, E, ntu;
   const qmoe_matrix* mats;
   int lg_wi, lg_wo, tasks_wi, tasks_wo;
+  int d_model, d_ff;
   int32_t* counters;  // int32[T + 1], zero at launch: [0] = CTAs done, [1 + r] = wi tasks done of run r
   int32_t* order_out;
   int32_t* count_out;
@@ -1055,7 +1088,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   // ---- 2. wi phase
   {
     const int tb = s_split[0], te = s_split[1];
-    PlanRuns src{runs4, nch, S.mats, 0, S.lg_wi, S.tasks_wi, nullptr, 0};
+    PlanRuns src{runs4, nch, S.mats, 0, S.lg_wi, S.tasks_wi, nullptr, 0, S.d_model};
     pipe_range<PlanRuns, false>(S.wi, src, tb, te, PS, tab_s);
     __threadfence();  // this thread's h stores before the CTA's release below
     __syncthreads();
@@ -1070,7 +1103,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   // ---- 3. wo phase
   {
     const int tb = s_split[2], te = s_split[3];
-    PlanRuns src{runs4, nch, S.mats, 1, S.lg_wo, S.tasks_wo, S.counters, S.tasks_wi};
+    PlanRuns src{runs4, nch, S.mats, 1, S.lg_wo, S.tasks_wo, S.counters, S.tasks_wi, S.d_ff};
     pipe_range<PlanRuns, true>(S.wo, src, tb, te, PS, tab_s);
   }
   // ---- 4. last CTA re-arms the counters
@@ -1374,6 +1407,8 @@ int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assig
   SP.lg_wo = lg_wo;
   SP.tasks_wi = ((d_ff << lg_wi) + 31) >> 5;
   SP.tasks_wo = ((d_model << lg_wo) + 31) >> 5;
+  SP.d_model = d_model;
+  SP.d_ff = d_ff;
   SP.counters = d_counters;
   SP.order_out = d_order;
   SP.count_out = d_expert_count;
