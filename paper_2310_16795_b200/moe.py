@@ -68,7 +68,9 @@ class CompressedMoELayer:
         # mean 8-codeword groups per row (wi, wo): lane-segment sizing
         self.mean_groups = tuple(float(np.mean([m.n_codewords / max(1, m.rows) / 8 for m in ms])) for ms in (wi, wo))
         # most lanes per row a step may use: segments of >= ~2 groups
-        self.max_lg = tuple(max(0, min(self.MAX_LG, int(np.floor(np.log2(max(1.0, mg / 2)))))) for mg in self.mean_groups)
+        boost = int(os.environ.get("QMOE_LG_BOOST", 0))  # experiment: finer checkpoints
+        self.max_lg = tuple(max(0, min(self.MAX_LG, int(np.floor(np.log2(max(1.0, mg / 2)))) + boost))
+                            for mg in self.mean_groups)
         for kind, ms in enumerate((wi, wo)):  # kernel-private PACKED layout (or row checkpoints)
             for m in ms:
                 if self.packed:
@@ -142,7 +144,8 @@ class CompressedMoELayer:
             for kind, (rows, mg) in enumerate(((self.d_ff, self.mean_groups[0]), (self.d_model, self.mean_groups[1]))):
                 cap = 5 if self.packed else max(m.lg for m in (self.wi if kind == 0 else self.wo))
                 lg = 0
-                while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES and mg / (1 << (lg + 1)) >= 2.0:
+                min_groups = float(os.environ.get("QMOE_MIN_SEG_GROUPS", 2.0))  # experiment
+                while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES and mg / (1 << (lg + 1)) >= min_groups:
                     lg += 1
                 out.append(lg)
             for kind, key in enumerate(("QMOE_LG_WI", "QMOE_LG_WO")):  # experiment overrides
