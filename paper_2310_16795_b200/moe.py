@@ -281,13 +281,64 @@ class CompressedMoELayer:
             _lib.ptr(out), out.stride(0), _lib.ptr(self.counters), _lib.ptr(self.order), _lib.ptr(self.expert_count),
             max(self.hot_entries(T, True), self.hot_entries(T, False)), _lib.stream_ptr(stream)))
 
+    GRAPH_CACHE = 8  # token counts with a captured host-API graph per layer
+
     def forward(self, x: np.ndarray, assign: np.ndarray) -> np.ndarray:
-        """Host API: numpy tokens + expert ids in, numpy outputs back."""
+        """Host API: numpy tokens + expert ids in, numpy outputs back.
+
+        Per token count T the layer keeps pinned host staging buffers, device
+        buffers and (after the first call) a CUDA graph holding the H2D copies,
+        the step and the D2H copy, so a call is: copy into pinned memory,
+        one graph launch, one stream sync, copy out."""
         import torch
 
-        xd = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(self.device)
-        ad = torch.from_numpy(np.ascontiguousarray(assign, np.int32)).to(self.device)
-        return self.forward_device(xd, ad).cpu().numpy()
+        x = np.ascontiguousarray(x, np.float32)
+        a = np.ascontiguousarray(assign, np.int32)
+        T = int(x.shape[0])
+        if x.ndim != 2 or x.shape[1] != self.d_model or a.shape != (T,):
+            raise ValueError(f"expected x (T, {self.d_model}) and assign (T,)")
+        st = self._stages.get(T) if hasattr(self, "_stages") else None
+        if st is None:
+            if not hasattr(self, "_stages"):
+                self._stages = {}
+            if len(self._stages) >= self.GRAPH_CACHE:
+                self._stages.pop(next(iter(self._stages)))
+            st = {
+                "x_h": torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True),
+                "a_h": torch.empty((T,), dtype=torch.int32, pin_memory=True),
+                "y_h": torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True),
+                "x_d": torch.empty((T, self.d_model), dtype=torch.float32, device=self.device),
+                "a_d": torch.empty((T,), dtype=torch.int32, device=self.device),
+                "y_d": torch.empty((T, self.d_model), dtype=torch.float32, device=self.device),
+                "graph": None,
+            }
+            self._stages[T] = st
+        st["x_h"].numpy()[...] = x
+        st["a_h"].numpy()[...] = a
+        stream = torch.cuda.current_stream(self.device)
+
+        def body():
+            st["x_d"].copy_(st["x_h"], non_blocking=True)
+            st["a_d"].copy_(st["a_h"], non_blocking=True)
+            self.forward_device(st["x_d"], st["a_d"], out=st["y_d"])
+            st["y_h"].copy_(st["y_d"], non_blocking=True)
+
+        if st["graph"] is not None:
+            st["graph"].replay()
+        else:
+            body()  # first call for this T runs eagerly (lazy setup), then the graph is captured
+            stream.synchronize()
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    body()
+                st["graph"] = g
+                g.replay()
+            except RuntimeError:  # capture not possible here: stay eager
+                st["graph"] = None
+                body()
+        stream.synchronize()
+        return st["y_h"].numpy().copy()
 
     def touched_bytes(self, assign: np.ndarray) -> int:
         """Compressed bytes one step must stream: each distinct expert once."""
