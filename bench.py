@@ -460,7 +460,8 @@ def main():
         e_sec = time.perf_counter() - t0
         e2e = {"value": e_bytes / e_sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(xs[0].nbytes + asg[0].nbytes),
                "d2h_bytes_per_step": int(T * d_model * 4), "tokens_per_s": T * args.steps / e_sec,
-               "api": "CompressedMoELayer.forward(numpy x f32, numpy expert ids) -> numpy y"}
+               "api": "CompressedMoELayer.forward(numpy x f32, numpy expert ids) -> numpy y",
+               "path": "one pinned H2D copy of x + ids, fused step (one launch) writing y rows into pinned host memory, stream sync, copy out"}
 
     # ---- CPU baseline (oracle port on this host), rank 0 at N=1 only
     cpu = None

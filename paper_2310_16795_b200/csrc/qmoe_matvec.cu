@@ -118,11 +118,20 @@ __device__ __forceinline__ Run get_run(const SegParams& P, int r) {
   return R;
 }
 
+// Codeword stream: read once per step, so it is marked L2 evict-first — the
+// stream must not push the dictionary table, run metadata, activations and
+// the kernel's own code out of L2 (a cold code/table fetch from HBM costs
+// each launch microseconds of serial latency).
+__device__ __forceinline__ uint64_t stream_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint4 ld_group(const uint16_t* cw, int g) {
   uint4 a;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
-               : "l"(cw + (size_t)g * GRP));
+               : "l"(cw + (size_t)g * GRP), "l"(stream_policy()));
   return a;
 }
 
@@ -582,13 +591,37 @@ __device__ __forceinline__ int claim_task(int* next) {
   return __shfl_sync(FULL_MASK, k, 0);
 }
 
+__device__ unsigned long long* g_step_trace = nullptr;  // qmoe_debug_step_trace: per-CTA phase stamps
+
+__device__ __forceinline__ void trace_stamp(int k) {
+  // slot 0: %globaltimer at the CTA's start (aligns CTAs); slots 1-7: SM
+  // clock cycles since then (globaltimer is too coarse for sub-µs phases)
+  __shared__ long long s_clk0;
+  if (g_step_trace && threadIdx.x == 0) {
+    const long long c = clock64();
+    if (k == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      s_clk0 = c;
+      g_step_trace[blockIdx.x * 8] = t;
+    } else {
+      g_step_trace[blockIdx.x * 8 + k] = (unsigned long long)(c - s_clk0);
+    }
+  }
+}
+
 // Walk global tasks [t_begin, t_end) of the runs `src` provides (task0
 // ascending): windows of runs whose x slots fit P.xbytes are staged at once,
 // then every warp walks its tasks with the cross-task pipeline.
 template <class Src, bool COHERENT_X>
 __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, int t_begin, int t_end, PipeShared& S,
-                                           uint32_t tab_s) {
-  if (t_begin >= t_end || src.n <= 0) return;
+                                           uint32_t tab_s, uint64_t* tab_bar = nullptr) {
+  // tab_bar: hot-table fill still in flight — waited on after the first
+  // window's metadata and codeword loads are issued (they need no table)
+  if (t_begin >= t_end || src.n <= 0) {
+    if (tab_bar) table_fill_wait(tab_bar);
+    return;
+  }
   const uint32_t xs_s = tab_s + (uint32_t)P.H * 4;
   char* xs = reinterpret_cast<char*>(seg_smem + (size_t)P.H * 4);
   const int warp = threadIdx.x >> 5;
@@ -668,7 +701,7 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     bool has_n = false, nready = false;
     Lane c{0, 0, 0, -1, 0u}, n{0, 0, 0, -1, 0u};
     uint32_t ea[GRP], eb[GRP];
-    uint4 q1 = make_uint4(0u, 0u, 0u, 0u);
+    uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = make_uint4(0u, 0u, 0u, 0u);
     if (active) {  // first tasks' metadata, groups and entries: needs no x
       while (win[wc].task1 <= k) ++wc;
       c = lane_task(win[wc], k);
@@ -680,17 +713,22 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
         n = lane_task(win[wn], kn);
       }
       maxgc = __reduce_max_sync(FULL_MASK, lane_groups(c));
-      const uint4 q0 = lane_load(win[wc].cw, c, 0);
+      q0 = lane_load(win[wc].cw, c, 0);
       if (maxgc >= 2) q1 = lane_load(win[wc].cw, c, 1);
       else q1 = has_n ? lane_load(win[wn].cw, n, 0) : make_uint4(0u, 0u, 0u, 0u);
-      lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
     }
+    if (tab_bar) {
+      table_fill_wait(tab_bar);
+      tab_bar = nullptr;
+    }
+    if (active) lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
     // x staging after the first loads are in flight (fused wo phase: the x
     // rows are other CTAs' h — wait for their runs first)
     if (COHERENT_X) {
       if (threadIdx.x == 0)
         for (int w = 0; w < nw; ++w) src.wait(win[w].ri);
       __syncthreads();
+      trace_stamp(6);  // (last) window's producer runs done
     }
     stage_x();
     __syncthreads();
@@ -849,16 +887,6 @@ struct PlanRuns {
   }
 };
 
-__device__ unsigned long long* g_step_trace = nullptr;  // qmoe_debug_step_trace: per-CTA phase stamps
-
-__device__ __forceinline__ void trace_stamp(int k) {
-  if (g_step_trace && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_step_trace[blockIdx.x * 8 + k] = t;
-  }
-}
-
 struct StepParams {
   SegParams wi, wo;  // per-phase x / y / modes; table fields from wi
   const int32_t* assign;
@@ -870,6 +898,7 @@ struct StepParams {
   int32_t* order_out;
   int32_t* count_out;
   int plan_off;       // byte offset of the plan area in dynamic shared memory
+  int w2;             // split weight of a 2-token run (a 1-token run weighs 8)
 };
 
 __device__ __forceinline__ int block_excl_scan2(int v, int w, int& wtot, int2* wsum, int* tot) {
@@ -993,6 +1022,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       }
     }
     __syncthreads();
+    trace_stamp(5);
     if (blockIdx.x == 0 && S.count_out)
       for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = cnt[e];
     __syncthreads();
@@ -1039,6 +1069,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
 
   }
   __syncthreads();
+  trace_stamp(7);
   const int nch = choff[E];
   // cost-weighted split of the run list over the CTAs: a 2-token run decodes
   // once but gathers and accumulates twice (~1.4x a 1-token run, measured)
@@ -1048,7 +1079,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     int carry = 0;
     for (int r0 = 0; r0 < nch; r0 += 32) {
       const int r = r0 + lane;
-      const int w = r < nch ? (runs4[4 * r + 1] > 1 ? 11 : 8) : 0;
+      const int w = r < nch ? (runs4[4 * r + 1] > 1 ? S.w2 : 8) : 0;
       int inc = w;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -1082,14 +1113,13 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     }
   }
   __syncthreads();
-  table_fill_wait(&tab_bar);
   trace_stamp(1);
   const uint32_t tab_s = smem_base();
   // ---- 2. wi phase
   {
     const int tb = s_split[0], te = s_split[1];
     PlanRuns src{runs4, nch, S.mats, 0, S.lg_wi, S.tasks_wi, nullptr, 0, S.d_model};
-    pipe_range<PlanRuns, false>(S.wi, src, tb, te, PS, tab_s);
+    pipe_range<PlanRuns, false>(S.wi, src, tb, te, PS, tab_s, &tab_bar);
     __threadfence();  // this thread's h stores before the CTA's release below
     __syncthreads();
     if (threadIdx.x == 0 && tb < te) {
@@ -1345,6 +1375,8 @@ int qmoe_fused_matmat(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_row_
 }
 
 __global__ void empty_kernel(int* sink) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (sink && threadIdx.x == 0 && blockIdx.x == 0) *sink = 1;
 }
 
@@ -1353,15 +1385,36 @@ int qmoe_debug_empty_launch(int32_t smem_bytes, int32_t threads, void* stream) {
   // the launch floor of 1 CTA x `threads` x `smem_bytes` per SM
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  // threads bits 16+: launch mode (1 = cooperative, 2 = programmatic
+  // dependent launch, 3 = both)
+  const int mode = threads >> 16;
+  threads &= 0xFFFF;
   CK(cudaFuncSetAttribute(empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes), "attr");
-  empty_kernel<<<nsm, threads, smem_bytes, S(stream)>>>(nullptr);
-  CK(cudaGetLastError(), "empty launch");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nsm);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = S(stream);
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (mode & 1) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  }
+  if (mode & 2) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  CK(cudaLaunchKernelEx(&cfg, empty_kernel, (int*)nullptr), "empty launch");
   return QMOE_OK;
 }
 
 int qmoe_debug_step_trace(void* d_buf) {
-  // debug hook: per-CTA %globaltimer stamps of the fused step (8 u64 per CTA:
-  // start, plan done, wi done, wo done); NULL disables
+  // debug hook: per-CTA phase stamps of the fused step (8 u64 per CTA: [0]
+  // %globaltimer at start, [1..7] SM cycles since start: plan done, wi done,
+  // wo done, then plan sub-steps); NULL disables
   CK(cudaMemcpyToSymbol(g_step_trace, &d_buf, sizeof(void*)), "trace symbol");
   return QMOE_OK;
 }
@@ -1412,6 +1465,7 @@ int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assig
   SP.counters = d_counters;
   SP.order_out = d_order;
   SP.count_out = d_expert_count;
+  SP.w2 = getenv("QMOE_W2") ? atoi(getenv("QMOE_W2")) : 11;  // experiment override
   const int maxc = std::max(d_model, d_ff);
   const size_t slot = (size_t)2 * 4 * (((maxc + 32) + 3) & ~3);
   const size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));

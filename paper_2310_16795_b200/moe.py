@@ -297,48 +297,64 @@ class CompressedMoELayer:
         T = int(x.shape[0])
         if x.ndim != 2 or x.shape[1] != self.d_model or a.shape != (T,):
             raise ValueError(f"expected x (T, {self.d_model}) and assign (T,)")
-        st = self._stages.get(T) if hasattr(self, "_stages") else None
+        key = (T, self.use_dense(T))  # the captured graph holds one path
+        st = self._stages.get(key) if hasattr(self, "_stages") else None
         if st is None:
-            if not hasattr(self, "_stages"):
-                self._stages = {}
-            if len(self._stages) >= self.GRAPH_CACHE:
-                self._stages.pop(next(iter(self._stages)))
-            st = {
-                "x_h": torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True),
-                "a_h": torch.empty((T,), dtype=torch.int32, pin_memory=True),
-                "y_h": torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True),
-                "x_d": torch.empty((T, self.d_model), dtype=torch.float32, device=self.device),
-                "a_d": torch.empty((T,), dtype=torch.int32, device=self.device),
-                "y_d": torch.empty((T, self.d_model), dtype=torch.float32, device=self.device),
-                "graph": None,
-            }
-            self._stages[T] = st
-        st["x_h"].numpy()[...] = x
-        st["a_h"].numpy()[...] = a
-        stream = torch.cuda.current_stream(self.device)
-
-        def body():
-            st["x_d"].copy_(st["x_h"], non_blocking=True)
-            st["a_d"].copy_(st["a_h"], non_blocking=True)
-            self.forward_device(st["x_d"], st["a_d"], out=st["y_d"])
-            st["y_h"].copy_(st["y_d"], non_blocking=True)
-
+            st = self._host_stage(T, key)
+        np.copyto(st["xv"], x)
+        np.copyto(st["av"], a)
         if st["graph"] is not None:
             st["graph"].replay()
         else:
-            body()  # first call for this T runs eagerly (lazy setup), then the graph is captured
+            stream = torch.cuda.current_stream(self.device)
+            st["body"]()  # first call for this T runs eagerly (lazy setup), then the graph is captured
             stream.synchronize()
             try:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    body()
+                    st["body"]()
                 st["graph"] = g
                 g.replay()
             except RuntimeError:  # capture not possible here: stay eager
                 st["graph"] = None
-                body()
-        stream.synchronize()
-        return st["y_h"].numpy().copy()
+                st["body"]()
+        st["done"].record()
+        st["done"].synchronize()
+        return st["yv"].copy()
+
+    def _host_stage(self, T: int, key) -> dict:
+        """Pinned staging for T tokens: ONE input buffer (x f32 rows, then the
+        int32 expert ids) so the step's inputs cross the link in one copy; the
+        step writes its output rows straight into pinned host memory (mapped,
+        UVA), which saves the D2H copy node and its dependency latency
+        (measured: tools/e2e_breakdown.py)."""
+        import torch
+
+        if not hasattr(self, "_stages"):
+            self._stages = {}
+        if len(self._stages) >= self.GRAPH_CACHE:
+            self._stages.pop(next(iter(self._stages)))
+        xb = T * self.d_model * 4
+        nb = xb + ((T * 4 + 15) & ~15)
+        in_h = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        in_d = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        y_h = torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True)
+        x_d = in_d[:xb].view(torch.float32).view(T, self.d_model)
+        a_d = in_d[xb:xb + T * 4].view(torch.int32)
+
+        def body():
+            in_d.copy_(in_h, non_blocking=True)
+            self.forward_device(x_d, a_d, out=y_h)
+
+        st = {
+            "in_h": in_h, "in_d": in_d, "y_h": y_h, "body": body, "graph": None,
+            "xv": in_h[:xb].numpy().view(np.float32).reshape(T, self.d_model),
+            "av": in_h[xb:xb + T * 4].numpy().view(np.int32),
+            "yv": y_h.numpy(),
+            "done": torch.cuda.Event(),
+        }
+        self._stages[key] = st
+        return st
 
     def touched_bytes(self, assign: np.ndarray) -> int:
         """Compressed bytes one step must stream: each distinct expert once."""

@@ -72,6 +72,35 @@ def test_moe_random_layer_vs_oracle(dic, odic, T):
     assert np.array_equal(order, want)
 
 
+def test_host_forward_graph_replays_fresh_inputs(dic, odic):
+    """forward() captures a per-T graph (H2D copy, step, y into pinned host
+    memory) on first use; later calls replay it. Every call must see its own
+    tokens and ids, and the returned array must not alias the next call's."""
+    rng = np.random.default_rng(5)
+    E, d_model, d_ff, T = 6, 128, 384, 24
+    wi, wo, host = [], [], []
+    for e in range(E):
+        pair = []
+        for rows, cols, lst in ((d_ff, d_model, wi), (d_model, d_ff, wo)):
+            w = (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+            c = q.encode(q.rtn_quantize(w, q.make_grid(w)), dic)
+            lst.append(c.to_device(dic))
+            pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
+        host.append(tuple(pair))
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+    outs = []
+    for call in range(4):
+        x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
+        assign = rng.integers(0, E, size=T).astype(np.int32)
+        y = layer.forward(x, assign)
+        outs.append((y, O.moe_layer(x, assign, host, odic)))
+    assert any(st["graph"] is not None for st in layer._stages.values())
+    for y, y_ref in outs:  # earlier results intact after later calls
+        d = bf16_ulp_diff(y, y_ref)
+        assert d.max() <= 2
+        assert np.mean(d == 0) >= 0.99
+
+
 def test_moe_step_is_graph_capturable(dic):
     rng = np.random.default_rng(5)
     E, d_model, d_ff = 4, 64, 256

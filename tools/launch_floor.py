@@ -26,15 +26,18 @@ for n in (1, 2):
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2310_16795_b200 import _lib
-for smem, thr in ((0, 768), (100 * 1024, 768), (200 * 1024, 768), (227 * 1024, 768), (227 * 1024, 256)):
+MODES = {0: "plain", 1: "cooperative", 2: "PDL", 3: "cooperative+PDL"}
+for smem, thr, mode in ((0, 768, 0), (227 * 1024, 768, 0), (227 * 1024, 768, 1), (227 * 1024, 768, 2),
+                        (227 * 1024, 768, 3), (0, 768, 1)):
+    thr_arg = thr | (mode << 16)
     for n in (1, 8):
         sp = torch.cuda.current_stream().cuda_stream
-        _lib.check(_lib.lib.qmoe_debug_empty_launch(smem, thr, sp))
+        _lib.check(_lib.lib.qmoe_debug_empty_launch(smem, thr_arg, sp))
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for _ in range(n):
-                _lib.check(_lib.lib.qmoe_debug_empty_launch(smem, thr, torch.cuda.current_stream().cuda_stream))
+                _lib.check(_lib.lib.qmoe_debug_empty_launch(smem, thr_arg, torch.cuda.current_stream().cuda_stream))
         for _ in range(5):
             g.replay()
         torch.cuda.synchronize()
@@ -44,5 +47,5 @@ for smem, thr in ((0, 768), (100 * 1024, 768), (200 * 1024, 768), (227 * 1024, 7
             g.replay()
         e1.record()
         torch.cuda.synchronize()
-        print(f"empty kernel x{n} per graph, 148 CTAs x {thr} thr, {smem >> 10} KB smem: "
+        print(f"empty kernel x{n} per graph, {MODES[mode]}, 148 CTAs x {thr} thr, {smem >> 10} KB smem: "
               f"{e0.elapsed_time(e1) / (100 * n) * 1e3:.2f} us per kernel")
