@@ -481,6 +481,7 @@ __global__ void __launch_bounds__(THREADS, 1) seg_matvec_kernel(SegParams P) {
 // range up front (a window of up to WIN_RUNS runs / the x budget), so there is
 // no barrier between runs inside a window.
 constexpr int WIN_RUNS = 16;
+constexpr int WARP_PLAN_MAX = 256;  // fused step: single-warp dispatcher plan up to this many tokens
 
 struct WinRun {
   const uint16_t* cw;
@@ -702,7 +703,7 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     Lane c{0, 0, 0, -1, 0u}, n{0, 0, 0, -1, 0u};
     uint32_t ea[GRP], eb[GRP];
     uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = make_uint4(0u, 0u, 0u, 0u);
-    if (active) {  // first tasks' metadata, groups and entries: needs no x
+    if (active) {  // first tasks' row metadata: needs no x
       while (win[wc].task1 <= k) ++wc;
       c = lane_task(win[wc], k);
       wn = wc;
@@ -712,6 +713,11 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
         while (win[wn].task1 <= kn) ++wn;
         n = lane_task(win[wn], kn);
       }
+    }
+    // wi: the x rows are ready — their loads go out together with the
+    // metadata loads above (one round trip for both)
+    if (!COHERENT_X) stage_x();
+    if (active) {  // first codeword groups
       maxgc = __reduce_max_sync(FULL_MASK, lane_groups(c));
       q0 = lane_load(win[wc].cw, c, 0);
       if (maxgc >= 2) q1 = lane_load(win[wc].cw, c, 1);
@@ -721,17 +727,19 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
       table_fill_wait(tab_bar);
       tab_bar = nullptr;
     }
-    if (active) lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
-    // x staging after the first loads are in flight (fused wo phase: the x
-    // rows are other CTAs' h — wait for their runs first)
     if (COHERENT_X) {
+      // wo: x rows are other CTAs' h — look the first group up while their
+      // runs finish, then wait and stage
+      if (active) lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
       if (threadIdx.x == 0)
         for (int w = 0; w < nw; ++w) src.wait(win[w].ri);
       __syncthreads();
       trace_stamp(6);  // (last) window's producer runs done
+      stage_x();
     }
-    stage_x();
     __syncthreads();
+    if (!COHERENT_X && active) lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
+    if (!COHERENT_X && t == t_begin) trace_stamp(5);  // first window staged (wi)
     if (active) {
       for (;;) {
         const WinRun& W = win[wc];
@@ -947,51 +955,106 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   trace_stamp(0);
   table_fill_async(PW.gtab, PW.H, &tab_bar);  // overlaps the plan below
   // ---- 1. plan
-  if (T <= 32) {
-    // small step: one warp, no block barriers. Lane t holds token t; experts
-    // are the match_any groups, ordered by id; buffer order within an expert.
-    if (blockIdx.x == 0 && S.count_out)
-      for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = 0;
-    __syncthreads();
+  bool wpre_ready = false;
+  if (T <= WARP_PLAN_MAX) {
+    // one warp, no block barriers (the other warps wait once, below):
+    //  a. per-expert counts + each token's stable rank inside its expert
+    //     (chunks of 32 tokens in buffer order; match_any groups a chunk)
+    //  b. exclusive scans over experts (contiguous blocks per lane): token
+    //     start, run offset, weighted-run prefix
+    //  c. tokens placed in expert order, then each lane emits its experts'
+    //     runs {expert, ntok, tok0, tok1} and their weighted prefix
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
-      const int e = lane < T ? __ldg(S.assign + lane) : -1;
-      const bool ok = lane < T && e >= 0 && e < E;
-      const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
-      const int c = __popc(peers), rank = __popc(peers & ((1u << lane) - 1u));
-      const bool leader = ok && (__ffs(peers) - 1) == lane;
-      const unsigned L = __ballot_sync(FULL_MASK, leader);
-      int st = 0, co = 0, tot_t = 0, tot_c = 0;
-      for (unsigned m = L; m; m &= m - 1) {  // over distinct experts
-        const int b = __ffs(m) - 1;
-        const int eb = __shfl_sync(FULL_MASK, e, b), cb = __shfl_sync(FULL_MASK, c, b);
-        if (eb < e) {
-          st += cb;
-          co += (cb + ntu - 1) / ntu;
-        }
-        tot_t += cb;
-        tot_c += (cb + ntu - 1) / ntu;
+      int* rank = runs4;  // scratch: token ranks (runs4 is written in c.)
+      for (int e = lane; e < E; e += 32) cnt[e] = 0;
+      int ids[WARP_PLAN_MAX / 32];
+#pragma unroll
+      for (int k = 0; k < WARP_PLAN_MAX / 32; ++k) {  // all loads in flight together
+        const int t = k * 32 + lane;
+        ids[k] = (k * 32 < T && t < T) ? __ldg(S.assign + t) : -1;
       }
-      const int my_start = __shfl_sync(FULL_MASK, st, __ffs(peers) - 1);
-      if (ok) order[my_start + rank] = lane;
       __syncwarp();
-      if (leader) {
-        if (blockIdx.x == 0 && S.count_out) S.count_out[e] = c;
-        for (int ch = 0; ch * ntu < c; ++ch) {
-          const int nt = min(ntu, c - ch * ntu);
-          runs4[4 * (co + ch)] = e;
-          runs4[4 * (co + ch) + 1] = nt;
-          runs4[4 * (co + ch) + 2] = order[st + ch * ntu];
-          runs4[4 * (co + ch) + 3] = order[st + ch * ntu + (nt > 1 ? 1 : 0)];
+#pragma unroll
+      for (int k = 0; k < WARP_PLAN_MAX / 32; ++k) {
+        if (k * 32 >= T) break;
+        const int t = k * 32 + lane, e = ids[k];
+        const bool ok = t < T && e >= 0 && e < E;
+        const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (ok && lane == leader) {
+          base = cnt[e];
+          cnt[e] = base + __popc(peers);
+        }
+        base = __shfl_sync(FULL_MASK, base, leader);
+        if (t < T) rank[t] = ok ? base + __popc(peers & ((1u << lane) - 1u)) : -1;
+        __syncwarp();
+      }
+      trace_stamp(4);
+      const int per = (E + 31) >> 5;
+      const int lgn = ntu > 1 ? 1 : 0;  // ntu is 1 or 2 (NT_STREAM): shifts, not divisions
+      const int e0 = min(E, lane * per), e1 = min(E, e0 + per);
+      const int wfull = ntu > 1 ? S.w2 : 8;
+      int sv = 0, sc = 0, sw = 0;
+      for (int e = e0; e < e1; ++e) {
+        const int c = cnt[e];
+        sv += c;
+        sc += (c + lgn) >> lgn;
+        sw += (c >> lgn) * wfull + ((c & lgn) ? 8 : 0);
+      }
+      int iv = sv, ic = sc, iw = sw;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(FULL_MASK, iv, d), b = __shfl_up_sync(FULL_MASK, ic, d),
+                  w = __shfl_up_sync(FULL_MASK, iw, d);
+        if (lane >= d) {
+          iv += a;
+          ic += b;
+          iw += w;
         }
       }
-      if (lane == 0) {
-        start[E] = tot_t;
-        choff[E] = tot_c;
+      int bv = iv - sv, bc = ic - sc, bw = iw - sw;
+      for (int e = e0; e < e1; ++e) {
+        const int c = cnt[e];
+        start[e] = bv;
+        choff[e] = bc;
+        if (blockIdx.x == 0 && S.count_out) S.count_out[e] = c;
+        bv += c;
+        bc += (c + lgn) >> lgn;
       }
+      if (lane == 31) {
+        start[E] = iv;
+        choff[E] = ic;
+        wpre[ic] = iw;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < WARP_PLAN_MAX / 32; ++k) {
+        if (k * 32 >= T) break;
+        const int t = k * 32 + lane;
+        if (t < T && rank[t] >= 0) order[start[ids[k]] + rank[t]] = t;
+      }
+      __syncwarp();
+      bc = ic - sc;
+      for (int e = e0; e < e1; ++e) {
+        const int c = cnt[e], s0 = start[e];
+        for (int ch = 0; ch * ntu < c; ++ch, ++bc) {
+          const int nt = min(ntu, c - ch * ntu);
+          runs4[4 * bc] = e;
+          runs4[4 * bc + 1] = nt;
+          runs4[4 * bc + 2] = order[s0 + ch * ntu];
+          runs4[4 * bc + 3] = order[s0 + ch * ntu + (nt > 1 ? 1 : 0)];
+          wpre[bc] = bw;
+          bw += nt > 1 ? S.w2 : 8;
+        }
+      }
+      __syncwarp();
+      const int placed = __shfl_sync(FULL_MASK, iv, 31);
+      if (blockIdx.x == 0 && S.order_out)
+        for (int t = lane; t < placed; t += 32) S.order_out[t] = order[t];
     }
-    __syncthreads();
-    if (blockIdx.x == 0 && S.order_out && threadIdx.x < start[E]) S.order_out[threadIdx.x] = order[threadIdx.x];
+    wpre_ready = true;
   } else {
     for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;
     __syncthreads();
@@ -1077,7 +1140,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     int carry = 0;
-    for (int r0 = 0; r0 < nch; r0 += 32) {
+    for (int r0 = 0; r0 < (wpre_ready ? 0 : nch); r0 += 32) {
       const int r = r0 + lane;
       const int w = r < nch ? (runs4[4 * r + 1] > 1 ? S.w2 : 8) : 0;
       int inc = w;
@@ -1089,12 +1152,16 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       if (r < nch) wpre[r] = carry + inc - w;
       carry += __shfl_sync(FULL_MASK, inc, 31);
     }
-    if (lane == 0) wpre[nch] = carry;
+    if (lane == 0 && !wpre_ready) wpre[nch] = carry;
     __syncwarp();
     if (lane < 4) {  // task bounds of this CTA in both phases: {wi begin, wi end, wo begin, wo end}
       const int tpr = (lane < 2) ? S.tasks_wi : S.tasks_wo;
-      const int64_t W = (int64_t)wpre[nch] * tpr;  // total weighted tasks
-      const int64_t target = W * (blockIdx.x + (lane & 1)) / gridDim.x;
+      // target = total weighted tasks * k / grid; in double (exact product,
+      // one rounding; every CTA evaluates the same k identically) — 64-bit
+      // integer division is a long emulated sequence on the plan's critical path
+      const int k = blockIdx.x + (lane & 1);
+      const int64_t target =
+          (int64_t)__ddiv_rz((double)wpre[nch] * (double)tpr * (double)k, (double)gridDim.x);
       int lo = 0, hi = nch;  // last run with wpre[r] * tpr <= target
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -1106,7 +1173,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
         t = nch * tpr;
       } else {
         const int w = wpre[lo + 1] - wpre[lo];
-        t = lo * tpr + (int)min((int64_t)tpr, (target - (int64_t)wpre[lo] * tpr) / max(1, w));
+        t = lo * tpr + min(tpr, (int)(target - (int64_t)wpre[lo] * tpr) / max(1, w));
       }
       if ((lane & 1) && blockIdx.x == gridDim.x - 1) t = nch * tpr;
       s_split[lane] = t;

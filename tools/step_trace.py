@@ -41,7 +41,8 @@ for T in [int(t) for t in sys.argv[1:]] or [1, 8, 64]:
     r[:, 1:] = r[:, :1] + cyc[:, :3]
     sub = cyc[:, 3:]
     print("   plan counted / runs built / plan end (us since CTA start, median):",
-          np.median(sub[:, 1]).round(2), np.median(sub[:, 3]).round(2), np.median(cyc[:, 0]).round(2))
+          np.median(sub[:, 0]).round(2), np.median(sub[:, 3]).round(2), np.median(cyc[:, 0]).round(2))
+    print("   wi first window staged (us since CTA start, median/max):", np.median(sub[:, 1]).round(2), sub[:, 1].max().round(2))
     wait = r[:, :1] + sub[:, 2:3]
     slow = np.argsort(-r[:, 3])[:6]
     print("   slowest CTAs (wi end, last wo wait done, wo end):",
