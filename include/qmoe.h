@@ -308,6 +308,34 @@ int qmoe_moe_step(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_as
                   int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count,
                   int32_t hot_entries, void* stream);
 
+/* qmoe_moe_step plus combine scaling: d_y rows = d_gate[t] * bf16(wo_e h_t)
+ * (one f32 multiply after the per-row rounding; d_gate = the router's top-1
+ * probability, e.g. from qmoe_route). d_gate == NULL is qmoe_moe_step. The
+ * reference has no probability scaling; this is the Switch
+ * Transformer combine. */
+int qmoe_moe_step_gated(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_assign, int32_t T,
+                        int32_t E, const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi,
+                        int32_t lg_wo, int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype,
+                        int64_t ldx, uint16_t* d_h, int64_t ldh, float* d_y, int64_t ldy,
+                        int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count,
+                        int32_t hot_entries, const float* d_gate, void* stream);
+
+/* Top-1 router on the device, replaces RouterSim.assign
+ * (reference pipeline.py:164-182) for x already in HBM:
+ *  QMOE_ROUTE_ARGMAX: scores = f64(x) . proj (d x E row-major f64) + bias
+ *    (E f64, nullable), float64 as the reference; d_assign[t] = argmax (lowest
+ *    index on ties); d_scores = f64 scratch of qmoe_route_scratch(T, d, E)
+ *    elements (its first T * E hold the scores afterwards). Matches the
+ *    reference up to near-ties (summation order differs from numpy's matmul).
+ *  QMOE_ROUTE_HASH: wrapping-u64 hash of the f32 bit patterns with d_mult[d]
+ *    (RouterSim's `mult`), bit-exact; d_proj / d_scores unused.
+ * d_gate (f32[T], nullable) receives softmax(scores)[id] (1 for HASH). */
+enum { QMOE_ROUTE_ARGMAX = 0, QMOE_ROUTE_HASH = 1 };
+int64_t qmoe_route_scratch(int32_t T, int32_t d, int32_t E);
+int qmoe_route(int rule, const void* d_x, int x_dtype, int64_t ldx, int32_t T, int32_t d, int32_t E,
+               const double* d_proj, const double* d_bias, const uint64_t* d_mult, double* d_scores,
+               int32_t* d_assign, float* d_gate, void* stream);
+
 /* Batched-token decode-then-MMA pass (many tokens per expert, e.g.
  * Switch-large-128 with T in the thousands): for every expert e with tokens
  * d_order[start_e .. start_e + d_expert_count[e]) (qmoe_moe_plan's outputs,
@@ -324,12 +352,14 @@ int qmoe_dense_moe_pass(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_ma
                         int x_dtype, int64_t ldx, void* d_y, int y_mode, int64_t ldy,
                         int32_t tokens_per_block, int32_t hot_entries, void* stream);
 
-/* Debug hook: d_buf = u64[num_sms * 8] receives per-CTA %globaltimer stamps of
- * qmoe_moe_step phases (0 start, 1 plan + table staged, 2 wi done, 3 wo
- * done); NULL disables. Not for production use. */
+/* Debug hook: d_buf = u64[num_sms * 8] receives per-CTA phase stamps of
+ * qmoe_moe_step: [0] %globaltimer at the CTA's start, [1..7] SM cycles since
+ * then (1 plan done, 2 wi done, 3 wo done, 4-7 plan / window sub-steps);
+ * NULL disables. Not for production use. */
 int qmoe_debug_step_trace(void* d_buf);
-/* Debug hook: an empty kernel of num_sms CTAs x threads with smem_bytes of
- * dynamic shared memory (launch-floor measurements). */
+/* Debug hook: an empty kernel of num_sms CTAs x (threads & 0xFFFF) with
+ * smem_bytes of dynamic shared memory (launch-floor measurements); threads
+ * bits 16+ = launch mode (1 cooperative, 2 programmatic dependent, 3 both). */
 int qmoe_debug_empty_launch(int32_t smem_bytes, int32_t threads, void* stream);
 
 #ifdef __cplusplus

@@ -40,7 +40,7 @@ from .dictionary import (
 )
 from .errors import ConfigError, CorruptionError, DictionaryMismatchError, MoepackError, TierCapacityError
 from .moe import CompressedMoELayer
-from .pipeline import RouterSim
+from .pipeline import DeviceRouter, RouterSim
 from .quantize import QuantGrid, TernaryMatrix, make_grid, reconstruction_levels, rtn_quantize, rtn_quantize_device
 from .stats import RateReport, compression_rate, natural_sparsity, sample_ternary, theoretical_limit
 

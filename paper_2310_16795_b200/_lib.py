@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("QMOE_LIB_PATH") or os.path.join(_HERE, "_lib", "libqm
 
 QMOE_OK, QMOE_EINVAL, QMOE_ECORRUPT, QMOE_ECUDA, QMOE_EUNSUPPORTED = 0, 1, 2, 3, 4
 QMOE_X_F32, QMOE_X_BF16 = 0, 1
+QMOE_ROUTE_ARGMAX, QMOE_ROUTE_HASH = 0, 1
 DICT_SIZE = 65536
 NT_MAX = 4
 
@@ -82,6 +83,10 @@ _SIGS = {
     "qmoe_moe_plan": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "qmoe_moe_step": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, ctypes.c_int, i64, vp,
                                      i64, vp, i64, vp, vp, vp, i32, vp]),
+    "qmoe_moe_step_gated": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, ctypes.c_int, i64,
+                                           vp, i64, vp, i64, vp, vp, vp, i32, vp, vp]),
+    "qmoe_route_scratch": (i64, [i32, i32, i32]),
+    "qmoe_route": (ctypes.c_int, [ctypes.c_int, vp, ctypes.c_int, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "qmoe_debug_step_trace": (ctypes.c_int, [vp]),
     "qmoe_debug_empty_launch": (ctypes.c_int, [i32, i32, vp]),
     "qmoe_dense_moe_pass": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, i32, i32, vp, ctypes.c_int, i64, vp,

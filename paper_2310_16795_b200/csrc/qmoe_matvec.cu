@@ -66,6 +66,7 @@ struct SegParams {
   int64_t ldy;
   int xcap;                   // x elements staged per token
   int xbytes;                 // x staging bytes (pipe kernel: several runs' slots)
+  const float* gate;          // STORE_F32 only, nullable: y = gate[t] * bf16(dot)
 };
 
 struct Run {
@@ -252,7 +253,9 @@ __device__ __forceinline__ void store_row(const SegParams& P, const Run& R, int 
     if (P.y_mode == QMOE_Y_RELU_BF16) {
       reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(v, 0.f)) >> 16);
     } else if (P.y_mode == QMOE_Y_STORE_F32) {
-      reinterpret_cast<float*>(P.y)[t * P.ldy + row] = v + 0.f;  // == 0 + v
+      float o = v + 0.f;  // == 0 + v
+      if (P.gate) o *= __ldg(P.gate + t);
+      reinterpret_cast<float*>(P.y)[t * P.ldy + row] = o;
     } else {
       float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
       *yp = *yp + v;
@@ -1491,6 +1494,16 @@ int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assig
                   int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h, int64_t ldh, float* d_y,
                   int64_t ldy, int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count, int32_t hot_entries,
                   void* stream) {
+  return qmoe_moe_step_gated(d, d_table, d_assign, T, E, d_mats, tokens_per_run, lg_wi, lg_wo, d_model, d_ff, d_x,
+                             x_dtype, ldx, d_h, ldh, d_y, ldy, d_counters, d_order, d_expert_count, hot_entries,
+                             nullptr, stream);
+}
+
+int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assign, int32_t T, int32_t E,
+                        const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo,
+                        int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h,
+                        int64_t ldh, float* d_y, int64_t ldy, int32_t* d_counters, int32_t* d_order,
+                        int32_t* d_expert_count, int32_t hot_entries, const float* d_gate, void* stream) {
   if (!d || !d->d_stab || !d_assign || T < 0 || E < 1 || !d_mats || tokens_per_run < 1 ||
       tokens_per_run > NT_STREAM || lg_wi < 0 || lg_wi > 5 || lg_wo < 0 || lg_wo > 5 || d_model <= 0 ||
       d_ff <= 0 || !d_h || !d_y || !d_counters || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16))
@@ -1518,6 +1531,7 @@ int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assig
   SP.wo.y = d_y;
   SP.wo.y_mode = QMOE_Y_STORE_F32;
   SP.wo.ldy = ldy;
+  SP.wo.gate = d_gate;
   SP.assign = d_assign;
   SP.T = T;
   SP.E = E;

@@ -267,19 +267,44 @@ class CompressedMoELayer:
             _lib.ptr(self.order), rows, cols, _lib.ptr(x), xt, x.stride(0), _lib.ptr(y), y_mode, y.stride(0), bn,
             0, _lib.stream_ptr(stream)))
 
-    def step(self, x, assign, out, stream=None) -> None:
-        """The whole step as one cooperative launch (qmoe_moe_step)."""
+    def step(self, x, assign, out, stream=None, gate=None) -> None:
+        """The whole step as one cooperative launch (qmoe_moe_step; with
+        `gate` (f32[T] on the device) the output rows are scaled by it,
+        qmoe_moe_step_gated)."""
         import torch
 
         T = assign.shape[0]
         self._T = T
         lg_wi, lg_wo = self.lanes_per_row(T)
         xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
-        _lib.check(_lib.lib.qmoe_moe_step(
+        _lib.check(_lib.lib.qmoe_moe_step_gated(
             self.handle, self._table(), _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit,
             lg_wi, lg_wo, self.d_model, self.d_ff, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h), self.h.stride(0),
             _lib.ptr(out), out.stride(0), _lib.ptr(self.counters), _lib.ptr(self.order), _lib.ptr(self.expert_count),
-            max(self.hot_entries(T, True), self.hot_entries(T, False)), _lib.stream_ptr(stream)))
+            max(self.hot_entries(T, True), self.hot_entries(T, False)), _lib.ptr(gate), _lib.stream_ptr(stream)))
+
+    def forward_routed(self, x, router, gated: bool = False, out=None, stream=None):
+        """Router + layer on the device: expert ids (and, with `gated`, the
+        top-1 softmax probability scaling each output row — the Switch combine;
+        the reference has none) from `router` (pipeline.DeviceRouter), then the
+        step. Returns (out, assign, gate)."""
+        import torch
+
+        assign, gate = router(x, gated=gated, stream=stream)
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty((T, self.d_model), dtype=torch.float32, device=self.device)
+        if self.fused and not self.use_dense(T) and T <= self.max_tokens:
+            try:
+                self.step(x, assign, out, stream, gate=gate)
+                return out, assign, gate
+            except _lib.QmoeError as err:
+                if err.status != _lib.QMOE_EUNSUPPORTED:
+                    raise
+        self.forward_device(x, assign, out=out, stream=stream)
+        if gate is not None:
+            out.mul_(gate[:, None])
+        return out, assign, gate
 
     GRAPH_CACHE = 8  # token counts with a captured host-API graph per layer
 

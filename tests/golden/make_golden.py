@@ -18,6 +18,10 @@ Every fixture records what reference call produced it:
   trace.json        simulate_warp_row traces (codec.py:293-338)
   checkpoint.bin    write_checkpoint bytes (codec.py:341-351)
   misc.json         compression_rate (stats.py:103-114), theoretical_limit
+  routing.npz       RouterSim.assign hash / argmax (+skew) (pipeline.py:164-182)
+                    on bf16 tokens (the GPU router's parity vectors)
+
+`python tests/golden/make_golden.py routing` regenerates routing.npz only.
 """
 
 from __future__ import annotations
@@ -118,7 +122,7 @@ def main() -> None:
         if codes.shape[1] > 0:
             x = (rng.normal(size=codes.shape[1]) / np.sqrt(codes.shape[1])).astype(np.float32)
             y0 = rng.normal(size=codes.shape[0]).astype(np.float32)
-            out[f"c{i}_x"] = x
+            out[f"c{i}_xbits"] = f32_to_bf16_bits(x)  # exact: x is bf16-valued
             out[f"c{i}_y"] = fused_matvec(c, x, dic)
             out[f"c{i}_y0"] = y0
             out[f"c{i}_y_acc"] = fused_matvec(c, x, dic, y=y0.copy())
@@ -215,5 +219,25 @@ def main() -> None:
     print("golden fixtures written to", HERE)
 
 
+def make_routing() -> None:
+    out = {}
+    cases = [("hash", 128, 768, 64, 0.0, 3), ("hash", 2048, 2080, 12, 0.0, 5), ("argmax", 128, 768, 64, 0.0, 1),
+             ("argmax", 128, 768, 64, 0.5, 1), ("argmax", 2048, 2080, 12, 0.0, 2)]
+    for i, (rule, E, d, T, skew, seed) in enumerate(cases):
+        x = bf16_round(np.random.default_rng(100 + i).normal(size=(T, d)).astype(np.float32))
+        out[f"c{i}_xbits"] = f32_to_bf16_bits(x)  # exact: x is bf16-valued
+        out[f"c{i}_assign"] = RouterSim(num_experts=E, rule=rule, seed=seed, skew=skew).assign(x)
+        out[f"c{i}_meta"] = np.array([E, d, T, seed], np.int64)
+        out[f"c{i}_rule"] = np.array(rule)
+        out[f"c{i}_skew"] = np.float64(skew)
+    out["n"] = np.int64(len(cases))
+    np.savez_compressed(os.path.join(HERE, "routing.npz"), **out)
+    print("routing.npz written")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["routing"]:
+        make_routing()
+    else:
+        main()
+        make_routing()

@@ -22,7 +22,7 @@ from paper_2310_16795_b200 import _lib
 def header_functions():
     with open(os.path.join(ROOT, "include", "qmoe.h")) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(qmoe_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(qmoe_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -110,3 +110,25 @@ def test_bf16_known_answers():
     u = np.array([0x3F808000, 0x3F818000, 0x3F80FFFF, 0x7F7FFFFF, 0x00000000, 0x80000000], np.uint32)
     bits = O.f32_to_bf16_bits(u.view(np.float32))
     assert bits.tolist() == [0x3F80, 0x3F82, 0x3F81, 0x7F80, 0x0000, 0x8000]
+
+
+def _routing_cases(golden):
+    g = golden("routing.npz")
+    for i in range(int(g["n"])):
+        E, d, T, seed = (int(v) for v in g[f"c{i}_meta"])
+        x = (g[f"c{i}_xbits"].astype(np.uint32) << 16).view(np.float32)
+        yield str(g[f"c{i}_rule"]), E, d, T, seed, float(g[f"c{i}_skew"]), x, g[f"c{i}_assign"]
+
+
+def test_routersim_mirror_matches_reference_routing(golden):
+    """The package's host RouterSim (the ids the GPU path and the oracle see)
+    reproduces the reference's RouterSim.assign (pipeline.py:164-182) on the
+    golden vectors, both rules."""
+    from paper_2310_16795_b200.pipeline import RouterSim
+
+    n = 0
+    for rule, E, d, T, seed, skew, x, want in _routing_cases(golden):
+        got = RouterSim(E, rule=rule, seed=seed, skew=skew).assign(x)
+        assert np.array_equal(got, want), (rule, E, d)
+        n += 1
+    assert n == 5
