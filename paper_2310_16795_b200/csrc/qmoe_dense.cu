@@ -25,6 +25,7 @@
 // streaming kernel).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <string>
 
 #include "qmoe_device.cuh"
@@ -408,6 +409,308 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
+// ------------------------------------------------------------------ row-walk kernel (v3)
+// Item = (expert e, 256-row block, <= BN-token block); thread = row; 128-column
+// chunks (2 SW128 K-blocks); two CTAs per SM, so one CTA's decode overlaps the
+// other's MMA wait and global-load latency.
+//   decode   each thread walks ITS row's codeword stream across the chunks
+//            (16-byte groups, three groups in flight): per codeword one table
+//            lookup and <= 3 shared stores of bf16 levels into its zero-filled
+//            tile row; a codeword that straddles the chunk end is revisited by
+//            the next chunk (values left of the chunk skipped), so no column
+//            points are needed and the work per row is exactly its codewords.
+//   mma      8 tcgen05.mma (2 M-blocks x 2 K-blocks x 4 K16 steps, N = BN) per
+//            chunk into 2 x BN TMEM columns, committed to an mbarrier that is
+//            awaited before the tiles are rewritten.
+
+__device__ __forceinline__ uint4 ld_group_nc(const uint16_t* cw, int g) {
+  // 8 codewords (16-byte aligned group g of the matrix's stream), read once
+  uint4 a;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+               : "l"(cw + (size_t)g * 8));
+  return a;
+}
+
+__device__ __forceinline__ uint32_t lookup_pred(uint32_t cw, uint32_t tab_s, uint32_t H, const uint32_t* gtab) {
+  // entry of codeword cw: hot table in shared memory, else global — both
+  // loads predicated (no divergent branch: a warp's misses do not serialise)
+  uint32_t v;
+  asm volatile(
+      "{ .reg .pred p; setp.lt.u32 p, %1, %2;\n\t"
+      "@p ld.shared.u32 %0, [%3];\n\t"
+      "@!p ld.global.nc.u32 %0, [%4]; }"
+      : "=r"(v)
+      : "r"(cw), "r"(H), "r"(tab_s + 4u * cw), "l"(gtab + cw));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t group_cw(const uint4& q, uint32_t u) {
+  const uint32_t w = (u & 4u) ? ((u & 2u) ? q.w : q.z) : ((u & 2u) ? q.y : q.x);
+  return (u & 1u) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+template <int BN, int RW_ROWS, int RW_KC, int MINB>
+__global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) {
+  constexpr int RW_THREADS = RW_ROWS;
+  constexpr int MB = RW_ROWS / 128, KB = RW_KC / 64;
+  constexpr uint32_t TMEM_COLS = MB * BN < 32 ? 32 : MB * BN;
+  __shared__ __align__(8) uint64_t tab_bar, mma_bar;
+  __shared__ int s_total;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_tok[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t base = sbase();
+  const uint32_t tab_s = base;
+  const uint32_t w_s = (base + P.w_off + 1023u) & ~1023u;  // KB blocks x 256 rows x 128 B
+  const uint32_t x_s = w_s + (uint32_t)KB * RW_ROWS * 128u;  // KB blocks x BN x 128 B
+  int* start = reinterpret_cast<int*>(dsm + P.plan_off);
+  int* ipre = start + P.E + 1;
+  const int E = P.E;
+  const int nrb = (P.rows + RW_ROWS - 1) / RW_ROWS;
+  const int nk = (P.cols + RW_KC - 1) / RW_KC;
+  const uint32_t tb_mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
+  const uint32_t mma_mb = (uint32_t)__cvta_generic_to_shared(&mma_bar);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_mb));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma_mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)P.H * 4;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tb_mb), "r"(bytes) : "memory");
+    for (uint32_t o = 0; o < bytes; o += 32768u)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tab_s + o),
+          "l"(reinterpret_cast<const char*>(P.gtab) + o), "r"(min(32768u, bytes - o)), "r"(tb_mb)
+          : "memory");
+  }
+  if (warp == 2) {  // item prefix over experts: warp scan of per-expert item counts
+    int carry_t = 0, carry_i = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int c = e < E ? __ldg(P.count + e) : 0;
+      const int ni = nrb * ((c + BN - 1) / BN);
+      int it = c, ii = ni;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(FULL_MASK, it, d), b = __shfl_up_sync(FULL_MASK, ii, d);
+        if (lane >= d) {
+          it += a;
+          ii += b;
+        }
+      }
+      if (e < E) {
+        start[e] = carry_t + it - c;
+        ipre[e] = carry_i + ii - ni;
+      }
+      carry_t += __shfl_sync(FULL_MASK, it, 31);
+      carry_i += __shfl_sync(FULL_MASK, ii, 31);
+    }
+    if (lane == 0) {
+      start[E] = carry_t;
+      ipre[E] = carry_i;
+      s_total = carry_i;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  mbar_wait(tb_mb, 0);
+  const uint32_t tmem = s_tmem;
+  const int total = s_total;
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t rx = (uint32_t)(tid & 7) << 4;  // SW128 16-byte chunk swizzle of my row
+  const uint32_t wrow = w_s + (uint32_t)tid * 128u;
+  const uint32_t idesc = idesc_bf16_f32<BN>();
+  uint32_t mma_phase = 0;
+  constexpr int XP = BN * (RW_KC / 8);                  // 16-byte x pieces per chunk
+  constexpr int XV = (XP + RW_THREADS - 1) / RW_THREADS;  // ... per thread
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    int lo = 0, hi = E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ipre[mid] <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    const int e = lo, local = item - ipre[e];
+    const int rb = local % nrb, tb = local / nrb;
+    const int cnt = start[e + 1] - start[e];
+    const int nt = min(BN, cnt - tb * BN);
+    const int tok0 = start[e] + tb * BN;
+    const qmoe_matrix& M = P.mats[2 * e + P.pass];
+    const uint16_t* cwp = M.cw;
+    const int r = rb * RW_ROWS + tid;
+    const bool valid = r < P.rows;
+    int s = 0, n = 0;
+    uint32_t wlo = 0, whi = 0;
+    if (valid) {
+      s = __ldg(M.row_off + r);
+      n = __ldg(M.row_off + r + 1) - s;
+      const uint32_t mm = __ldg(M.row_minmax + r);
+      wlo = mm & 0xFFFFu;
+      whi = mm >> 16;
+    }
+    if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
+    // my row's codeword stream: groups of 8 (16 bytes), three in flight, and
+    // the entries of the next 4 codewords (looked up 4 codewords ahead)
+    const int glast = n > 0 ? (s + n - 1) >> 3 : (s >> 3);
+    int g = s >> 3;
+    uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = q0, q2 = q0;
+    if (n > 0) {
+      q0 = ld_group_nc(cwp, g);
+      q1 = ld_group_nc(cwp, min(g + 1, glast));
+      q2 = ld_group_nc(cwp, min(g + 2, glast));
+    }
+    int p = s;  // global index of my next codeword
+    auto cw_at = [&](int idx) -> uint32_t {  // idx within groups g, g + 1
+      return (idx >> 3) == g ? group_cw(q0, (uint32_t)idx & 7u) : group_cw(q1, (uint32_t)idx & 7u);
+    };
+    uint32_t e0 = 0u, e1 = 0u, e2 = 0u, e3 = 0u;
+    if (n > 0) {
+      e0 = lookup_pred(cw_at(p), tab_s, H, P.gtab);
+      e1 = lookup_pred(cw_at(p + 1), tab_s, H, P.gtab);
+      e2 = lookup_pred(cw_at(p + 2), tab_s, H, P.gtab);
+      e3 = lookup_pred(cw_at(p + 3), tab_s, H, P.gtab);
+    }
+    int i = 0, c = 0;  // my next codeword (row-relative), its start column
+    __syncthreads();   // s_tok
+    uint4 xr[XV];
+    auto load_x = [&](int k0) {
+#pragma unroll
+      for (int v = 0; v < XV; ++v) {
+        const int idx = tid + v * RW_THREADS, nn = idx / (RW_KC / 8), c8 = idx % (RW_KC / 8);
+        xr[v] = (idx < XP && nn < nt && k0 + c8 * 8 < P.cols) ? x_chunk8(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8)
+                                                  : make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    load_x(0);
+    for (int k = 0; k < nk; ++k) {
+      const int k0 = k * RW_KC;
+      if (k > 0) {  // the previous chunk's MMAs must be done reading W / X
+        mbar_wait(mma_mb, mma_phase);
+        mma_phase ^= 1u;
+      }
+#pragma unroll
+      for (int v = 0; v < XV; ++v) {
+        const int idx = tid + v * RW_THREADS, nn = idx / (RW_KC / 8), c8 = idx % (RW_KC / 8);
+        const uint32_t a = x_s + (uint32_t)(c8 >> 3) * (BN * 128u) + (uint32_t)nn * 128u +
+                           ((uint32_t)((c8 & 7) ^ (nn & 7)) << 4);
+        if (idx < XP)
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(xr[v].x), "r"(xr[v].y), "r"(xr[v].z),
+                       "r"(xr[v].w));
+      }
+      if (k + 1 < nk) load_x(k0 + RW_KC);
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+        for (int c16 = 0; c16 < 8; ++c16)
+          sts_zero16(wrow + (uint32_t)kb * (RW_ROWS * 128u) + 16u * (uint32_t)((c16 + lane) & 7));
+      // walk: codewords starting left of the chunk end
+      const int kend = k0 + RW_KC;
+      while (i < n && c < kend) {
+        const uint32_t en = e0;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          const uint32_t f = __byte_perm(en, 0u, 0x4440u + jj);
+          const int vk = c + (int)(f >> 2) - k0;
+          if (f != 0x7Fu && (unsigned)vk < (unsigned)RW_KC)
+            sts_u16(wrow + (uint32_t)(vk >> 6) * (RW_ROWS * 128u) + ((((uint32_t)vk & 63u) * 2u) ^ rx),
+                    ((en >> (24 + jj)) & 1u) ? whi : wlo);
+        }
+        const int nl = (int)(en >> 28) * 2;
+        if (c + nl > kend) break;  // straddles into the next chunk: revisit there
+        c += nl;
+        ++i;
+        ++p;
+        e0 = e1;
+        e1 = e2;
+        e2 = e3;
+        if ((p & 7) == 0) {
+          ++g;
+          q0 = q1;
+          q1 = q2;
+          q2 = ld_group_nc(cwp, min(g + 2, glast));
+        }
+        e3 = lookup_pred(cw_at(p + 3), tab_s, H, P.gtab);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint64_t da =
+                  sw128_desc(w_s + (uint32_t)kb * (RW_ROWS * 128u) + (uint32_t)mb * (128u * 128u) + (uint32_t)ks * 32u);
+              const uint64_t db = sw128_desc(x_s + (uint32_t)kb * (BN * 128u) + (uint32_t)ks * 32u);
+              const uint32_t accf = (k > 0 || kb > 0 || ks > 0) ? 1u : 0u;
+              asm volatile(
+                  "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+                      tmem + (uint32_t)mb * BN),
+                  "l"(da), "l"(db), "r"(idesc), "r"(accf));
+            }
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mma_mb)
+                     : "memory");
+      }
+    }
+    mbar_wait(mma_mb, mma_phase);
+    mma_phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    {  // epilogue: warp w reads TMEM lane quarter w % 4 of M-block w / 4, 32 tokens per load
+      const int quarter = warp & 3, mbk = warp >> 2;
+      const int row = rb * RW_ROWS + mbk * 128 + 32 * quarter + lane;
+#pragma unroll
+      for (int half = 0; half < (BN + 31) / 32; ++half) {
+        uint32_t v[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)mbk * BN + (uint32_t)half * 32u;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < P.rows) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int nn = half * 32 + j;
+            if (nn >= nt) break;
+            const int64_t t = s_tok[nn];
+            const float vv = bf16_round_dev(__uint_as_float(v[j]));
+            if (P.y_mode == QMOE_Y_RELU_BF16) {
+              reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(vv, 0.f)) >> 16);
+            } else if (P.y_mode == QMOE_Y_STORE_F32) {
+              reinterpret_cast<float*>(P.y)[t * P.ldy + row] = vv + 0.f;
+            } else {
+              float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
+              *yp = *yp + vv;
+            }
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // TMEM read before the next item's first MMA; token ids reused
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
 bool al16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
 
 }  // namespace
@@ -443,7 +746,51 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   const int BN = tokens_per_block;
   P.cp_log2 = 7;  // DeviceMatrix.build_colpoints: 128-column points
   P.dbg = getenv("QMOE_DENSE_DBG") ? atoi(getenv("QMOE_DENSE_DBG")) : 0;
-  // item shape: 128 rows x 256-column chunks (default, 4 lanes per row) or 256 x 128 (QMOE_DENSE_SHAPE)
+  if (!getenv("QMOE_DENSE_V2")) {  // row-walk kernel
+    // shape: rows per item (= threads) x columns per chunk x CTAs per SM; the
+    // hot table gets the rest of shared memory (its hit rate matters: the
+    // codeword ranks are spread, 16K entries cover ~80%, 32K ~91%)
+    int RWR = 256, RWK = 64, RWB = 2;
+    if (const char* sh = getenv("QMOE_DENSE_RW")) sscanf(sh, "%dx%dx%d", &RWR, &RWK, &RWB);
+    const size_t wbytes = (size_t)RWR * RWK * 2 + 1024, xbytes = (size_t)(RWK / 64) * BN * 128;
+    const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
+    const size_t static_smem = 1024, per_cta = (size_t)d->max_smem_optin / RWB - (RWB > 1 ? 1024 : 0);
+    if (wbytes + xbytes + plan + static_smem + 4096 > per_cta)
+      return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts for the dense pass");
+    int H = (int)((per_cta - wbytes - xbytes - plan - static_smem) / 4);
+    H = std::min(H, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE) & ~255;
+    P.H = std::max(H, 256);
+    P.w_off = P.H * 4;
+    P.x_off = P.w_off + (int)wbytes;
+    P.plan_off = P.x_off + (int)xbytes;
+    const size_t smem = (size_t)P.plan_off + plan;
+    const int grid = RWB * d->num_sms;
+#define QMOE_RW_LAUNCH(BNv, Rv, Kv, Bv)                                                                        \
+  do {                                                                                                       \
+    CK(cudaFuncSetAttribute(dense_rw_kernel<BNv, Rv, Kv, Bv>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                            (int)smem),                                                                      \
+       "attr");                                                                                              \
+    dense_rw_kernel<BNv, Rv, Kv, Bv><<<grid, Rv, smem, S(stream)>>>(P);                                      \
+  } while (0)
+    auto is = [&](int r, int k, int b) { return RWR == r && RWK == k && RWB == b; };
+    if (BN == 64) {
+      if (is(512, 64, 1)) QMOE_RW_LAUNCH(64, 512, 64, 1);
+      else if (is(512, 128, 1)) QMOE_RW_LAUNCH(64, 512, 128, 1);
+      else if (is(256, 128, 2)) QMOE_RW_LAUNCH(64, 256, 128, 2);
+      else if (is(256, 64, 2)) QMOE_RW_LAUNCH(64, 256, 64, 2);
+      else return qmoe::fail(QMOE_EINVAL, "QMOE_DENSE_RW: unknown shape");
+    } else {
+      if (is(512, 64, 1)) QMOE_RW_LAUNCH(32, 512, 64, 1);
+      else if (is(512, 128, 1)) QMOE_RW_LAUNCH(32, 512, 128, 1);
+      else if (is(256, 128, 2)) QMOE_RW_LAUNCH(32, 256, 128, 2);
+      else if (is(256, 64, 2)) QMOE_RW_LAUNCH(32, 256, 64, 2);
+      else return qmoe::fail(QMOE_EINVAL, "QMOE_DENSE_RW: unknown shape");
+    }
+#undef QMOE_RW_LAUNCH
+    CK(cudaGetLastError(), "dense_rw_kernel launch");
+    return QMOE_OK;
+  }
+  // v2 (QMOE_DENSE_V2): 128 rows x 256-column chunks (4 lanes per row) or 256 x 128 (QMOE_DENSE_SHAPE)
   const bool tall = getenv("QMOE_DENSE_SHAPE") && std::string(getenv("QMOE_DENSE_SHAPE")) == "256x128";
   const int R = tall ? 256 : 128, KC = tall ? 128 : 256;  // rows per item x columns per chunk
   const size_t wbytes = (size_t)R * KC * 2 + 1024, xbytes = (size_t)(KC / 64) * BN * 128;  // + 1 KB: SW128 alignment
