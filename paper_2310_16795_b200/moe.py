@@ -241,7 +241,10 @@ class CompressedMoELayer:
         streaming path)."""
         import torch
 
-        if self.packed or not bool(self.dic.device_info(self.device.index)["sparse_path"]):
+        sparse = getattr(self, "_sparse_path", None)
+        if sparse is None:  # a property of the dictionary: ask the library once
+            sparse = self._sparse_path = bool(self.dic.device_info(self.device.index)["sparse_path"])
+        if self.packed or not sparse:
             return False
         mode = os.environ.get("QMOE_DENSE", "auto")
         want = mode == "1" if mode in ("0", "1") else T / self._runs_est(T) >= self.DENSE_MIN_TOKENS

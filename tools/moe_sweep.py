@@ -41,11 +41,20 @@ for T in Ts:
     for i in range(n):
         layers[i % L].forward_device(xd[i % 4], ad[i % 4], out=outs[i % L])
     torch.cuda.synchronize()
-    for i in range(n):
+    if os.environ.get("ONEGRAPH") == "1":  # all n steps in one graph (a model forward's launch pattern)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            layers[i % L].forward_device(xd[i % 4], ad[i % 4], out=outs[i % L])
+            for i in range(n):
+                layers[i % L].forward_device(xd[i % 4], ad[i % 4], out=outs[i % L])
         graphs.append(g)
+        n_per_graph = n
+    else:
+        n_per_graph = 1
+        for i in range(n):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                layers[i % L].forward_device(xd[i % 4], ad[i % 4], out=outs[i % L])
+            graphs.append(g)
     for g in graphs:
         g.replay()
     torch.cuda.synchronize()
@@ -57,7 +66,7 @@ for T in Ts:
             g.replay()
     e1.record()
     torch.cuda.synchronize()
-    step = e0.elapsed_time(e1) / (reps * n) * 1e3
+    step = e0.elapsed_time(e1) / (reps * len(graphs) * n_per_graph) * 1e3
     nbytes = np.mean([layers[i % L].touched_bytes(asg[i % 4]) for i in range(n)])
     # per-pass timings (outside graphs)
     s = torch.cuda.current_stream()
