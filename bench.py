@@ -550,7 +550,10 @@ def main():
 def ep_main(args, world, rank, local):
     """--gpus N > 1: expert-parallel layer, experts sharded in contiguous
     blocks over the ranks, NCCL all-to-all dispatch/combine (weak scaling:
-    every rank brings T tokens)."""
+    every rank brings T tokens). value = compressed bytes all ranks streamed /
+    max-over-ranks device time."""
+    import time
+
     import torch
     import torch.distributed as dist
 
@@ -564,7 +567,7 @@ def ep_main(args, world, rank, local):
     T = args.tokens
     dic = q.generate_dictionary()
     layers, pool = [], 0
-    while pool < args.pool_factor * L2_BYTES / max(1, world) or not layers:
+    while pool < args.pool_factor * L2_BYTES or not layers:
         lay = build_layer(E_loc, d_model, d_ff, seed=1000 * rank + len(layers), dic=dic, device=dev,
                           max_tokens=T * world)
         layers.append(lay)
@@ -573,42 +576,79 @@ def ep_main(args, world, rank, local):
             break
     L = len(layers)
     router = q.RouterSim(E, rule="argmax", seed=0)
-    rng = np.random.default_rng(rank)
     nb = 4
-    xs = [q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32)) for _ in range(nb)]
-    asg = [router.assign(x) for x in xs]
+    # every rank's tokens are a pure function of (rank, batch): each rank can
+    # count, on the host, the experts of its block that step i touches
+    all_x = [[q.bf16_round(np.random.default_rng(1000 * r + b).normal(size=(T, d_model)).astype(np.float32))
+              for b in range(nb)] for r in range(world)]
+    all_a = [[router.assign(x) for x in xr] for xr in all_x]
+    xs, asg = all_x[rank], all_a[rank]
     xd = [torch.from_numpy(x).to(dev).to(torch.bfloat16) for x in xs]
     ad = [torch.from_numpy(a).to(dev) for a in asg]
-    cur = {"l": 0, "bytes": 0}
+
+    def step_bytes(i):
+        ids = np.concatenate([all_a[r][i % nb] for r in range(world)])
+        mine = ids[(ids >= rank * E_loc) & (ids < (rank + 1) * E_loc)] - rank * E_loc
+        return layers[i % L].touched_bytes(mine) if mine.size else 0
+
+    cur = {"l": 0}
 
     def local_fn(x_recv, local_ids):
-        lay = layers[cur["l"]]
-        cur["bytes"] += lay.touched_bytes(local_ids.cpu().numpy()) if local_ids.numel() else 0
         if local_ids.numel() == 0:
             return torch.zeros((0, d_model), device=dev)
-        return lay.forward_device(x_recv, local_ids)
+        return layers[cur["l"]].forward_device(x_recv, local_ids)
 
     ep = ExpertParallelMoE(E, local_fn)
-    for i in range(args.warmup):
+
+    def step(i):
         cur["l"] = i % L
-        ep.forward(xd[i % nb], ad[i % nb])
+        return ep.forward(xd[i % nb], ad[i % nb])
+
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize()
     dist.barrier()
-    cur["bytes"] = 0
+    my_bytes = float(sum(step_bytes(args.warmup + i) for i in range(args.steps)))
+    cs = ClockSampler(local)
+    cs.__enter__()
+    t_end = time.time() + 0.5
+    while time.time() < t_end:  # sustained steps into the timed region (clock sampling window)
+        for i in range(8):
+            step(i)
+        torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        cur["l"] = i % L
-        ep.forward(xd[i % nb], ad[i % nb])
+        step(args.warmup + i)
     e1.record()
     torch.cuda.synchronize()
+    cs.__exit__()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    b = torch.tensor([float(cur["bytes"])], device=dev, dtype=torch.float64)
+    b = torch.tensor([my_bytes], device=dev, dtype=torch.float64)
     dist.all_reduce(b)
     t_sec, tot = float(t.item()), float(b.item())
+    # e2e: host tokens + ids in, host outputs back, through the EP layer
+    xh = [torch.from_numpy(x).pin_memory() for x in xs]
+    ah = [torch.from_numpy(a).pin_memory() for a in asg]
+    dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        cur["l"] = i % L
+        y = ep.forward(xh[i % nb].to(dev, non_blocking=True), ah[i % nb].to(dev, non_blocking=True))
+        y.cpu()
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_sec = float(te.item())
+    eb = torch.tensor([float(sum(step_bytes(i) for i in range(args.steps)))], device=dev, dtype=torch.float64)
+    dist.all_reduce(eb)
+    e2e_bytes = float(eb.item())
     hbm_peak, peak_kind = peaks()
     if rank == 0:
+        per_gpu = tot / world / t_sec / 1e9
         print(json.dumps({
             "metric": METRIC, "value": tot / t_sec / 1e9, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_sec / args.steps, "higher_is_better": True,
@@ -616,9 +656,18 @@ def ep_main(args, world, rank, local):
             "data": "synthetic random-init weights, GPU RTN + bit-exact GPU encoder",
             "config": {"workload": args.workload, "experts": E, "experts_per_rank": E_loc, "d_model": d_model,
                        "d_ff": d_ff, "tokens_per_step_per_rank": T, "parallelism": f"ep{world}",
-                       "exchange": "NCCL all_to_all_single dispatch + combine"},
-            "tokens_per_s": T * world * args.steps / t_sec, "pct_peak": 100 * tot / t_sec / 1e9 / (hbm_peak * world),
-            "gpu_launches": (1 if fused else 3) * args.steps, "e2e": None, "cpu_baseline": None, "roofline": None,
+                       "exchange": "NCCL all_to_all_single dispatch + combine", "layer_pool_per_rank": L,
+                       "l2": "cold: rotating layers, pool >= 4x L2 per rank"},
+            "tokens_per_s": T * world * args.steps / t_sec, "pct_peak": 100 * per_gpu / hbm_peak,
+            "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": per_gpu / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "whole EP step per GPU (fused local step + NCCL exchange)"},
+            "e2e": {"value": e2e_bytes / e2e_sec / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": int(xs[0].nbytes + asg[0].nbytes),
+                    "d2h_bytes_per_step": int(T * d_model * 4), "tokens_per_s": T * world * args.steps / e2e_sec,
+                    "api": "ExpertParallelMoE.forward(host tokens + ids copied in, outputs copied out)"},
+            "gpu_launches": args.steps, "cpu_baseline": None,
+            "clocks": dict(cs.summary(), window="sustained EP steps (0.5 s) into the timed region"),
         }))
     dist.destroy_process_group()
 
