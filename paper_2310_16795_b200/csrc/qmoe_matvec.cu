@@ -942,120 +942,168 @@ __device__ __forceinline__ int block_excl_scan2(int v, int w, int& wtot, int2* w
   return wsum[warp].x + iv - v;
 }
 
+// Warp dispatcher plan by sorting (T <= 32 * NPL tokens, any E): the keys
+// (expert << 8 | token) of the valid tokens go through a warp bitonic sort
+// (NPL keys per lane, position p = lane * NPL + j), which IS the stable
+// expert-major token order (pipeline.py:86-90); segmented scans over the
+// sorted positions then give each token's index inside its expert, the runs
+// of <= ntu (1 or 2) tokens and their cost-weighted prefix. Nothing scales
+// with E (a c2048 layer has 2048 experts). Returns the run count; lane 0..31
+// all return it.
+template <int NPL>
+__device__ __forceinline__ int warp_plan_sort(const int32_t* __restrict__ assign, int T, int E, int ntu, int w2,
+                                              int* order, int* runs4, int* wpre, int* count_out, int32_t* order_out,
+                                              bool write_out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t k[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int t = lane * NPL + j;
+    const int e = t < T ? __ldg(assign + t) : -1;
+    k[j] = (t < T && e >= 0 && e < E) ? ((uint32_t)e << 8) | (uint32_t)t : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int kk = 2; kk <= 32 * NPL; kk <<= 1) {
+#pragma unroll
+    for (int jd = kk >> 1; jd > 0; jd >>= 1) {
+      if (jd < NPL) {
+#pragma unroll
+        for (int j = 0; j < NPL; ++j) {
+          const int pj = j ^ jd;
+          if (pj > j) {
+            const bool up = (((lane * NPL + j) & kk) == 0);
+            const uint32_t a = k[j], b = k[pj];
+            const bool sw = up ? (a > b) : (a < b);
+            k[j] = sw ? b : a;
+            k[pj] = sw ? a : b;
+          }
+        }
+      } else {
+        const int ld = jd / NPL;
+#pragma unroll
+        for (int j = 0; j < NPL; ++j) {
+          const uint32_t o = __shfl_xor_sync(FULL_MASK, k[j], ld);
+          const bool up = (((lane * NPL + j) & kk) == 0);
+          const bool lower = (lane & ld) == 0;
+          k[j] = (lower == up) ? min(k[j], o) : max(k[j], o);
+        }
+      }
+    }
+  }
+  // sorted: positions lane * NPL + j ascending; invalid keys (0xFFFFFFFF) last
+  const uint32_t prev_last = __shfl_up_sync(FULL_MASK, k[NPL - 1], 1);
+  const uint32_t next_first = __shfl_down_sync(FULL_MASK, k[0], 1);
+  int segmax = -1;  // running max of segment starts (lane-local, then carried)
+  int seg[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int p = lane * NPL + j;
+    const uint32_t pk = j ? k[j - 1] : (lane ? prev_last : 0xFFFFFFFFu);
+    const bool valid = k[j] != 0xFFFFFFFFu;
+    const bool f = valid && (p == 0 || (pk >> 8) != (k[j] >> 8));
+    if (f) segmax = p;
+    seg[j] = segmax;
+  }
+  int carry = segmax;  // inclusive max-scan over lanes, then shift to exclusive
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(FULL_MASK, carry, d);
+    if (lane >= d) carry = max(carry, o);
+  }
+  carry = __shfl_up_sync(FULL_MASK, carry, 1);
+  if (lane == 0) carry = -1;
+  int nrun = 0, wsum = 0;
+  bool rs[NPL];
+  int ntv[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int p = lane * NPL + j;
+    const bool valid = k[j] != 0xFFFFFFFFu;
+    const int q = p - max(seg[j], carry);
+    const uint32_t nk = j + 1 < NPL ? k[j + 1] : (lane < 31 ? next_first : 0xFFFFFFFFu);
+    rs[j] = valid && ((q & (ntu - 1)) == 0);
+    ntv[j] = (ntu > 1 && nk != 0xFFFFFFFFu && (nk >> 8) == (k[j] >> 8)) ? 2 : 1;
+    if (rs[j]) {
+      ++nrun;
+      wsum += ntv[j] > 1 ? w2 : 8;
+    }
+    if (valid) {
+      order[p] = (int)(k[j] & 0xFFu);
+      if (write_out) {
+        order_out[p] = (int)(k[j] & 0xFFu);
+        const bool seg_end = nk == 0xFFFFFFFFu || (nk >> 8) != (k[j] >> 8);
+        if (seg_end && count_out) count_out[k[j] >> 8] = q + 1;
+      }
+    }
+  }
+  int rinc = nrun, winc = wsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int a = __shfl_up_sync(FULL_MASK, rinc, d), b = __shfl_up_sync(FULL_MASK, winc, d);
+    if (lane >= d) {
+      rinc += a;
+      winc += b;
+    }
+  }
+  int ri = rinc - nrun, wp = winc - wsum;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    if (rs[j]) {
+      const uint32_t nk = j + 1 < NPL ? k[j + 1] : (lane < 31 ? next_first : 0xFFFFFFFFu);
+      runs4[4 * ri] = (int)(k[j] >> 8);
+      runs4[4 * ri + 1] = ntv[j];
+      runs4[4 * ri + 2] = (int)(k[j] & 0xFFu);
+      runs4[4 * ri + 3] = (int)((ntv[j] > 1 ? nk : k[j]) & 0xFFu);
+      wpre[ri] = wp;
+      ++ri;
+      wp += ntv[j] > 1 ? w2 : 8;
+    }
+  }
+  const int total = __shfl_sync(FULL_MASK, rinc, 31);
+  if (lane == 31) wpre[total] = winc;
+  return total;
+}
+
 __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   __shared__ PipeShared PS;
   __shared__ int2 wsum[NWARPS];
   __shared__ int tot[2];
   const int E = S.E, T = S.T, ntu = S.ntu;
-  int* cnt = reinterpret_cast<int*>(seg_smem + S.plan_off);  // E
-  int* start = cnt + E;                                        // E + 1
-  int* choff = start + E + 1;                                  // E + 1
-  int* order = choff + E + 1;                                  // T
-  int* runs4 = order + T;                                      // 4 T
-  int* wpre = runs4 + 4 * T;                                   // T + 1: weighted run prefix
+  // plan area: [cnt E | start E+1 | choff E+1] (block-scan plan only), then
+  // order T | runs4 4T | wpre T+1 (weighted run prefix)
+  const int ecells = T <= WARP_PLAN_MAX ? 0 : 3 * E + 2;
+  int* cnt = reinterpret_cast<int*>(seg_smem + S.plan_off);
+  int* start = cnt + E;
+  int* choff = start + E + 1;
+  int* order = cnt + ecells;
+  int* runs4 = order + T;
+  int* wpre = runs4 + 4 * T;
   const SegParams& PW = S.wi;
   __shared__ __align__(8) uint64_t tab_bar;
   trace_stamp(0);
   table_fill_async(PW.gtab, PW.H, &tab_bar);  // overlaps the plan below
   // ---- 1. plan
   bool wpre_ready = false;
+  __shared__ int s_nch;
   if (T <= WARP_PLAN_MAX) {
-    // one warp, no block barriers (the other warps wait once, below):
-    //  a. per-expert counts + each token's stable rank inside its expert
-    //     (chunks of 32 tokens in buffer order; match_any groups a chunk)
-    //  b. exclusive scans over experts (contiguous blocks per lane): token
-    //     start, run offset, weighted-run prefix
-    //  c. tokens placed in expert order, then each lane emits its experts'
-    //     runs {expert, ntok, tok0, tok1} and their weighted prefix
+    // one warp sorts the (expert, token) keys; no work proportional to E.
+    // Block 0 also publishes the plan (expert counts zeroed first).
+    if (blockIdx.x == 0 && S.count_out) {
+      for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = 0;
+      __syncthreads();
+    }
     if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      int* rank = runs4;  // scratch: token ranks (runs4 is written in c.)
-      for (int e = lane; e < E; e += 32) cnt[e] = 0;
-      int ids[WARP_PLAN_MAX / 32];
-#pragma unroll
-      for (int k = 0; k < WARP_PLAN_MAX / 32; ++k) {  // all loads in flight together
-        const int t = k * 32 + lane;
-        ids[k] = (k * 32 < T && t < T) ? __ldg(S.assign + t) : -1;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < WARP_PLAN_MAX / 32; ++k) {
-        if (k * 32 >= T) break;
-        const int t = k * 32 + lane, e = ids[k];
-        const bool ok = t < T && e >= 0 && e < E;
-        const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (ok && lane == leader) {
-          base = cnt[e];
-          cnt[e] = base + __popc(peers);
-        }
-        base = __shfl_sync(FULL_MASK, base, leader);
-        if (t < T) rank[t] = ok ? base + __popc(peers & ((1u << lane) - 1u)) : -1;
-        __syncwarp();
-      }
-      trace_stamp(4);
-      const int per = (E + 31) >> 5;
-      const int lgn = ntu > 1 ? 1 : 0;  // ntu is 1 or 2 (NT_STREAM): shifts, not divisions
-      const int e0 = min(E, lane * per), e1 = min(E, e0 + per);
-      const int wfull = ntu > 1 ? S.w2 : 8;
-      int sv = 0, sc = 0, sw = 0;
-      for (int e = e0; e < e1; ++e) {
-        const int c = cnt[e];
-        sv += c;
-        sc += (c + lgn) >> lgn;
-        sw += (c >> lgn) * wfull + ((c & lgn) ? 8 : 0);
-      }
-      int iv = sv, ic = sc, iw = sw;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int a = __shfl_up_sync(FULL_MASK, iv, d), b = __shfl_up_sync(FULL_MASK, ic, d),
-                  w = __shfl_up_sync(FULL_MASK, iw, d);
-        if (lane >= d) {
-          iv += a;
-          ic += b;
-          iw += w;
-        }
-      }
-      int bv = iv - sv, bc = ic - sc, bw = iw - sw;
-      for (int e = e0; e < e1; ++e) {
-        const int c = cnt[e];
-        start[e] = bv;
-        choff[e] = bc;
-        if (blockIdx.x == 0 && S.count_out) S.count_out[e] = c;
-        bv += c;
-        bc += (c + lgn) >> lgn;
-      }
-      if (lane == 31) {
-        start[E] = iv;
-        choff[E] = ic;
-        wpre[ic] = iw;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < WARP_PLAN_MAX / 32; ++k) {
-        if (k * 32 >= T) break;
-        const int t = k * 32 + lane;
-        if (t < T && rank[t] >= 0) order[start[ids[k]] + rank[t]] = t;
-      }
-      __syncwarp();
-      bc = ic - sc;
-      for (int e = e0; e < e1; ++e) {
-        const int c = cnt[e], s0 = start[e];
-        for (int ch = 0; ch * ntu < c; ++ch, ++bc) {
-          const int nt = min(ntu, c - ch * ntu);
-          runs4[4 * bc] = e;
-          runs4[4 * bc + 1] = nt;
-          runs4[4 * bc + 2] = order[s0 + ch * ntu];
-          runs4[4 * bc + 3] = order[s0 + ch * ntu + (nt > 1 ? 1 : 0)];
-          wpre[bc] = bw;
-          bw += nt > 1 ? S.w2 : 8;
-        }
-      }
-      __syncwarp();
-      const int placed = __shfl_sync(FULL_MASK, iv, 31);
-      if (blockIdx.x == 0 && S.order_out)
-        for (int t = lane; t < placed; t += 32) S.order_out[t] = order[t];
+      const bool wo = blockIdx.x == 0;
+      int n;
+      if (T <= 32)
+        n = warp_plan_sort<1>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+      else if (T <= 64)
+        n = warp_plan_sort<2>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+      else if (T <= 128)
+        n = warp_plan_sort<4>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+      else
+        n = warp_plan_sort<8>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+      if (threadIdx.x == 0) s_nch = n;
     }
     wpre_ready = true;
   } else {
@@ -1136,7 +1184,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   }
   __syncthreads();
   trace_stamp(7);
-  const int nch = choff[E];
+  const int nch = wpre_ready ? s_nch : choff[E];
   // cost-weighted split of the run list over the CTAs: a 2-token run decodes
   // once but gathers and accumulates twice (~1.4x a 1-token run, measured)
   __shared__ int s_split[4];
@@ -1550,7 +1598,9 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   const int maxc = std::max(d_model, d_ff);
   const size_t slot = (size_t)2 * 4 * (((maxc + 32) + 3) & ~3);
   const size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
-  const size_t plan = ((size_t)(3 * E + 3 + 6 * (size_t)T) * 4 + 15) & ~(size_t)15;
+  // the single-warp plan (T <= WARP_PLAN_MAX) needs no per-expert arrays
+  const size_t ecells = T <= WARP_PLAN_MAX ? 0 : (size_t)3 * E + 2;
+  const size_t plan = ((ecells + 1 + 6 * (size_t)T) * 4 + 15) & ~(size_t)15;
   const size_t static_smem = 2048;
   if (xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
     return qmoe::fail(QMOE_EUNSUPPORTED, "step too large for the fused kernel's shared memory (use the grouped path)");
