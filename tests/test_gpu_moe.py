@@ -232,7 +232,7 @@ def _random_layer(dic, rng, E, d_model, d_ff, max_tokens):
     return wi, wo, host
 
 
-@pytest.mark.parametrize("T", [5, 48])
+@pytest.mark.parametrize("T", [5, 48, 100, 200, 300])
 def test_fused_step_equals_grouped_passes_and_plan(dic, T):
     """The single-launch step (qmoe_moe_step) runs the same decode with the same
     lanes as the plan kernel + two grouped passes: outputs must be bit-identical,
@@ -245,10 +245,10 @@ def test_fused_step_equals_grouped_passes_and_plan(dic, T):
     layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
     assert layer.fused
     x = torch.from_numpy(q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))).cuda().to(torch.bfloat16)
-    a_np = rng.integers(-1, E, size=T).astype(np.int32)  # -1: no expert (dropped)
+    a_np = rng.integers(-1, E + 1, size=T).astype(np.int32)  # -1 and E: no expert (dropped)
     a = torch.from_numpy(a_np).cuda()
     y_fused = layer.forward_device(x, a).clone()
-    ok = a_np >= 0
+    ok = (a_np >= 0) & (a_np < E)
     order = np.argsort(np.where(ok, a_np, E), kind="stable")[: ok.sum()]
     assert np.array_equal(layer.order[: ok.sum()].cpu().numpy(), order)
     assert np.array_equal(layer.expert_count.cpu().numpy(), np.bincount(a_np[ok], minlength=E))
@@ -287,3 +287,31 @@ def test_packed_layout_matches_oracle(dic, odic):
     d = bf16_ulp_diff(y, y_ref)
     assert d.max() <= 2
     assert np.mean(d == 0) >= 0.99
+
+
+def test_fused_plan_many_experts(dic):
+    """The fused step's warp plan sorts (expert, token) keys: with hundreds of
+    experts (nothing in it scales with E) the stable order, counts and outputs
+    still match the grouped path."""
+    import os
+
+    rng = np.random.default_rng(77)
+    E, d_model, d_ff, T = 600, 64, 128, 160
+    wi, wo, _ = _random_layer(dic, rng, E, d_model, d_ff, T)
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+    assert layer.fused
+    x = torch.from_numpy(q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))).cuda().to(torch.bfloat16)
+    a_np = np.where(rng.random(T) < 0.5, rng.integers(0, 8, size=T), rng.integers(-2, E + 2, size=T)).astype(np.int32)
+    a = torch.from_numpy(a_np).cuda()
+    y_fused = layer.forward_device(x, a).clone()
+    ok = (a_np >= 0) & (a_np < E)
+    order = np.argsort(np.where(ok, a_np, E), kind="stable")[: ok.sum()]
+    assert np.array_equal(layer.order[: ok.sum()].cpu().numpy(), order)
+    assert np.array_equal(layer.expert_count.cpu().numpy(), np.bincount(a_np[ok], minlength=E))
+    os.environ["QMOE_FUSED"] = "0"
+    try:
+        layer2 = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+        y_grouped = layer2.forward_device(x, a)
+    finally:
+        os.environ.pop("QMOE_FUSED")
+    assert torch.equal(y_fused[ok], y_grouped[ok])
