@@ -750,7 +750,7 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
     // shape: rows per item (= threads) x columns per chunk x CTAs per SM; the
     // hot table gets the rest of shared memory (its hit rate matters: the
     // codeword ranks are spread, 16K entries cover ~80%, 32K ~91%)
-    int RWR = 256, RWK = 64, RWB = 2;
+    int RWR = 128, RWK = 64, RWB = 4;
     if (const char* sh = getenv("QMOE_DENSE_RW")) sscanf(sh, "%dx%dx%d", &RWR, &RWK, &RWB);
     const size_t wbytes = (size_t)RWR * RWK * 2 + 1024, xbytes = (size_t)(RWK / 64) * BN * 128;
     const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
@@ -778,12 +778,16 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
       else if (is(512, 128, 1)) QMOE_RW_LAUNCH(64, 512, 128, 1);
       else if (is(256, 128, 2)) QMOE_RW_LAUNCH(64, 256, 128, 2);
       else if (is(256, 64, 2)) QMOE_RW_LAUNCH(64, 256, 64, 2);
+      else if (is(256, 64, 3)) QMOE_RW_LAUNCH(64, 256, 64, 3);
+      else if (is(128, 64, 4)) QMOE_RW_LAUNCH(64, 128, 64, 4);
       else return qmoe::fail(QMOE_EINVAL, "QMOE_DENSE_RW: unknown shape");
     } else {
       if (is(512, 64, 1)) QMOE_RW_LAUNCH(32, 512, 64, 1);
       else if (is(512, 128, 1)) QMOE_RW_LAUNCH(32, 512, 128, 1);
       else if (is(256, 128, 2)) QMOE_RW_LAUNCH(32, 256, 128, 2);
       else if (is(256, 64, 2)) QMOE_RW_LAUNCH(32, 256, 64, 2);
+      else if (is(256, 64, 3)) QMOE_RW_LAUNCH(32, 256, 64, 3);
+      else if (is(128, 64, 4)) QMOE_RW_LAUNCH(32, 128, 64, 4);
       else return qmoe::fail(QMOE_EINVAL, "QMOE_DENSE_RW: unknown shape");
     }
 #undef QMOE_RW_LAUNCH
