@@ -556,28 +556,34 @@ __global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) 
       whi = mm >> 16;
     }
     if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
-    // my row's codeword stream: groups of 8 (16 bytes), three in flight, and
-    // the entries of the next 4 codewords (looked up 4 codewords ahead)
+    // my row's codeword stream in groups of 8 (16-byte loads, two groups
+    // ahead). A group is looked up at once (8 independent lookups) and its
+    // codewords' start columns prefix-summed once; every chunk the group
+    // overlaps then writes its values in that chunk — no per-codeword
+    // dependence chain, and rows advance group by group in step.
     const int glast = n > 0 ? (s + n - 1) >> 3 : (s >> 3);
     int g = s >> 3;
-    uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = q0, q2 = q0;
-    if (n > 0) {
-      q0 = ld_group_nc(cwp, g);
+    uint4 q1 = make_uint4(0u, 0u, 0u, 0u), q2 = q1;
+    uint32_t ge[8];
+    int gc[9];  // start column of slot u; gc[8] = end of the group
+    bool more = n > 0;
+    auto open_group = [&](const uint4& q, int gstart_col) {
+      const int base = g * 8;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool in = base + u >= s && base + u < s + n;
+        ge[u] = in ? lookup_pred(group_cw(q, (uint32_t)u), tab_s, H, P.gtab) : 0x007F7F7Fu;  // no value, len 0
+      }
+      gc[0] = gstart_col;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) gc[u + 1] = gc[u] + (int)(ge[u] >> 28) * 2;
+    };
+    if (more) {
+      const uint4 q0 = ld_group_nc(cwp, g);
       q1 = ld_group_nc(cwp, min(g + 1, glast));
       q2 = ld_group_nc(cwp, min(g + 2, glast));
+      open_group(q0, 0);
     }
-    int p = s;  // global index of my next codeword
-    auto cw_at = [&](int idx) -> uint32_t {  // idx within groups g, g + 1
-      return (idx >> 3) == g ? group_cw(q0, (uint32_t)idx & 7u) : group_cw(q1, (uint32_t)idx & 7u);
-    };
-    uint32_t e0 = 0u, e1 = 0u, e2 = 0u, e3 = 0u;
-    if (n > 0) {
-      e0 = lookup_pred(cw_at(p), tab_s, H, P.gtab);
-      e1 = lookup_pred(cw_at(p + 1), tab_s, H, P.gtab);
-      e2 = lookup_pred(cw_at(p + 2), tab_s, H, P.gtab);
-      e3 = lookup_pred(cw_at(p + 3), tab_s, H, P.gtab);
-    }
-    int i = 0, c = 0;  // my next codeword (row-relative), its start column
     __syncthreads();   // s_tok
     uint4 xr[XV];
     auto load_x = [&](int k0) {
@@ -610,33 +616,31 @@ __global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) 
 #pragma unroll
         for (int c16 = 0; c16 < 8; ++c16)
           sts_zero16(wrow + (uint32_t)kb * (RW_ROWS * 128u) + 16u * (uint32_t)((c16 + lane) & 7));
-      // walk: codewords starting left of the chunk end
+      // groups overlapping this chunk: write their values that fall in it
       const int kend = k0 + RW_KC;
-      while (i < n && c < kend) {
-        const uint32_t en = e0;
+      while (more && gc[0] < kend) {
 #pragma unroll
-        for (int jj = 0; jj < 3; ++jj) {
-          const uint32_t f = __byte_perm(en, 0u, 0x4440u + jj);
-          const int vk = c + (int)(f >> 2) - k0;
-          if (f != 0x7Fu && (unsigned)vk < (unsigned)RW_KC)
-            sts_u16(wrow + (uint32_t)(vk >> 6) * (RW_ROWS * 128u) + ((((uint32_t)vk & 63u) * 2u) ^ rx),
-                    ((en >> (24 + jj)) & 1u) ? whi : wlo);
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t en = ge[u];
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) {
+            const uint32_t f = __byte_perm(en, 0u, 0x4440u + jj);
+            const int vk = gc[u] + (int)(f >> 2) - k0;
+            if (f != 0x7Fu && (unsigned)vk < (unsigned)RW_KC)
+              sts_u16(wrow + (uint32_t)(vk >> 6) * (RW_ROWS * 128u) + ((((uint32_t)vk & 63u) * 2u) ^ rx),
+                      ((en >> (24 + jj)) & 1u) ? whi : wlo);
+          }
         }
-        const int nl = (int)(en >> 28) * 2;
-        if (c + nl > kend) break;  // straddles into the next chunk: revisit there
-        c += nl;
-        ++i;
-        ++p;
-        e0 = e1;
-        e1 = e2;
-        e2 = e3;
-        if ((p & 7) == 0) {
-          ++g;
-          q0 = q1;
-          q1 = q2;
-          q2 = ld_group_nc(cwp, min(g + 2, glast));
+        if (gc[8] > kend) break;  // the group continues in the next chunk
+        if (g >= glast) {
+          more = false;
+          break;
         }
-        e3 = lookup_pred(cw_at(p + 3), tab_s, H, P.gtab);
+        ++g;
+        const uint4 q0 = q1;
+        q1 = q2;
+        q2 = ld_group_nc(cwp, min(g + 2, glast));
+        open_group(q0, gc[8]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
