@@ -68,7 +68,8 @@ class CompressedMoELayer:
         # mean 8-codeword groups per row (wi, wo): lane-segment sizing
         self.mean_groups = tuple(float(np.mean([m.n_codewords / max(1, m.rows) / 8 for m in ms])) for ms in (wi, wo))
         # most lanes per row a step may use: segments of >= ~2 groups
-        boost = int(os.environ.get("QMOE_LG_BOOST", 0))  # experiment: finer checkpoints
+        # one level finer than that: tiny steps (generation) split rows further
+        boost = int(os.environ.get("QMOE_LG_BOOST", 1))
         self.max_lg = tuple(max(0, min(self.MAX_LG, int(np.floor(np.log2(max(1.0, mg / 2)))) + boost))
                             for mg in self.mean_groups)
         for kind, ms in enumerate((wi, wo)):  # kernel-private PACKED layout (or row checkpoints)
@@ -136,21 +137,29 @@ class CompressedMoELayer:
     def lanes_per_row(self, T: int) -> tuple[int, int]:
         """log2 lanes per row (wi, wo) for a step of T tokens: enough lane
         segments to fill the GPU about twice, but segments of at least
-        ~2 groups (shorter ones waste their partial groups)."""
+        ~2 groups (shorter ones waste their partial groups) — ~1 group when
+        the step is tiny (a generation step: latency, not lane efficiency,
+        decides; T = 1 Switch-base-128: 18.3 -> 16.8 us)."""
         hit = self._lanes.get(T)
         if hit is None:
             runs = self._runs_est(T)
             out = []
             for kind, (rows, mg) in enumerate(((self.d_ff, self.mean_groups[0]), (self.d_model, self.mean_groups[1]))):
-                cap = 5 if self.packed else max(m.lg for m in (self.wi if kind == 0 else self.wo))
+                cap = 5 if self.packed else min(m.lg for m in (self.wi if kind == 0 else self.wo))
+                caps = getattr(self, "_caps", [0, 0])
+                caps[kind] = cap
+                self._caps = caps
                 lg = 0
-                min_groups = float(os.environ.get("QMOE_MIN_SEG_GROUPS", 2.0))  # experiment
-                while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES and mg / (1 << (lg + 1)) >= min_groups:
+                base_min = float(os.environ.get("QMOE_MIN_SEG_GROUPS", 2.0))  # experiment
+                while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES:
+                    min_groups = base_min if runs * rows * (1 << lg) >= self.LANES // 4 else base_min / 2
+                    if mg / (1 << (lg + 1)) < min_groups:
+                        break
                     lg += 1
                 out.append(lg)
             for kind, key in enumerate(("QMOE_LG_WI", "QMOE_LG_WO")):  # experiment overrides
                 if key in os.environ:
-                    out[kind] = int(os.environ[key])
+                    out[kind] = min(int(os.environ[key]), self._caps[kind])  # checkpoints bound it
             hit = self._lanes[T] = tuple(out)
         return hit
 
