@@ -212,7 +212,7 @@ int qmoe_remap(const uint16_t* d_in, int64_t n, const uint16_t* d_rank_of, uint1
                void* stream);
 
 /* Row-segment checkpoints for a matrix (kernel-private, derived once): for
- * G = 2^lg (1 <= lg <= 3) segments per row, d_ck[r*(G-1) + j-1] = column where
+ * G = 2^lg (1 <= lg <= 5) segments per row, d_ck[r*(G-1) + j-1] = column where
  * segment j of row r starts. d_table selects the entry order the stream is
  * indexed in (NULL = dictionary). Rows that do not decode to cols values are
  * counted in d_bad (int32[2], as qmoe_validate_rows). */

@@ -842,8 +842,8 @@ int qmoe_remap(const uint16_t* d_in, int64_t n, const uint16_t* d_rank_of, uint1
 
 int qmoe_checkpoints(qmoe_dict_t d, const uint32_t* d_table, const uint16_t* d_cw, const int32_t* d_row_off,
                      int64_t rows, int64_t cols, int lg, uint16_t* d_ck, int32_t* d_bad, void* stream) {
-  if (bad_dict(d) || rows < 0 || cols < 0 || cols > 65535 || lg < 1 || lg > 3 || !d_ck)
-    return qmoe::fail(QMOE_EINVAL, "bad argument (1 <= lg <= 3, cols <= 65535)");
+  if (bad_dict(d) || rows < 0 || cols < 0 || cols > 65535 || lg < 1 || lg > 5 || !d_ck)
+    return qmoe::fail(QMOE_EINVAL, "bad argument (1 <= lg <= 5, cols <= 65535)");
   if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "checkpoints need a <=3-non-zero dictionary");
   if (rows == 0) return QMOE_OK;
   checkpoints_kernel<<<(int)((rows + 127) / 128), 128, 0, S(stream)>>>(d_table ? d_table : d->d_mtab, d_cw,

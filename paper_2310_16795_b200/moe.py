@@ -128,7 +128,7 @@ class CompressedMoELayer:
 
     # ------------------------------------------------------------------ device step
     LANES = 148 * 768  # resident lanes of the streaming kernel on a B200 (1 CTA x 24 warps per SM)
-    MAX_LG = 3  # RAW layout: checkpoints stored for 8 lanes per row (any 1/2/4/8 usable)
+    MAX_LG = 3  # RAW layout: checkpoints stored for up to 8 lanes per row (16 measured no faster)
 
     def _runs_est(self, T: int) -> float:
         """expected distinct experts of a step under uniform top-1 routing"""
