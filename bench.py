@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--pool-factor", type=float, default=4.0, help="layer pool size in multiples of L2")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
+    p.add_argument("--force-ep", action="store_true", help="run the expert-parallel path even at 1 rank (testing)")
     return p.parse_args()
 
 
@@ -322,7 +323,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.force_ep:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return ep_main(args, world, rank, local)
     dev = torch.device("cuda", local)
@@ -617,20 +618,49 @@ def ep_main(args, world, rank, local):
         step(i)
     torch.cuda.synchronize()
     dist.barrier()
+    # the EP step is device-only (fixed-slot exchange): capture each (layer,
+    # batch) step — fused local step + NCCL all-to-alls — in a CUDA graph;
+    # eager if the capture is refused
+    nsg = L * nb // int(np.gcd(L, nb))
+    graphs, graph_note = [], "cuda graph per step (NCCL all-to-alls captured)"
+    try:
+        for i in range(nsg):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(i)
+            graphs.append(g)
+        torch.cuda.synchronize()
+        dist.barrier()
+    except Exception as exc:  # noqa: BLE001 - report and run eager
+        graphs, graph_note = [], f"eager (capture refused: {type(exc).__name__})"
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    def run(i):
+        if graphs:
+            cur["l"] = i % L
+            graphs[i % nsg].replay()
+        else:
+            step(i)
+
+    for i in range(args.warmup):
+        run(i)
+    torch.cuda.synchronize()
+    dist.barrier()
     my_bytes = float(sum(step_bytes(args.warmup + i) for i in range(args.steps)))
     cs = ClockSampler(local)
     cs.__enter__()
     t_end = time.time() + 0.5
     while time.time() < t_end:  # sustained steps into the timed region (clock sampling window)
         for i in range(8):
-            step(i)
+            run(i)
         torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        step(args.warmup + i)
+        run(args.warmup + i)
     e1.record()
     torch.cuda.synchronize()
     cs.__exit__()
@@ -665,7 +695,8 @@ def ep_main(args, world, rank, local):
             "data": "synthetic random-init weights, GPU RTN + bit-exact GPU encoder",
             "config": {"workload": args.workload, "experts": E, "experts_per_rank": E_loc, "d_model": d_model,
                        "d_ff": d_ff, "tokens_per_step_per_rank": T, "parallelism": f"ep{world}",
-                       "exchange": "NCCL all_to_all_single dispatch + combine", "layer_pool_per_rank": L,
+                       "exchange": "NCCL all_to_all_single dispatch + combine (fixed slots, no host sync)",
+                       "launch": graph_note, "layer_pool_per_rank": L,
                        "l2": "cold: rotating layers, pool >= 4x L2 per rank"},
             "tokens_per_s": T * world * args.steps / t_sec, "pct_peak": 100 * per_gpu / hbm_peak,
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": hbm_peak, "unit": "GB/s",

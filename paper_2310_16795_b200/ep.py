@@ -7,11 +7,17 @@ dictionary / codebook). One forward, per rank, for that rank's T local tokens:
   1. route   top-1 expert ids (host RouterSim or GPU router) -> destination
              rank = id // (E / P); tokens are grouped by destination rank,
              stable in buffer order;
-  2. dispatch  all_to_all_single of the token rows (+ their expert ids) —
-             NCCL over NVLink on B200 boxes, gloo on CPU for the tests;
-  3. compute   the local CompressedMoELayer on the received tokens (expert
-             ids rebased to the local block);
-  4. combine   all_to_all_single of the outputs back, scattered to the
+  2. dispatch  all_to_all_single of the token rows (+ their expert ids) into
+             fixed slots: every rank reserves T slots per destination
+             (a token's slot = its stable rank among the tokens going to the
+             same rank), empty slots carry expert id -1. Equal splits mean
+             no host round trip for the counts, so the whole layer is
+             device-only and CUDA-graph capturable — NCCL over NVLink on
+             B200 boxes, gloo on CPU for the tests;
+  3. compute   the local CompressedMoELayer on the received W x T slots
+             (expert ids rebased to the local block; -1 slots are dropped by
+             its dispatcher plan);
+  4. combine   all_to_all_single of the slot outputs back, gathered to the
              tokens' original positions.
 
 Per-token arithmetic never depends on placement, so outputs are bit-identical
@@ -48,33 +54,34 @@ class ExpertParallelMoE:
         return expert_ids // self.per_rank
 
     def forward(self, x, assign):
-        """x: (T, d) tensor, assign: (T,) int32 tensor of global expert ids.
-        Returns y (T, d_out) float32 in the original token order."""
+        """x: (T, d) tensor, assign: (T,) int32 tensor of global expert ids
+        (ids outside [0, E) get no expert: zero output rows). Returns y
+        (T, d_out) float32 in the original token order."""
         import torch
 
         dist = self.dist
-        T = x.shape[0]
-        dest = (assign.to(torch.int64) // self.per_rank).to(torch.int64)
-        order = torch.argsort(dest, stable=True)  # group by destination, buffer order kept
-        send_counts = torch.bincount(dest, minlength=self.world).to(torch.int64)
-        recv_counts = torch.empty_like(send_counts)
-        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
-        sc = send_counts.cpu().tolist()
-        rc = recv_counts.cpu().tolist()
-        self.last_split = (sc, rc)
-        x_send = x[order].contiguous()
-        id_send = assign[order].to(torch.int32).contiguous()
-        n_recv = int(sum(rc))
-        x_recv = torch.empty((n_recv, x.shape[1]), dtype=x.dtype, device=x.device)
-        id_recv = torch.empty(n_recv, dtype=torch.int32, device=x.device)
-        dist.all_to_all_single(x_recv, x_send, rc, sc, group=self.group)
-        dist.all_to_all_single(id_recv, id_send, rc, sc, group=self.group)
-        local_ids = id_recv - self.rank * self.per_rank
-        y_recv = self.local_fn(x_recv, local_ids).to(torch.float32).contiguous()
-        y_send = torch.empty((T, y_recv.shape[1]), dtype=torch.float32, device=x.device)
-        dist.all_to_all_single(y_send, y_recv, sc, rc, group=self.group)
-        y = torch.empty_like(y_send)
-        y[order] = y_send
+        T, W = x.shape[0], self.world
+        a64 = assign.to(torch.int64)
+        valid = (a64 >= 0) & (a64 < self.E)
+        dest = torch.where(valid, a64 // self.per_rank, torch.zeros_like(a64))
+        onehot = torch.nn.functional.one_hot(dest, W) * valid[:, None].to(torch.int64)
+        pos = (torch.cumsum(onehot, 0) - onehot).gather(1, dest[:, None])[:, 0]  # stable rank per destination
+        slot = torch.where(valid, dest * T + pos, torch.full_like(dest, W * T))  # W*T: a spill slot for invalid
+        x_send = torch.zeros((W * T + 1, x.shape[1]), dtype=x.dtype, device=x.device)
+        id_send = torch.full((W * T + 1,), -1, dtype=torch.int32, device=x.device)
+        x_send[slot] = x
+        id_send[slot] = torch.where(valid, a64 - dest * self.per_rank, torch.full_like(a64, -1)).to(torch.int32)
+        x_send, id_send = x_send[: W * T], id_send[: W * T]
+        self.last_split = (onehot.sum(0), None)  # tokens sent to each rank (device tensor)
+        x_recv = torch.empty_like(x_send)
+        id_recv = torch.empty_like(id_send)
+        dist.all_to_all_single(x_recv, x_send, group=self.group)
+        dist.all_to_all_single(id_recv, id_send, group=self.group)
+        y_recv = self.local_fn(x_recv, id_recv).to(torch.float32).contiguous()
+        y_back = torch.empty_like(y_recv)
+        dist.all_to_all_single(y_back, y_recv, group=self.group)
+        y_back = torch.cat([y_back, torch.zeros((1, y_back.shape[1]), dtype=y_back.dtype, device=y_back.device)])
+        y = y_back[slot]  # invalid tokens read the zero spill row
         return y
 
 
