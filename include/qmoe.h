@@ -336,6 +336,20 @@ int qmoe_route(int rule, const void* d_x, int x_dtype, int64_t ldx, int32_t T, i
                const double* d_proj, const double* d_bias, const uint64_t* d_mult, double* d_scores,
                int32_t* d_assign, float* d_gate, void* stream);
 
+/* Expert-parallel exchange helpers (ep.ExpertParallelMoE):
+ * fixed-slot dispatch. Token t with expert id a in [0, E) goes to rank
+ * d = a / (E / world), slot d * T + its stable rank among the tokens bound for
+ * d (buffer order, pipeline.py:86-90): d_slot[t] (-1: no expert),
+ * d_id_send[world * T] = rank-local expert id per slot (-1: empty slot),
+ * d_send_counts[world] (nullable) = tokens per destination. world <= 64. */
+int qmoe_ep_slots(const int32_t* d_assign, int32_t T, int32_t E, int32_t world, int32_t* d_slot,
+                  int32_t* d_id_send, int32_t* d_send_counts, void* stream);
+/* Row moves by an index (rows of row_bytes, 16-byte aligned): scatter = 1:
+ * dst[index[i]] = src[i] (index -1 skipped); scatter = 0: dst[i] =
+ * src[index[i]] (index -1: zero row). */
+int qmoe_ep_rows(const void* d_src, void* d_dst, int32_t n_rows, int64_t row_bytes, const int32_t* d_index,
+                 int scatter, void* stream);
+
 /* Batched-token decode-then-MMA pass (many tokens per expert, e.g.
  * Switch-large-128 with T in the thousands): for every expert e with tokens
  * d_order[start_e .. start_e + d_expert_count[e]) (qmoe_moe_plan's outputs,

@@ -86,6 +86,8 @@ _SIGS = {
     "qmoe_moe_step_gated": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, ctypes.c_int, i64,
                                            vp, i64, vp, i64, vp, vp, vp, i32, vp, vp]),
     "qmoe_route_scratch": (i64, [i32, i32, i32]),
+    "qmoe_ep_slots": (ctypes.c_int, [vp, i32, i32, i32, vp, vp, vp, vp]),
+    "qmoe_ep_rows": (ctypes.c_int, [vp, vp, i32, i64, vp, ctypes.c_int, vp]),
     "qmoe_route": (ctypes.c_int, [ctypes.c_int, vp, ctypes.c_int, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "qmoe_debug_step_trace": (ctypes.c_int, [vp]),
     "qmoe_debug_empty_launch": (ctypes.c_int, [i32, i32, vp]),

@@ -61,6 +61,8 @@ class ExpertParallelMoE:
 
         dist = self.dist
         T, W = x.shape[0], self.world
+        if x.is_cuda and W <= 64 and (x.shape[1] * x.element_size()) % 16 == 0:
+            return self._forward_device(x, assign)
         a64 = assign.to(torch.int64)
         valid = (a64 >= 0) & (a64 < self.E)
         dest = torch.where(valid, a64 // self.per_rank, torch.zeros_like(a64))
@@ -82,6 +84,39 @@ class ExpertParallelMoE:
         dist.all_to_all_single(y_back, y_recv, group=self.group)
         y_back = torch.cat([y_back, torch.zeros((1, y_back.shape[1]), dtype=y_back.dtype, device=y_back.device)])
         y = y_back[slot]  # invalid tokens read the zero spill row
+        return y
+
+
+    def _forward_device(self, x, assign):
+        """CUDA path of forward: slots + row scatter / gather as two small
+        library kernels (qmoe_ep_slots, qmoe_ep_rows) around the NCCL
+        all-to-alls — device-only, graph-capturable."""
+        import torch
+
+        from . import _lib
+
+        dist = self.dist
+        T, W, d = x.shape[0], self.world, x.shape[1]
+        x = x.contiguous()
+        a = assign.to(torch.int32).contiguous()
+        slot = torch.empty(T, dtype=torch.int32, device=x.device)
+        id_send = torch.empty(W * T, dtype=torch.int32, device=x.device)
+        counts = torch.empty(W, dtype=torch.int32, device=x.device)
+        x_send = torch.empty((W * T, d), dtype=x.dtype, device=x.device)
+        s = _lib.stream_ptr()
+        _lib.check(_lib.lib.qmoe_ep_slots(_lib.ptr(a), T, self.E, W, _lib.ptr(slot), _lib.ptr(id_send),
+                                          _lib.ptr(counts), s))
+        _lib.check(_lib.lib.qmoe_ep_rows(_lib.ptr(x), _lib.ptr(x_send), T, d * x.element_size(), _lib.ptr(slot), 1, s))
+        self.last_split = (counts, None)
+        x_recv = torch.empty_like(x_send)
+        id_recv = torch.empty_like(id_send)
+        dist.all_to_all_single(x_recv, x_send, group=self.group)
+        dist.all_to_all_single(id_recv, id_send, group=self.group)
+        y_recv = self.local_fn(x_recv, id_recv).to(torch.float32).contiguous()
+        y_back = torch.empty_like(y_recv)
+        dist.all_to_all_single(y_back, y_recv, group=self.group)
+        y = torch.empty((T, y_back.shape[1]), dtype=torch.float32, device=x.device)
+        _lib.check(_lib.lib.qmoe_ep_rows(_lib.ptr(y_back), _lib.ptr(y), T, y_back.shape[1] * 4, _lib.ptr(slot), 0, s))
         return y
 
 
