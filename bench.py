@@ -582,7 +582,7 @@ def ep_main(args, world, rank, local):
                           max_tokens=T * world)
         layers.append(lay)
         pool += int(lay.expert_bytes.sum())
-        if len(layers) >= 16:
+        if len(layers) >= 96:  # each rank holds E / N experts per layer: more layers for a cold L2
             break
     L = len(layers)
     router = q.RouterSim(E, rule="argmax", seed=0)
