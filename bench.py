@@ -635,6 +635,10 @@ def ep_main(args, world, rank, local):
         graphs, graph_note = [], f"eager (capture refused: {type(exc).__name__})"
         torch.cuda.synchronize()
         dist.barrier()
+    ok = torch.tensor([1 if graphs else 0], device=dev, dtype=torch.int32)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank replays graphs, or none does
+    if not int(ok.item()) and graphs:
+        graphs, graph_note = [], "eager (another rank could not capture)"
 
     def run(i):
         if graphs:
