@@ -323,3 +323,36 @@ def test_c2048_shapes_round_trip_and_matvec(dic, odic, rows, cols):
     lv = O.levels(mmh)
     dense = np.take_along_axis(lv, h_codes.astype(np.intp), axis=1)
     assert_matvec_close(y.cpu().numpy(), y_ref, dense, x)
+
+
+def test_acceptance_c05_round_trip_1000(dic, odic):
+    """The reference's acceptance criterion 05 (test_acceptance.py:125-135),
+    same generator and seed, so the same 1000 matrices: GPU encode ->
+    GPU decompress is the identity; the GPU stream equals the oracle encoder's
+    on every 10th case."""
+    rng = np.random.default_rng(500)
+    for i in range(1000):
+        rows = int(rng.integers(1, 258))
+        cols = 2 * int(rng.integers(1, 514))
+        p0 = float(rng.choice([0.0, 0.3, 0.6, 0.885, 0.99, 1.0]))
+        t = make_ternary(random_codes(rng, rows, cols, p0))
+        c = q.encode(t, dic)
+        assert np.array_equal(q.decompress(c, dic).codes, t.codes), f"random case {i} failed"
+        if i % 10 == 0:
+            cw, ro = O.encode_codes(t.codes, odic)
+            assert np.array_equal(c.codewords, cw) and np.array_equal(c.row_off, ro), f"case {i} stream"
+
+
+def test_acceptance_c01_c02_iid_rate(dic):
+    """The reference's acceptance criteria 01-02 (test_acceptance.py:50-70):
+    theoretical limit 25.40 and the i.i.d. 4096 x 16384 (p0 = 0.885, seed 1234)
+    rate in [20.5, 21.7] — with the GPU encoder the stream is the reference's
+    own: 3,088,944 codewords, rate 21.610863901743134 (computed with the
+    reference package in the build container)."""
+    assert abs(q.theoretical_limit(0.885) - 25.40) <= 0.01
+    t = q.sample_ternary(q.PairDistribution(0.885), 4096, 16384, seed=1234)
+    c = q.encode(t, dic)
+    assert len(c.codewords) == 3_088_944
+    rate = q.compression_rate(c).moe_only_rate
+    assert rate == 21.610863901743134
+    assert 20.5 <= rate <= 21.7 and rate < q.theoretical_limit(0.885)
