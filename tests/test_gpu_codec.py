@@ -356,3 +356,58 @@ def test_acceptance_c01_c02_iid_rate(dic):
     rate = q.compression_rate(c).moe_only_rate
     assert rate == 21.610863901743134
     assert 20.5 <= rate <= 21.7 and rate < q.theoretical_limit(0.885)
+
+
+def test_acceptance_c04_natural_sparsity():
+    """Acceptance criterion 04 (test_acceptance.py:101-122): RTN sparsity of
+    Gaussian matrices in [0.60, 0.95], increasing with width; the sampler
+    reproduces p0 within 0.001."""
+    sp = []
+    for width in (64, 256, 1024, 4096):
+        w = np.random.default_rng(100 + width).normal(size=(64, width))
+        sp.append(q.natural_sparsity(q.rtn_quantize(w, q.make_grid(w.astype(np.float32)))))
+    assert all(0.60 <= s <= 0.95 for s in sp) and all(a < b for a, b in zip(sp, sp[1:]))
+    t = q.sample_ternary(q.PairDistribution(0.885), 1000, 1000, seed=77)
+    assert abs(q.natural_sparsity(t) - 0.885) <= 0.001
+
+
+def test_acceptance_c07_fused_kernel_fidelity(dic):
+    """Acceptance criterion 07 (test_acceptance.py:229-262), same generator:
+    the GPU fused matvec within 1e-2 of the float64 dense product on the same
+    100 random shapes, and the lane replay equals decompress with lanes
+    28..31 idle."""
+    rng = np.random.default_rng(700)
+    worst = 0.0
+    for _ in range(100):
+        rows = int(rng.integers(1, 65))
+        cols = 2 * int(rng.integers(1, 65))
+        t = make_ternary(random_codes(rng, rows, cols, float(rng.choice([0.6, 0.885, 0.97]))))
+        c = q.encode(t, dic)
+        x = (rng.normal(size=cols) / np.sqrt(cols)).astype(np.float32)
+        y = q.fused_matvec(c, x, dic)
+        dense = t.dequant().astype(np.float64) @ x.astype(np.float64)
+        worst = max(worst, float(np.max(np.abs(y - dense))))
+    assert worst <= 1e-2
+    for _ in range(8):
+        t = make_ternary(random_codes(rng, int(rng.integers(1, 33)), 56, 0.885))
+        c = q.encode(t, dic)
+        codes = q.decompress(c, dic).codes
+        for r in range(t.rows):
+            trace = q.simulate_warp_row(c, r, dic)
+            assert np.array_equal(trace.extracted_values(), codes[r])
+            assert np.all(trace.extract_counts[28:] == 0)
+
+
+def test_acceptance_c09_dictionary_invariants(dic, tmp_path):
+    """Acceptance criterion 09 (test_acceptance.py:299-318)."""
+    assert len(dic) == 65536
+    logs = np.array([dic.entry_log2_probability(i) for i in range(65536)])
+    assert np.all(np.diff(logs) <= 1e-12)
+    singles = {dic.entry(i) for i in range(65536) if dic.pair_counts[i] == 1}
+    assert singles == {((a, b),) for a in range(3) for b in range(3)}
+    assert dic.entry(0) == ((0, 0),)
+    again = q.generate_dictionary(q.PairDistribution(0.885))
+    p1, p2 = tmp_path / "a.dict", tmp_path / "b.dict"
+    q.save_dictionary(dic, str(p1))
+    q.save_dictionary(again, str(p2))
+    assert p1.read_bytes() == p2.read_bytes()
