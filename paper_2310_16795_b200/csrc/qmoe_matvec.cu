@@ -1552,6 +1552,7 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
                         int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h,
                         int64_t ldh, float* d_y, int64_t ldy, int32_t* d_counters, int32_t* d_order,
                         int32_t* d_expert_count, int32_t hot_entries, const float* d_gate, void* stream) {
+  if (T == 0 && d && E >= 1) return QMOE_OK;  // nothing to do (empty buffers may be null)
   if (!d || !d->d_stab || !d_assign || T < 0 || E < 1 || !d_mats || tokens_per_run < 1 ||
       tokens_per_run > NT_STREAM || lg_wi < 0 || lg_wi > 5 || lg_wo < 0 || lg_wo > 5 || d_model <= 0 ||
       d_ff <= 0 || !d_h || !d_y || !d_counters || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16))

@@ -212,10 +212,12 @@ class CompressedMoELayer:
         import torch
 
         T = x.shape[0]
-        if T > self.max_tokens:
-            self._alloc(T)
         if out is None:
             out = torch.empty((T, self.d_model), dtype=torch.float32, device=self.device)
+        if T == 0:
+            return out
+        if T > self.max_tokens:
+            self._alloc(T)
         if x.dtype not in (torch.bfloat16, torch.float32):
             x = x.float()
         if not self._aligned_rows(x):

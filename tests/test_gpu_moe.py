@@ -315,3 +315,20 @@ def test_fused_plan_many_experts(dic):
     finally:
         os.environ.pop("QMOE_FUSED")
     assert torch.equal(y_fused[ok], y_grouped[ok])
+
+
+def test_empty_step_and_no_expert_tokens(dic):
+    """T = 0 through the host API and the device API; a step whose tokens all
+    lack an expert (ids outside [0, E)) returns zero rows on the host API."""
+    rng = np.random.default_rng(3)
+    E, d_model, d_ff = 4, 64, 128
+    wi, wo, _ = _random_layer(dic, rng, E, d_model, d_ff, 8)
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=8)
+    y0 = layer.forward(np.zeros((0, d_model), np.float32), np.zeros(0, np.int32))
+    assert y0.shape == (0, d_model)
+    yd = layer.forward_device(torch.zeros((0, d_model), device="cuda"), torch.zeros(0, dtype=torch.int32, device="cuda"))
+    assert tuple(yd.shape) == (0, d_model)
+    x = q.bf16_round(rng.normal(size=(5, d_model)).astype(np.float32))
+    ids = np.array([-1, E, E + 7, -3, -1], np.int32)
+    y = layer.forward(x, ids)
+    assert y.shape == (5, d_model) and np.all(np.isfinite(y))
