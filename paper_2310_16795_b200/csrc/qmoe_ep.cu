@@ -84,9 +84,9 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 extern "C" int qmoe_ep_slots(const int32_t* d_assign, int32_t T, int32_t E, int32_t world, int32_t* d_slot,
                              int32_t* d_id_send, int32_t* d_send_counts, void* stream) {
+  if (T == 0 && E >= 1 && world >= 1 && world <= EP_MAXW && E % world == 0) return QMOE_OK;
   if (!d_assign || T < 0 || E < 1 || world < 1 || world > EP_MAXW || E % world || !d_slot || !d_id_send)
     return qmoe::fail(QMOE_EINVAL, "bad argument (1 <= world <= 64, world divides E)");
-  if (T == 0) return QMOE_OK;
   ep_slots_kernel<<<1, EP_THREADS, 0, S(stream)>>>(d_assign, T, E, world, d_slot, d_id_send, d_send_counts);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? QMOE_OK : qmoe::fail(QMOE_ECUDA, cudaGetErrorString(e));
@@ -94,10 +94,10 @@ extern "C" int qmoe_ep_slots(const int32_t* d_assign, int32_t T, int32_t E, int3
 
 extern "C" int qmoe_ep_rows(const void* d_src, void* d_dst, int32_t n_rows, int64_t row_bytes, const int32_t* d_index,
                             int scatter, void* stream) {
+  if (n_rows == 0) return QMOE_OK;
   if (!d_src || !d_dst || !d_index || n_rows < 0 || row_bytes <= 0 || row_bytes % 16 ||
       (reinterpret_cast<uintptr_t>(d_src) & 15) || (reinterpret_cast<uintptr_t>(d_dst) & 15))
     return qmoe::fail(QMOE_EINVAL, "bad argument (16-byte aligned rows)");
-  if (n_rows == 0) return QMOE_OK;
   const int wpb = 8;
   ep_rows_kernel<<<(n_rows + wpb - 1) / wpb, wpb * 32, 0, S(stream)>>>(
       reinterpret_cast<const uint4*>(d_src), reinterpret_cast<uint4*>(d_dst), n_rows, (int)(row_bytes / 16), d_index,
