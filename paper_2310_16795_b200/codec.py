@@ -328,12 +328,52 @@ def fused_matvec_device(dm: DeviceMatrix, dic: Dictionary, x, y, stream=None, ba
     xt = _lib.QMOE_X_BF16 if _x_dtype_code(x) == _lib.QMOE_X_BF16 else _lib.QMOE_X_F32
     x = _staging_x(x)
     if x.dim() == 1:
-        _lib.check(_lib.lib.qmoe_fused_matvec(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), _lib.ptr(dm.row_minmax),
-                                              dm.rows, dm.cols, _lib.ptr(x), xt, _lib.ptr(y), _lib.ptr(bad), sp))
+        runs = _api_run(dm, dic) if dic.device_info(dm.cw.device.index)["sparse_path"] else None
+        if runs is not None:  # one matrix spread over ~6K lanes (row checkpoints), one grouped launch
+            raw, n = runs
+            ldx = ((dm.cols + 7) // 8) * 8 if xt == _lib.QMOE_X_BF16 else ((dm.cols + 3) // 4) * 4
+            _lib.check(_lib.lib.qmoe_grouped_matvec(h, None, _lib.ptr(raw), _lib.ptr(n), 1, dm.cols, 1, _lib.ptr(x),
+                                                    xt, ldx, _lib.ptr(y), _lib.QMOE_Y_ACCUM_F32, dm.rows,
+                                                    API_HOT_ENTRIES, _lib.ptr(bad), sp))
+        else:
+            _lib.check(_lib.lib.qmoe_fused_matvec(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off),
+                                                  _lib.ptr(dm.row_minmax), dm.rows, dm.cols, _lib.ptr(x), xt,
+                                                  _lib.ptr(y), _lib.ptr(bad), sp))
     else:
         _lib.check(_lib.lib.qmoe_fused_matmat(h, _lib.ptr(dm.cw), _lib.ptr(dm.row_off), _lib.ptr(dm.row_minmax),
                                               dm.rows, dm.cols, _lib.ptr(x), xt, x.shape[0], x.stride(0),
                                               _lib.ptr(y), y.stride(0), _lib.ptr(bad), sp))
+
+
+API_LANES = 6144  # lanes one API matvec is spread over (~192 warps)
+API_HOT_ENTRIES = 4096  # table entries each CTA stages for it (the fill is per CTA per launch)
+
+
+def _api_run(dm: DeviceMatrix, dic: Dictionary):
+    """Work record (one run) + row checkpoints that let a single matrix use
+    ~API_LANES lanes: G = 2^lg lanes per row while each keeps >= ~1.5 groups
+    of 8 codewords. Built once per uploaded matrix; None when one lane per row
+    already fills the lanes (then qmoe_fused_matvec is used)."""
+    hit = getattr(dm, "_api_runs", None)
+    if hit is not None:
+        return hit or None
+    torch = _torch()
+    mg = dm.n_codewords / max(1, dm.rows) / 8
+    lg = 0
+    while lg < 3 and dm.rows * (1 << lg) < API_LANES and mg / (1 << (lg + 1)) >= 1.5:
+        lg += 1
+    if lg == 0 or dm.rows == 0:
+        dm._api_runs = ()
+        return None
+    if dm.ck is None or dm.lg < lg:
+        dm.build_checkpoints(dic, lg)
+    tasks = ((dm.rows << lg) + 31) >> 5
+    rec = _lib.QmoeWork(dm.cw.data_ptr(), dm.row_off.data_ptr(), dm.row_minmax.data_ptr(), dm.ck.data_ptr(),
+                        dm.cols, 0, dm.rows, lg | (dm.lg << 8), 1, 0, 0, (0, 0, 0, 0))
+    raw = torch.from_numpy(np.frombuffer(bytes(rec), dtype=np.uint8).copy()).to(dm.cw.device)
+    n = torch.tensor([1, tasks], dtype=torch.int32, device=dm.cw.device)
+    dm._api_runs = (raw, n)
+    return dm._api_runs
 
 
 def _staging_x(x):
