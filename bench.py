@@ -296,6 +296,56 @@ def matvec_at_scale(dic, dev, hbm_peak, rows=768, cols=3072, lg=2, iters=20):
     return out
 
 
+def single_matrix_api(dic, dev, rows=768, cols=3072, n=64):
+    """Config 1 through the drop-in API: fused_matvec(c, x, dic) on one
+    768 x 3072 matrix (batch 1) — device path per call (uploaded matrix, CUDA
+    graph of n calls over n distinct matrices: cold) and the host call with
+    numpy x in / numpy y out."""
+    import time
+
+    import torch
+
+    import paper_2310_16795_b200 as q
+    from paper_2310_16795_b200.codec import fused_matvec_device
+    from paper_2310_16795_b200.synth import _stacked
+
+    mats = _stacked(n, rows, cols, seed=777, dic=dic, device=dev)  # uploaded, dictionary order
+    x = torch.randn(cols, device=dev).to(torch.bfloat16)
+    y = torch.zeros(rows, device=dev)
+    for m in mats:
+        fused_matvec_device(m, dic, x, y)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for m in mats:
+            fused_matvec_device(m, dic, x, y)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    dev_us = e0.elapsed_time(e1) / (5 * n) * 1e3
+    # host API: a CompressedMatrix (uploaded once, cached), numpy x -> numpy y
+    w = (np.random.default_rng(5).normal(size=(rows, cols)) * 0.02).astype(np.float32)
+    c = q.encode(q.rtn_quantize(w, q.make_grid(w)), dic)
+    xh = q.bf16_round(np.random.default_rng(6).normal(size=cols).astype(np.float32))
+    for _ in range(10):
+        q.fused_matvec(c, xh, dic)
+    t0 = time.perf_counter()
+    for _ in range(200):
+        q.fused_matvec(c, xh, dic)
+    host_us = (time.perf_counter() - t0) / 200 * 1e6
+    nbytes = float(np.mean([m.compressed_bytes for m in mats]))
+    del mats
+    torch.cuda.empty_cache()
+    return {"api": "fused_matvec (drop-in, batch 1)", "shape": f"{rows}x{cols}", "device_us_per_call": dev_us,
+            "device_GBps": nbytes / dev_us / 1e3, "host_us_per_call": host_us,
+            "host_what": "numpy x in, numpy y out, matrix uploaded once (cached)"}
+
+
 def profiled_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu
     capture (profiles/roofline_r01.json), or None."""
@@ -509,9 +559,10 @@ def main():
     # ---- the decode + matvec kernel at scale (first half of the metric): one
     # grouped launch over a pool (> 4x L2) of distinct 768x3072 matrices
     # (Switch-base wo shape, 4 lanes per row), 1 token, cold
-    at_scale = None
+    at_scale = config1 = None
     if not args.profile:
         at_scale = matvec_at_scale(dic, dev, hbm_peak)
+        config1 = single_matrix_api(dic, dev)
 
     traffic, _ = profiled_traffic()
     if rank == 0:
@@ -546,6 +597,7 @@ def main():
                                       "GEMMs per touched expert in a CUDA graph, and its HBM speed-of-light "
                                       "(bf16 bytes of the touched experts / measured HBM peak)"},
             "kernel_at_scale": at_scale,
+            "config1_single_matrix": config1,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": (1 if fused else 3) * args.steps,
