@@ -622,13 +622,20 @@ __global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint32_t en = ge[u];
+          const int b = gc[u] - k0;  // the codeword's start column in this chunk (may be < 0)
 #pragma unroll
           for (int jj = 0; jj < 3; ++jj) {
             const uint32_t f = __byte_perm(en, 0u, 0x4440u + jj);
-            const int vk = gc[u] + (int)(f >> 2) - k0;
-            if (f != 0x7Fu && (unsigned)vk < (unsigned)RW_KC)
-              sts_u16(wrow + (uint32_t)(vk >> 6) * (RW_ROWS * 128u) + ((((uint32_t)vk & 63u) * 2u) ^ rx),
-                      ((en >> (24 + jj)) & 1u) ? whi : wlo);
+            const int vk = b + (int)(f >> 2);
+            if (f != 0x7Fu && (unsigned)vk < (unsigned)RW_KC) {
+              uint32_t a;
+              if constexpr (RW_KC == 64) {
+                a = wrow + (((uint32_t)vk * 2u) ^ rx);  // one SW128 K-block per chunk
+              } else {
+                a = wrow + (uint32_t)(vk >> 6) * (RW_ROWS * 128u) + ((((uint32_t)vk & 63u) * 2u) ^ rx);
+              }
+              sts_u16(a, ((en >> (24 + jj)) & 1u) ? whi : wlo);
+            }
           }
         }
         if (gc[8] > kend) break;  // the group continues in the next chunk
