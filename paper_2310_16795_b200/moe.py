@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -321,7 +322,7 @@ class CompressedMoELayer:
         return out, assign, gate
 
     GRAPH_CACHE = 8  # token counts with a captured host-API graph per layer
-    _HOST_STAGING: dict = {}  # (bytes, T, d_model) -> pinned (input, output) buffers
+    _HOST_STAGING = threading.local()  # per thread: (bytes, T, d_model) -> pinned (input, output) buffers
 
     def forward(self, x: np.ndarray, assign: np.ndarray) -> np.ndarray:
         """Host API: numpy tokens + expert ids in, numpy outputs back.
@@ -329,7 +330,8 @@ class CompressedMoELayer:
         Per token count T the layer keeps pinned host staging buffers, device
         buffers and (after the first call) a CUDA graph holding the H2D copies,
         the step and the D2H copy, so a call is: copy into pinned memory,
-        one graph launch, one stream sync, copy out."""
+        one graph launch, one stream sync, copy out. A layer (its hidden,
+        counters and captured graphs) serves one thread at a time."""
         import torch
 
         x = np.ascontiguousarray(x, np.float32)
@@ -379,12 +381,12 @@ class CompressedMoELayer:
         # pinned staging shared by every layer of the same shape (calls are
         # synchronous): a model's layers reuse host memory that stays in the
         # CPU caches
+        shared = CompressedMoELayer._HOST_STAGING.__dict__.setdefault("bufs", {})  # per thread
         hkey = (nb, T, self.d_model)
-        if hkey not in CompressedMoELayer._HOST_STAGING:
-            CompressedMoELayer._HOST_STAGING[hkey] = (
-                torch.empty(nb, dtype=torch.uint8, pin_memory=True),
-                torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True))
-        in_h, y_h = CompressedMoELayer._HOST_STAGING[hkey]
+        if hkey not in shared:
+            shared[hkey] = (torch.empty(nb, dtype=torch.uint8, pin_memory=True),
+                            torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True))
+        in_h, y_h = shared[hkey]
         in_d = torch.empty(nb, dtype=torch.uint8, device=self.device)
         x_d = in_d[:xb].view(torch.float32).view(T, self.d_model)
         a_d = in_d[xb:xb + T * 4].view(torch.int32)
