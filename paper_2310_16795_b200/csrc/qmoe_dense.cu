@@ -131,6 +131,24 @@ __device__ __forceinline__ uint4 x_chunk8(const void* x, int bf16, int64_t i) {
   return make_uint4(pk(a.x, a.y), pk(a.z, a.w), pk(b.x, b.y), pk(b.z, b.w));
 }
 
+__device__ __forceinline__ uint4 x_chunk8_cols(const void* x, int bf16, int64_t i, int valid) {
+  // 8 x values from column c, of which only the first `valid` (= cols - c)
+  // belong to the row: the rest are zeroed — the row padding is never
+  // written (it may hold NaN / Inf bit patterns, and 0 * NaN would poison the
+  // MMA accumulators of every row)
+  uint4 v = x_chunk8(x, bf16, i);
+  if (valid < 8) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (2 * k >= valid) w[k] = 0u;
+      else if (2 * k + 1 >= valid) w[k] &= 0xFFFFu;
+    }
+    v = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  return v;
+}
+
 // ROWS rows per item (ROWS / 128 UMMA row blocks, DTHREADS / ROWS lanes per
 // row), KC columns per chunk (KC / 64 SW128 blocks).
 template <int BN, int ROWS, int KC>
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
       for (int u = 0; u < XV; ++u) {
         const int i = tid + u * DTHREADS, nn = i / (DT_KC / 8), c8 = i % (DT_KC / 8);
         xr[u] = (nn < nt && k0 + c8 * 8 < P.cols)
-                    ? x_chunk8(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8)
+                    ? x_chunk8_cols(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8, P.cols - k0 - c8 * 8)
                     : make_uint4(0u, 0u, 0u, 0u);
       }
     };
@@ -590,8 +608,9 @@ __global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) 
 #pragma unroll
       for (int v = 0; v < XV; ++v) {
         const int idx = tid + v * RW_THREADS, nn = idx / (RW_KC / 8), c8 = idx % (RW_KC / 8);
-        xr[v] = (idx < XP && nn < nt && k0 + c8 * 8 < P.cols) ? x_chunk8(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8)
-                                                  : make_uint4(0u, 0u, 0u, 0u);
+        xr[v] = (idx < XP && nn < nt && k0 + c8 * 8 < P.cols)
+                    ? x_chunk8_cols(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8, P.cols - k0 - c8 * 8)
+                    : make_uint4(0u, 0u, 0u, 0u);
       }
     };
     load_x(0);

@@ -332,3 +332,36 @@ def test_empty_step_and_no_expert_tokens(dic):
     ids = np.array([-1, E, E + 7, -3, -1], np.int32)
     y = layer.forward(x, ids)
     assert y.shape == (5, d_model) and np.all(np.isfinite(y))
+
+
+def test_dense_pass_ignores_row_padding(dic, odic):
+    """The hidden rows are padded to a 16-byte stride and the padding is never
+    written: the decode-then-MMA pass must not read it into the MMA (NaN bit
+    patterns there would poison whole accumulators: 0 * NaN = NaN)."""
+    import os
+
+    rng = np.random.default_rng(41)
+    E, d_model, d_ff, T = 3, 96, 300, 90  # d_ff % 8 != 0: padded hidden rows
+    wi, wo, host = [], [], []
+    for e in range(E):
+        pair = []
+        for rows, cols, lst in ((d_ff, d_model, wi), (d_model, d_ff, wo)):
+            w = (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+            c = q.encode(q.rtn_quantize(w, q.make_grid(w)), dic)
+            lst.append(c.to_device(dic))
+            pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
+        host.append(tuple(pair))
+    layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+    assert layer.h.stride(0) > d_ff
+    layer.h.fill_(float("nan"))
+    x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
+    assign = rng.integers(0, E, size=T).astype(np.int32)
+    os.environ["QMOE_DENSE"] = "1"
+    try:
+        y = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
+    finally:
+        os.environ.pop("QMOE_DENSE")
+    y_ref = O.moe_layer(x, assign, host, odic)
+    d = bf16_ulp_diff(y.cpu().numpy(), y_ref)
+    assert np.isfinite(y.cpu().numpy()).all()
+    assert d.max() <= 2 and np.mean(d == 0) >= 0.99
