@@ -146,7 +146,9 @@ def padded_empty(n: int, dtype, device):
 
     esz = torch.empty((), dtype=dtype).element_size()
     pad = (64 + esz - 1) // esz  # the streaming kernel reads whole 32-byte groups
-    return torch.empty(n + pad, dtype=dtype, device=device)[:n]
+    buf = torch.empty(n + pad, dtype=dtype, device=device)
+    buf[n:].zero_()  # the over-read tail is defined (its values are never used)
+    return buf[:n]
 
 
 def padded_copy(t):

@@ -136,17 +136,10 @@ __device__ __forceinline__ uint4 x_chunk8_cols(const void* x, int bf16, int64_t 
   // belong to the row: the rest are zeroed — the row padding is never
   // written (it may hold NaN / Inf bit patterns, and 0 * NaN would poison the
   // MMA accumulators of every row)
-  uint4 v = x_chunk8(x, bf16, i);
-  if (valid < 8) {
-    uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (2 * k >= valid) w[k] = 0u;
-      else if (2 * k + 1 >= valid) w[k] &= 0xFFFFu;
-    }
-    v = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-  return v;
+  if (valid >= 8) return x_chunk8(x, bf16, i);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};  // the row's tail: element loads, nothing past the row
+  for (int e = 0; e < valid; ++e) w[e >> 1] |= (uint32_t)x_bf16_bits(x, bf16, i + e) << (16 * (e & 1));
+  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // ROWS rows per item (ROWS / 128 UMMA row blocks, DTHREADS / ROWS lanes per

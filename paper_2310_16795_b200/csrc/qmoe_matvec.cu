@@ -1082,6 +1082,17 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   __shared__ __align__(8) uint64_t tab_bar;
   trace_stamp(0);
   table_fill_async(PW.gtab, PW.H, &tab_bar);  // overlaps the plan below
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x >= 32) {
+    // tokens without an expert (ids outside [0, E)) get zero output rows
+    // (the composed reference leaves them zero); the other warps of this CTA
+    // do it while warp 0 plans
+    float* y = reinterpret_cast<float*>(S.wo.y);
+    for (int t = 0; t < T; ++t) {
+      const int e = __ldg(S.assign + t);
+      if (e < 0 || e >= E)
+        for (int i = (int)threadIdx.x - 32; i < S.d_model; i += THREADS - 32) y[(int64_t)t * S.wo.ldy + i] = 0.f;
+    }
+  }
   // ---- 1. plan
   bool wpre_ready = false;
   __shared__ int s_nch;

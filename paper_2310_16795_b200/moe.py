@@ -226,6 +226,7 @@ class CompressedMoELayer:
             buf.copy_(x)
             x = buf
         if self.use_dense(T):
+            self._zero_out(out, stream)
             self.plan(assign, stream)
             self.pass_dense(x, 0, self.h, _lib.QMOE_Y_RELU_BF16, stream)
             self.pass_dense(self.h, 1, out, _lib.QMOE_Y_STORE_F32, stream)
@@ -238,10 +239,25 @@ class CompressedMoELayer:
                 if err.status != _lib.QMOE_EUNSUPPORTED:
                     raise
         if True:
+            self._zero_out(out, stream)
             self.plan(assign, stream)
             self.pass_wi(x, stream)
             self.pass_wo(out, stream)
         return out
+
+    @staticmethod
+    def _zero_out(out, stream=None):
+        """The grouped / dense passes store only the rows of tokens that have
+        an expert; tokens without one (ids outside [0, E)) keep zero rows, as
+        the composed reference leaves them (the fused step zeroes them in its
+        kernel). A memset, capture-friendly."""
+        import torch
+
+        if stream is None:
+            out.zero_()
+        else:
+            with torch.cuda.stream(stream):
+                out.zero_()
 
     DENSE_MIN_TOKENS = 12.0  # tokens per touched expert above which decode-then-MMA wins (measured)
 
@@ -391,9 +407,16 @@ class CompressedMoELayer:
         x_d = in_d[:xb].view(torch.float32).view(T, self.d_model)
         a_d = in_d[xb:xb + T * 4].view(torch.int32)
 
+        direct = self.fused and not key[1]  # the fused step writes every output row (dropped ones: zero)
+        y_d = None if direct else torch.empty((T, self.d_model), dtype=torch.float32, device=self.device)
+
         def body():
             in_d.copy_(in_h, non_blocking=True)
-            self.forward_device(x_d, a_d, out=y_h)
+            if direct:
+                self.forward_device(x_d, a_d, out=y_h)
+            else:  # grouped / decode-then-MMA passes: device output, then one D2H copy
+                self.forward_device(x_d, a_d, out=y_d)
+                y_h.copy_(y_d, non_blocking=True)
 
         st = {
             "in_h": in_h, "in_d": in_d, "y_h": y_h, "body": body, "graph": None,

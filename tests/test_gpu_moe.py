@@ -259,7 +259,8 @@ def test_fused_step_equals_grouped_passes_and_plan(dic, T):
         y_grouped = layer2.forward_device(x, a)
     finally:
         os.environ.pop("QMOE_FUSED")
-    assert torch.equal(y_fused[ok], y_grouped[ok])
+    assert torch.equal(y_fused, y_grouped)  # incl. zero rows for tokens without an expert
+    assert torch.all(y_fused[~torch.from_numpy(ok).cuda()] == 0)
     # a second step with the same layer reuses the self-resetting counters
     y_again = layer.forward_device(x, a)
     assert torch.equal(y_again[ok], y_fused[ok])
@@ -331,7 +332,10 @@ def test_empty_step_and_no_expert_tokens(dic):
     x = q.bf16_round(rng.normal(size=(5, d_model)).astype(np.float32))
     ids = np.array([-1, E, E + 7, -3, -1], np.int32)
     y = layer.forward(x, ids)
-    assert y.shape == (5, d_model) and np.all(np.isfinite(y))
+    assert y.shape == (5, d_model) and np.all(y == 0)  # no expert: zero rows, as the composed reference
+    mixed = np.array([0, -1, 2, E, 1], np.int32)
+    ym = layer.forward(x, mixed)
+    assert np.all(ym[[1, 3]] == 0) and np.any(ym[[0, 2, 4]] != 0)
 
 
 def test_dense_pass_ignores_row_padding(dic, odic):
