@@ -259,7 +259,7 @@ class CompressedMoELayer:
             with torch.cuda.stream(stream):
                 out.zero_()
 
-    DENSE_MIN_TOKENS = 12.0  # tokens per touched expert above which decode-then-MMA wins (measured)
+    DENSE_MIN_TOKENS = 7.0  # tokens per touched expert above which decode-then-MMA wins (measured: 6 -> streaming, 8 -> dense)
 
     def use_dense(self, T: int) -> bool:
         """Batched regime: each expert block decoded once and multiplied with
