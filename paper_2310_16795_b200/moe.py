@@ -164,6 +164,10 @@ class CompressedMoELayer:
             hit = self._lanes[T] = tuple(out)
         return hit
 
+    # the fused step stages at most 32K entries (91-92% of lookups): a smaller
+    # per-step fill than the whole table, measured 2% faster at T = 64 / 256
+    STEP_HOT_MAX = 32768
+
     def hot_entries(self, T: int, wi: bool) -> int:
         """table entries to stage per SM: ~4x the codewords one SM decodes in
         the pass (small steps stage little: the fill is per CTA per launch)"""
@@ -312,7 +316,8 @@ class CompressedMoELayer:
             self.handle, self._table(), _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit,
             lg_wi, lg_wo, self.d_model, self.d_ff, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h), self.h.stride(0),
             _lib.ptr(out), out.stride(0), _lib.ptr(self.counters), _lib.ptr(self.order), _lib.ptr(self.expert_count),
-            max(self.hot_entries(T, True), self.hot_entries(T, False)), _lib.ptr(gate), _lib.stream_ptr(stream)))
+            min(self.STEP_HOT_MAX, max(self.hot_entries(T, True), self.hot_entries(T, False))), _lib.ptr(gate),
+            _lib.stream_ptr(stream)))
 
     def forward_routed(self, x, router, gated: bool = False, out=None, stream=None):
         """Router + layer on the device: expert ids (and, with `gated`, the
