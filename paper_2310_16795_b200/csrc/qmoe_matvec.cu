@@ -67,6 +67,7 @@ struct SegParams {
   int xcap;                   // x elements staged per token
   int xbytes;                 // x staging bytes (pipe kernel: several runs' slots)
   const float* gate;          // STORE_F32 only, nullable: y = gate[t] * bf16(dot)
+  unsigned long long* trace;  // fused step debug stamps (qmoe_debug_step_trace), nullable
 };
 
 struct Run {
@@ -595,21 +596,21 @@ __device__ __forceinline__ int claim_task(int* next) {
   return __shfl_sync(FULL_MASK, k, 0);
 }
 
-__device__ unsigned long long* g_step_trace = nullptr;  // qmoe_debug_step_trace: per-CTA phase stamps
-
-__device__ __forceinline__ void trace_stamp(int k) {
+__device__ __forceinline__ void trace_stamp(unsigned long long* trace, int k) {
+  // qmoe_debug_step_trace: per-CTA phase stamps. The pointer is a kernel
+  // parameter (constant bank), so a disabled trace costs no memory load.
   // slot 0: %globaltimer at the CTA's start (aligns CTAs); slots 1-7: SM
   // clock cycles since then (globaltimer is too coarse for sub-µs phases)
   __shared__ long long s_clk0;
-  if (g_step_trace && threadIdx.x == 0) {
+  if (trace && threadIdx.x == 0) {
     const long long c = clock64();
     if (k == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       s_clk0 = c;
-      g_step_trace[blockIdx.x * 8] = t;
+      trace[blockIdx.x * 8] = t;
     } else {
-      g_step_trace[blockIdx.x * 8 + k] = (unsigned long long)(c - s_clk0);
+      trace[blockIdx.x * 8 + k] = (unsigned long long)(c - s_clk0);
     }
   }
 }
@@ -737,12 +738,12 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
       if (threadIdx.x == 0)
         for (int w = 0; w < nw; ++w) src.wait(win[w].ri);
       __syncthreads();
-      trace_stamp(6);  // (last) window's producer runs done
+      trace_stamp(P.trace, 6);  // (last) window's producer runs done
       stage_x();
     }
     __syncthreads();
     if (!COHERENT_X && active) lookup_any(ea, q0, lane_vm(c, 0), tab_s, H, gtab);
-    if (!COHERENT_X && t == t_begin) trace_stamp(5);  // first window staged (wi)
+    if (!COHERENT_X && t == t_begin) trace_stamp(P.trace, 5);  // first window staged (wi)
     if (active) {
       for (;;) {
         const WinRun& W = win[wc];
@@ -1080,7 +1081,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   int* wpre = runs4 + 4 * T;
   const SegParams& PW = S.wi;
   __shared__ __align__(8) uint64_t tab_bar;
-  trace_stamp(0);
+  trace_stamp(S.wi.trace, 0);
   table_fill_async(PW.gtab, PW.H, &tab_bar);  // overlaps the plan below
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x >= 32) {
     // tokens without an expert (ids outside [0, E)) get zero output rows
@@ -1147,7 +1148,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       }
     }
     __syncthreads();
-    trace_stamp(5);
+    trace_stamp(S.wi.trace, 5);
     if (blockIdx.x == 0 && S.count_out)
       for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = cnt[e];
     __syncthreads();
@@ -1194,7 +1195,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
 
   }
   __syncthreads();
-  trace_stamp(7);
+  trace_stamp(S.wi.trace, 7);
   const int nch = wpre_ready ? s_nch : choff[E];
   // cost-weighted split of the run list over the CTAs: a 2-token run decodes
   // once but gathers and accumulates twice (~1.4x a 1-token run, measured)
@@ -1242,7 +1243,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     }
   }
   __syncthreads();
-  trace_stamp(1);
+  trace_stamp(S.wi.trace, 1);
   const uint32_t tab_s = smem_base();
   // ---- 2. wi phase
   {
@@ -1257,7 +1258,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
         atomicAdd(S.counters + 1 + r, b - a);
       }
     }
-    trace_stamp(2);
+    trace_stamp(S.wi.trace, 2);
   }
   // ---- 3. wo phase
   {
@@ -1267,7 +1268,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   }
   // ---- 4. last CTA re-arms the counters
   __syncthreads();
-  trace_stamp(3);
+  trace_stamp(S.wi.trace, 3);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(S.counters, 1) == (int)gridDim.x - 1) {
@@ -1279,6 +1280,8 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
 }
 
 // ----------------------------------------------------------------- host side
+unsigned long long* g_trace_host = nullptr;  // qmoe_debug_step_trace buffer (debug only)
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int hot_override() {
@@ -1544,7 +1547,7 @@ int qmoe_debug_step_trace(void* d_buf) {
   // debug hook: per-CTA phase stamps of the fused step (8 u64 per CTA: [0]
   // %globaltimer at start, [1..7] SM cycles since start: plan done, wi done,
   // wo done, then plan sub-steps); NULL disables
-  CK(cudaMemcpyToSymbol(g_step_trace, &d_buf, sizeof(void*)), "trace symbol");
+  g_trace_host = reinterpret_cast<unsigned long long*>(d_buf);  // taken by the next launches
   return QMOE_OK;
 }
 
@@ -1592,6 +1595,7 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   SP.wo.y_mode = QMOE_Y_STORE_F32;
   SP.wo.ldy = ldy;
   SP.wo.gate = d_gate;
+  SP.wi.trace = SP.wo.trace = g_trace_host;
   SP.assign = d_assign;
   SP.T = T;
   SP.E = E;
