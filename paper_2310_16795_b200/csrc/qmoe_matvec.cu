@@ -569,6 +569,15 @@ struct ListRuns {
   }
   __device__ __forceinline__ void fill(WinRun& W, int r) const { fill_win(W, get_run(*P, r)); }
   __device__ __forceinline__ void wait(int) const {}
+  __device__ __forceinline__ int first_run(int t) const {  // last run with task0 <= t
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (meta(mid).task0 <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
 };
 
 __device__ __forceinline__ float load_x_cg(const void* x, int bf16, int64_t i) {
@@ -632,50 +641,55 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
   const int warp = threadIdx.x >> 5;
   const uint32_t H = (uint32_t)P.H;
   const uint32_t* gtab = P.gtab;
-  __syncthreads();
-  if (threadIdx.x == 0) {  // run holding t_begin: last run with task0 <= t_begin
-    int lo = 0, hi = src.n - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (src.meta(mid).task0 <= t_begin) lo = mid;
-      else hi = mid - 1;
-    }
-    S.run = lo;
-  }
   WinRun* win = S.win;
   int t = t_begin;
+  bool first = true;
   while (t < t_end) {
     __syncthreads();  // previous window done with xs / win (and S.run published)
-    if (threadIdx.x == 0) {  // next window: consecutive runs whose x slots fit the budget
-      int ri = S.run, nw = 0, xo = 0, wend = t;
-      while (ri < src.n && nw < WIN_RUNS && wend < t_end) {
-        const RunMeta R = src.meta(ri);
-        const int r_end = R.task1;
-        const int need = ((R.ntok > 1 ? 8 : 4) * (R.cols + 32) + 15) & ~15;
-        if (nw > 0 && xo + need > P.xbytes) break;
-        if (r_end > t) {
-          WinRun& W = win[nw++];
-          W.ri = ri;
-          W.cols = R.cols;
-          W.ntok = R.ntok;
-          W.task0 = R.task0;
-          W.task1 = r_end;
-          W.xoff = xo;
-          xo += need;
-          wend = min(t_end, r_end);
-        }
-        if (r_end > t_end) break;
-        ++ri;
+    if (threadIdx.x < 32) {
+      // warp 0 builds the next window and loads its pointers: lane i looks
+      // at run r0 + i; the window is the longest prefix whose x slots fit the
+      // budget (the first run always), ending at the run that reaches t_end
+      const int lane = threadIdx.x;
+      const int r0 = first ? src.first_run(t_begin) : S.run;
+      const int ri = r0 + lane;
+      const bool in = lane < WIN_RUNS && ri < src.n;
+      RunMeta R{0, 0, 0, 0};
+      int need = 0;
+      if (in) {
+        R = src.meta(ri);
+        need = ((R.ntok > 1 ? 8 : 4) * (R.cols + 32) + 15) & ~15;
       }
-      S.nwin = nw;
-      S.wend = wend;
-      S.run = ri;  // first run of the next window
-      S.next = t;
+      int pre = need;  // inclusive prefix of the x slots
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(FULL_MASK, pre, d);
+        if (lane >= d) pre += v;
+      }
+      const unsigned ends = __ballot_sync(FULL_MASK, in && R.task1 >= t_end);
+      const bool take = in && (lane == 0 || pre <= P.xbytes) && (ends & ((1u << lane) - 1u)) == 0;
+      const int nw = __popc(__ballot_sync(FULL_MASK, take));
+      if (take) {
+        WinRun& W = win[lane];
+        W.ri = ri;
+        W.cols = R.cols;
+        W.ntok = R.ntok;
+        W.task0 = R.task0;
+        W.task1 = R.task1;
+        W.xoff = pre - need;
+        src.fill(W, ri);  // pointers, one lane per run
+      }
+      const int last_t1 = __shfl_sync(FULL_MASK, R.task1, nw - 1);
+      if (lane == 0) {
+        S.nwin = nw;
+        S.wend = min(t_end, last_t1);
+        S.run = r0 + nw;  // first run of the next window
+        S.next = t;
+      }
     }
+    first = false;
     __syncthreads();
     const int nw = S.nwin, wend = S.wend;
-    if ((int)threadIdx.x < nw) src.fill(win[threadIdx.x], win[threadIdx.x].ri);  // pointers, in parallel
-    __syncthreads();
     auto stage_x = [&]() {
       for (int w = 0; w < nw; ++w) {  // stage x (fp32; two tokens interleaved)
         const WinRun& W = win[w];
@@ -888,6 +902,7 @@ struct PlanRuns {
     return RunMeta{r * tasks_per_run, (r + 1) * tasks_per_run, runs4[4 * r + 1], cols};
   }
   __device__ __forceinline__ void fill(WinRun& W, int r) const { fill_win(W, get(r)); }
+  __device__ __forceinline__ int first_run(int t) const { return min(n - 1, t / tasks_per_run); }
   __device__ __forceinline__ void wait(int r) const {
     if (!counters) return;
     for (;;) {
