@@ -53,25 +53,17 @@ enum { QMOE_X_F32 = 0, QMOE_X_BF16 = 1 };
 
 typedef struct qmoe_dict* qmoe_dict_t;
 
-/* One compressed matrix resident on the device (grouped launches), in one of
- * two layouts:
- *  RAW (row_id == NULL): the reference format. cw / row_off / row_minmax as
- *    in CompressedMatrix; the arrays must start 16-byte aligned and be
- *    readable 32 bytes past their end. ck / lg: optional row-segment
- *    checkpoints (qmoe_checkpoints): with G = 2^lg lanes per row,
- *    ck[r * (G-1) + j - 1] is the column at which segment j of row r starts
- *    (segment j = codewords [s + j*n/G, s + (j+1)*n/G) of the row's n).
- *  PACKED (row_id != NULL, built by qmoe_pack): kernel-private. Rows sorted
- *    by codeword count (descending), each row's stream padded with codeword 0
- *    (no non-zero value) to whole 8-codeword groups:
- *      cw         uint16[8 * G_total]  group g = cw[8g .. 8g+8)
- *      row_off    int32[rows + 1]      first GROUP of sorted row i (G_total last)
- *      row_minmax uint32[rows]         bf16 (min, max) of sorted row i
- *      ck         uint16[G_total]      column at which group g starts in its row
- *      row_id     uint16[rows]         original row of sorted row i
- *    lg is then only a default: the lanes per row are chosen per run.
- * colpts (RAW, optional): column points for the decode-then-MMA pass
- *    (qmoe_colpoints, 256-column chunks). */
+/* One compressed matrix resident on the device (grouped launches): the
+ * reference format (cw / row_off / row_minmax as in CompressedMatrix; the
+ * arrays must start 16-byte aligned and be readable 32 bytes past their end)
+ * plus optional kernel-private, read-only derived data:
+ *  ck / lg: row-segment checkpoints (qmoe_checkpoints): with G = 2^lg lanes
+ *    per row, ck[r * (G-1) + j - 1] is the column at which segment j of row r
+ *    starts; segment j starts at codeword s + j*n/G rounded UP to a multiple
+ *    of 8 (clamped to the row end e), so inner segment boundaries are 16-byte
+ *    group boundaries of the stream.
+ *  row_id: reserved, must be NULL.
+ *  colpts: column points for the decode-then-MMA pass (qmoe_colpoints). */
 typedef struct qmoe_matrix {
   const uint16_t* cw;
   const int32_t* row_off;
@@ -86,8 +78,7 @@ typedef struct qmoe_matrix {
 } qmoe_matrix;
 
 /* One RUN of a grouped launch (self-contained, 80 bytes): rows [row0, row1)
- * of one matrix (fields as qmoe_matrix; row_id != NULL selects the PACKED
- * layout, rows then being sorted-row indices), applied to `ntok` tokens (<= 2
+ * of one matrix (fields as qmoe_matrix; row_id reserved, NULL), applied to `ntok` tokens (<= 2
  * on the streaming path) with G = 2^lg lanes per row. Token t reads x row
  * tok[t] (x + tok[t] * ldx) and writes y row tok[t] (y + tok[t] * ldy). A
  * run is cut into ceil(((row1 - row0) << lg) / 32) warp TASKS; task0 is the
@@ -114,10 +105,8 @@ enum {
   QMOE_Y_ACCUM_F32 = 0,     /* y (f32) += bf16(dot)                       (codec.py:243) */
   QMOE_Y_RELU_BF16 = 1,     /* y (bf16) = relu(bf16(dot)) — the FFN hidden h, written
                                once from zero: equals relu(fused_matvec(wi, x, y=0)) */
-  QMOE_Y_STORE_F32 = 2,     /* y (f32) = 0 + bf16(dot): accumulate into a zero y
+  QMOE_Y_STORE_F32 = 2      /* y (f32) = 0 + bf16(dot): accumulate into a zero y
                                without reading it */
-  QMOE_RUNS_PACKED = 0x100  /* flag OR-ed into y_mode: every run of the list is a
-                               PACKED-layout matrix (qmoe_pack) */
 };
 
 /* ------------------------------------------------------------------ host-only
@@ -190,8 +179,8 @@ int qmoe_fused_matmat(qmoe_dict_t dict, const uint16_t* d_cw, const int32_t* d_r
  * have been validated (qmoe_validate_rows); d_bad is used by the general
  * (> 3 non-zero) path only. hot_entries: entries of the table staged in
  * shared memory per SM (0 = as many as fit); small launches should stage few.
- * RAW runs: bits 0-7 of work.lg = lanes per row of the run (log2), bits 8-15 =
- * the checkpoint granularity the matrix stores (0 = same); a run may use any
+ * Bits 0-7 of work.lg = lanes per row of the run (log2), bits 8-15 = the
+ * checkpoint granularity the matrix stores (0 = same); a run may use any
  * lg <= the stored one (segment boundaries nest). */
 int qmoe_grouped_matvec(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_work* d_work,
                         const int32_t* d_n_work, int32_t max_work, int32_t max_cols,
@@ -229,18 +218,6 @@ int qmoe_checkpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* 
 int qmoe_colpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d_cw,
                    const int32_t* d_row_off, int64_t rows, int64_t cols, int chunk_log2,
                    uint32_t* d_cp, void* stream);
-
-/* PACKED layout of one RAW matrix (see qmoe_matrix), built once on the device.
- * d_order: int32[rows], the sorted row order (row of sorted row i; e.g. a
- * stable descending sort of the rows' codeword counts); d_gstart:
- * int32[rows + 1], exclusive prefix over sorted rows of ceil(n_row / 8).
- * Outputs d_pcw (uint16[8 * gstart[rows]] + 16 readable), d_pmm, d_pck
- * (uint16[gstart[rows]]), d_rid. d_table as for qmoe_checkpoints (entry order
- * of the stream). Rows that do not decode to cols values are counted in d_bad. */
-int qmoe_pack(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d_cw,
-              const int32_t* d_row_off, const uint32_t* d_row_minmax, int64_t rows, int64_t cols,
-              const int32_t* d_order, const int32_t* d_gstart, uint16_t* d_pcw, uint32_t* d_pmm,
-              uint16_t* d_pck, uint16_t* d_rid, int32_t* d_bad, void* stream);
 
 /* Paper Listing 1 kept as the "paper design on B200"
  * baseline: warp per row, lanes 0..27 extract, decode words read through the
@@ -283,7 +260,8 @@ int qmoe_rtn_quantize(const float* d_w, int64_t rows, int64_t cols, const uint32
  * with task0 prefixes filled. d_runs_* hold max_runs (>= T) records;
  * d_n = int32[4] {runs wi, tasks wi, runs wo, tasks wo}. Ids outside
  * [0, E) are dropped (the token gets no expert output). lg_wi / lg_wo: lanes
- * per row (2^lg) of the runs of PACKED matrices, -1 = the matrix's lg. */
+ * per row (2^lg) of the runs, bounded by each matrix's checkpoint lg; -1 =
+ * the matrix's lg. */
 int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matrix* d_mats,
                   int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo, int32_t max_runs, qmoe_work* d_runs_wi,
                   qmoe_work* d_runs_wo, int32_t* d_n, int32_t* d_expert_count, int32_t* d_order,
@@ -338,17 +316,23 @@ int qmoe_route(int rule, const void* d_x, int x_dtype, int64_t ldx, int32_t T, i
 
 /* Expert-parallel exchange helpers (ep.ExpertParallelMoE):
  * fixed-slot dispatch. Token t with expert id a in [0, E) goes to rank
- * d = a / (E / world), slot d * T + its stable rank among the tokens bound for
- * d (buffer order, pipeline.py:86-90): d_slot[t] (-1: no expert),
- * d_id_send[world * T] = rank-local expert id per slot (-1: empty slot),
+ * d = a / (E / world), slot d * C + its stable rank among the tokens bound for
+ * d (buffer order, pipeline.py:86-90), C = slots_per_rank >= T (the layer's
+ * token capacity, equal on every rank): d_slot[t] (-1: no expert),
+ * d_id_send[world * C] = rank-local expert id per slot (-1: empty slot),
  * d_send_counts[world] (nullable) = tokens per destination. world <= 64. */
-int qmoe_ep_slots(const int32_t* d_assign, int32_t T, int32_t E, int32_t world, int32_t* d_slot,
-                  int32_t* d_id_send, int32_t* d_send_counts, void* stream);
+int qmoe_ep_slots(const int32_t* d_assign, int32_t T, int32_t E, int32_t world, int32_t slots_per_rank,
+                  int32_t* d_slot, int32_t* d_id_send, int32_t* d_send_counts, void* stream);
 /* Row moves by an index (rows of row_bytes, 16-byte aligned): scatter = 1:
  * dst[index[i]] = src[i] (index -1 skipped); scatter = 0: dst[i] =
  * src[index[i]] (index -1: zero row). */
 int qmoe_ep_rows(const void* d_src, void* d_dst, int32_t n_rows, int64_t row_bytes, const int32_t* d_index,
                  int scatter, void* stream);
+/* Combine gather: d_dst[i][:] (f32, d columns) = f32(d_src_bf16[index[i]][:])
+ * (index -1: zero row). Exact for expert outputs (bf16-rounded values), so
+ * the combine all-to-all moves bf16 rows. */
+int qmoe_ep_combine(const uint16_t* d_src_bf16, float* d_dst, int32_t n_rows, int32_t d, const int32_t* d_index,
+                    void* stream);
 
 /* Batched-token decode-then-MMA pass (many tokens per expert, e.g.
  * Switch-large-128 with T in the thousands): for every expert e with tokens

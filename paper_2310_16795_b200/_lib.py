@@ -49,7 +49,6 @@ class QmoeWork(ctypes.Structure):
 
 
 QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16, QMOE_Y_STORE_F32 = 0, 1, 2
-QMOE_RUNS_PACKED = 0x100
 
 
 WORK_BYTES = ctypes.sizeof(QmoeWork)
@@ -86,7 +85,8 @@ _SIGS = {
     "qmoe_moe_step_gated": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, ctypes.c_int, i64,
                                            vp, i64, vp, i64, vp, vp, vp, i32, vp, vp]),
     "qmoe_route_scratch": (i64, [i32, i32, i32]),
-    "qmoe_ep_slots": (ctypes.c_int, [vp, i32, i32, i32, vp, vp, vp, vp]),
+    "qmoe_ep_slots": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, vp, vp, vp]),
+    "qmoe_ep_combine": (ctypes.c_int, [vp, vp, i32, i32, vp, vp]),
     "qmoe_ep_rows": (ctypes.c_int, [vp, vp, i32, i64, vp, ctypes.c_int, vp]),
     "qmoe_route": (ctypes.c_int, [ctypes.c_int, vp, ctypes.c_int, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "qmoe_debug_step_trace": (ctypes.c_int, [vp]),
@@ -94,7 +94,6 @@ _SIGS = {
     "qmoe_dense_moe_pass": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, i32, i32, vp, ctypes.c_int, i64, vp,
                                            ctypes.c_int, i64, i32, i32, vp]),
     "qmoe_colpoints": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, ctypes.c_int, vp, vp]),
-    "qmoe_pack": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

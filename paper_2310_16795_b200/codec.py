@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import struct
 import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -72,6 +73,7 @@ class CompressedMatrix:
         if hit is not None and hit[0] == self._key():
             return hit[1]
         dm = DeviceMatrix.from_host(self, dic, dev)
+        dm.shared = True  # cached for the drop-in API: layers re-index private copies
         self._device[dev.index] = (self._key(), dm)
         return dm
 
@@ -93,8 +95,8 @@ class DeviceMatrix:
         # row-segment checkpoints (G = 2^lg lanes per row), see build_checkpoints
         self.ck = None
         self.lg = 0
-        # kernel-private PACKED layout (qmoe_pack), see build_layout
-        self.packed = None
+        # True when cached on a CompressedMatrix (shared with the drop-in API)
+        self.shared = False
         # column points for the decode-then-MMA pass (qmoe_colpoints), see build_colpoints
         self.colpts = None
 
@@ -128,12 +130,17 @@ class DeviceMatrix:
         self.bad_rows, self.first_bad = b[0], (b[1] if b[0] else None)
         return self.bad_rows
 
+    def private_copy(self) -> "DeviceMatrix":
+        """Same matrix with its own codeword stream (row offsets, levels and
+        kernel-private checkpoints are shared, read-only): what a layer
+        re-indexes with its codebook when this matrix is shared."""
+        dm = DeviceMatrix(self.rows, self.cols, _lib.padded_copy(self.cw), self.row_off, self.row_minmax,
+                          self.dict_hash, self.bad_rows, self.first_bad)
+        dm.ck, dm.lg = self.ck, self.lg
+        return dm
+
     def descriptor(self) -> tuple:
-        """qmoe_matrix fields (include/qmoe.h): the PACKED layout when built."""
-        if self.packed is not None:
-            p = self.packed
-            return (p["cw"].data_ptr(), p["gstart"].data_ptr(), p["mm"].data_ptr(), p["ck"].data_ptr(), self.rows,
-                    self.cols, self.n_codewords, p["lg"], p["rid"].data_ptr(), 0)
+        """qmoe_matrix fields (include/qmoe.h)."""
         return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(),
                 self.ck.data_ptr() if self.ck is not None else 0, self.rows, self.cols, self.n_codewords, self.lg, 0,
                 self.colpts.data_ptr() if self.colpts is not None else 0)
@@ -153,42 +160,6 @@ class DeviceMatrix:
         _lib.check(_lib.lib.qmoe_colpoints(dic.device_handle(self.cw.device.index), _lib.ptr(table), _lib.ptr(self.cw),
                                            _lib.ptr(self.row_off), self.rows, self.cols, self.COLPT_LOG2,
                                            _lib.ptr(self.colpts), _lib.stream_ptr()))
-
-    def build_layout(self, dic: Dictionary) -> None:
-        """Kernel-private PACKED layout (qmoe_pack): rows sorted by codeword
-        count, each padded with codeword 0 to whole 8-codeword groups, plus the
-        start column of every group — lanes then walk whole groups of one row
-        with no masking, and the lanes per row can be chosen per launch. The
-        host format and this matrix's own arrays are unchanged."""
-        torch = _torch()
-        dev = self.cw.device
-        n = (self.row_off[1:] - self.row_off[:-1]).to(torch.int64)
-        m = (n + 7) // 8
-        order = torch.sort(m, descending=True, stable=True).indices.to(torch.int32)
-        gstart = torch.zeros(self.rows + 1, dtype=torch.int64, device=dev)
-        gstart[1:] = torch.cumsum(m[order.long()], 0)
-        G_total = int(gstart[-1].item()) if self.rows else 0
-        gstart = _lib.padded_copy(gstart.to(torch.int32))
-        p = {
-            "cw": _lib.padded_empty(8 * G_total + 16, torch.int16, dev),
-            "gstart": gstart,
-            "mm": _lib.padded_empty(max(1, self.rows), torch.int32, dev),
-            "ck": _lib.padded_empty(max(1, G_total), torch.int16, dev),
-            "rid": _lib.padded_empty(max(1, self.rows), torch.int16, dev),
-            "groups": G_total,
-            "mean_groups": G_total / max(1, self.rows),
-        }
-        p["cw"][8 * G_total:].zero_()
-        bad = torch.tensor([0, INT32_MAX], dtype=torch.int32, device=dev)
-        table = self.codebook.table if self.codebook is not None else None
-        _lib.check(_lib.lib.qmoe_pack(dic.device_handle(dev.index), _lib.ptr(table), _lib.ptr(self.cw),
-                                      _lib.ptr(self.row_off), _lib.ptr(self.row_minmax), self.rows, self.cols,
-                                      _lib.ptr(order), _lib.ptr(gstart), _lib.ptr(p["cw"]), _lib.ptr(p["mm"]),
-                                      _lib.ptr(p["ck"]), _lib.ptr(p["rid"]), _lib.ptr(bad), _lib.stream_ptr()))
-        if int(bad[0].item()):
-            raise CorruptionError("row decodes to the wrong number of values")
-        p["lg"] = max(0, min(3, int(np.log2(max(1.0, p["mean_groups"] / 4)))))
-        self.packed = p
 
     def mean_codewords_per_row(self) -> float:
         return self.n_codewords / max(1, self.rows)
@@ -375,8 +346,9 @@ def _mv_stage(device, rows: int, cols: int) -> dict:
         h = torch.empty(n, dtype=torch.float32, pin_memory=True)
         d = _lib.padded_empty(n, torch.float32, device)
         st = stages[key] = {"h": h, "d": d, "xh": h[:cols].numpy(), "yh": h[xw:].numpy(),
-                                "xd": d[:cols], "yd": d[xw:], "yout": torch.empty(rows, dtype=torch.float32,
-                                                                                  pin_memory=True)}
+                            "xd": d[:cols], "yd": d[xw:],
+                            "yout": torch.empty(rows, dtype=torch.float32, pin_memory=True),
+                            "graphs": weakref.WeakKeyDictionary()}
     return st
 
 
@@ -490,15 +462,23 @@ def fused_matvec(c, x, dic: Dictionary, y=None, workers: int = 1):
         raise _row_len_error()  # y untouched (codec.py:237-243 computes all parts first)
     staged = False
     if not on_device:
+        # float32 y is updated on the GPU (y += bf16(part) in fp32, as the
+        # reference); any other dtype gets the bf16 part back and adds it on
+        # the host in its own dtype (codec.py:243: y[rows] += part)
+        accum_dev = y.dtype == np.float32
         st = _mv_stage(dm.cw.device, dm_rows, dm_cols)
         np.copyto(st["xh"], x32)
-        np.copyto(st["yh"], y, casting="unsafe")
+        if accum_dev:
+            np.copyto(st["yh"], y)
+        else:
+            st["yh"].fill(0.0)
         finite = bool(np.isfinite(x32).all())
         if finite and dm_cols > 0 and torch.cuda.current_device() == dm.cw.device.index:
-            # H2D copy + kernel + D2H copy, captured once per (matrix, staging)
-            # and replayed: the call is then one graph launch and one sync
-            graphs = dm.__dict__.setdefault("_api_graphs", {})
-            g = graphs.get(id(st))
+            # H2D copy + kernel + D2H copy, captured once per (staging, matrix)
+            # and replayed: the call is then one graph launch and one sync. The
+            # graph lives in the (per-thread) staging that owns its buffers,
+            # keyed weakly by the matrix whose buffers it reads.
+            g = st["graphs"].get(dm)
             if g is None:
                 def body():
                     st["d"].copy_(st["h"], non_blocking=True)
@@ -509,15 +489,15 @@ def fused_matvec(c, x, dic: Dictionary, y=None, workers: int = 1):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
                     body()
-                graphs[id(st)] = g
-                np.copyto(st["yh"], y, casting="unsafe")  # the eager call consumed the staged y
+                st["graphs"][dm] = g
+                # the eager call consumed the staged y
+                if accum_dev:
+                    np.copyto(st["yh"], y)
+                else:
+                    st["yh"].fill(0.0)
             g.replay()
             torch.cuda.current_stream().synchronize()
-            out = st["yout"].numpy()
-            if y.dtype == np.float32:
-                y[...] = out
-            else:
-                y[...] = out.astype(y.dtype)
+            _mv_out(y, st["yout"].numpy(), accum_dev)
             return y
         st["d"].copy_(st["h"], non_blocking=True)
         xd, yd, staged = st["xd"], st["yd"], True
@@ -533,12 +513,15 @@ def fused_matvec(c, x, dic: Dictionary, y=None, workers: int = 1):
         return y
     st["yout"].copy_(yd, non_blocking=True)
     torch.cuda.current_stream(dm.cw.device).synchronize()
-    out = st["yout"].numpy()
-    if y.dtype == np.float32:
+    _mv_out(y, st["yout"].numpy(), accum_dev)
+    return y
+
+
+def _mv_out(y: np.ndarray, out: np.ndarray, accum_dev: bool) -> None:
+    if accum_dev:
         y[...] = out
     else:
-        y[...] = out.astype(y.dtype)
-    return y
+        y += out  # out = bf16-rounded part (f32), added in y's dtype
 
 
 def paper_matvec_device(dm: DeviceMatrix, dic: Dictionary, x, y, trace=None, stream=None) -> None:

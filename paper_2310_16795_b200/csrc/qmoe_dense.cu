@@ -34,10 +34,7 @@ using namespace qmoe_dev;
 
 namespace {
 
-constexpr int DTHREADS = 512;
-constexpr int DWARPS = DTHREADS / 32;
-constexpr int BM = DTHREADS;  // rows per item (thread = row)
-constexpr int BK = 64;        // columns per chunk (128-byte bf16 rows)
+constexpr int BK = 64;  // columns per chunk (128-byte bf16 rows)
 
 extern __shared__ __align__(128) uint8_t dsm[];
 
@@ -56,7 +53,6 @@ struct DenseParams {
   int64_t ldy;
   int w_off, x_off, plan_off;  // byte offsets in dynamic shared memory
   int cp_log2;                 // column-point granularity the matrices store (qmoe_colpoints)
-  int dbg;                     // experiment switches (QMOE_DENSE_DBG): 1 skip mma, 2 skip decode
 };
 
 __device__ __forceinline__ uint32_t sbase() {
@@ -140,284 +136,6 @@ __device__ __forceinline__ uint4 x_chunk8_cols(const void* x, int bf16, int64_t 
   uint32_t w[4] = {0u, 0u, 0u, 0u};  // the row's tail: element loads, nothing past the row
   for (int e = 0; e < valid; ++e) w[e >> 1] |= (uint32_t)x_bf16_bits(x, bf16, i + e) << (16 * (e & 1));
   return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-// ROWS rows per item (ROWS / 128 UMMA row blocks, DTHREADS / ROWS lanes per
-// row), KC columns per chunk (KC / 64 SW128 blocks).
-template <int BN, int ROWS, int KC>
-__global__ void __launch_bounds__(DTHREADS, 1) dense_tc_kernel(DenseParams P) {
-  constexpr int DT_ROWS = ROWS, DT_KC = KC, DT_LPR = DTHREADS / ROWS, MB = ROWS / 128, KB = KC / 64;
-  __shared__ __align__(8) uint64_t tab_bar, mma_bar;
-  __shared__ int s_total;
-  __shared__ uint32_t s_tmem;
-  __shared__ int s_tok[64];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t base = sbase();
-  const uint32_t tab_s = base;
-  const uint32_t w_s = (base + P.w_off + 1023u) & ~1023u;   // 4 blocks x 16 KB, 1 KB aligned
-  const uint32_t x_s = w_s + (uint32_t)KB * DT_ROWS * 128u;  // KB blocks x BN x 128 B
-  int* start = reinterpret_cast<int*>(dsm + P.plan_off);
-  int* ipre = start + P.E + 1;
-  const int E = P.E;
-  const int nrb = (P.rows + DT_ROWS - 1) / DT_ROWS;
-  const int nk = (P.cols + DT_KC - 1) / DT_KC;  // chunks
-  const int nb = ((P.cols + (1 << P.cp_log2) - 1) >> P.cp_log2) - 1;  // stored column points per row
-  const int cps = DT_KC >> P.cp_log2;  // stored points per chunk
-  constexpr uint32_t TMEM_COLS = MB * BN < 32 ? 32 : MB * BN;
-  const uint32_t tb_mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
-  const uint32_t mma_mb = (uint32_t)__cvta_generic_to_shared(&mma_bar);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 32) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_mb));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma_mb));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t bytes = (uint32_t)P.H * 4;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tb_mb), "r"(bytes) : "memory");
-    for (uint32_t o = 0; o < bytes; o += 32768u)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tab_s + o),
-          "l"(reinterpret_cast<const char*>(P.gtab) + o), "r"(min(32768u, bytes - o)), "r"(tb_mb)
-          : "memory");
-    int a = 0, it = 0;
-    for (int e = 0; e < E; ++e) {
-      const int c = __ldg(P.count + e);
-      start[e] = a;
-      ipre[e] = it;
-      a += c;
-      it += nrb * ((c + BN - 1) / BN);
-    }
-    start[E] = a;
-    ipre[E] = it;
-    s_total = it;
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  mbar_wait(tb_mb, 0);
-  const uint32_t tmem = s_tmem;
-  const int total = s_total;
-  const uint32_t H = (uint32_t)P.H;
-  const int rr = tid / DT_LPR, q = tid % DT_LPR;  // my row in the item, my quarter of its chunk
-  const uint32_t rx = (uint32_t)(rr & 7) << 4;    // SW128 chunk swizzle of my row
-  const uint32_t idesc = idesc_bf16_f32<BN>();
-  uint32_t mma_phase = 0;
-  constexpr int XV = BN * (DT_KC / 8) / DTHREADS;  // 16-byte x pieces per thread per chunk
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    int lo = 0, hi = E - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (ipre[mid] <= item) lo = mid;
-      else hi = mid - 1;
-    }
-    const int e = lo, local = item - ipre[e];
-    const int rb = local % nrb, tb = local / nrb;
-    const int cnt = start[e + 1] - start[e];
-    const int nt = min(BN, cnt - tb * BN);
-    const int tok0 = start[e] + tb * BN;
-    const qmoe_matrix& M = P.mats[2 * e + P.pass];
-    const uint16_t* cwp = M.cw;
-    const uint32_t* cpp = M.colpts;
-    const int r = rb * DT_ROWS + rr;
-    const bool valid = r < P.rows;
-    int s = 0, n = 0;
-    uint32_t wlo = 0, whi = 0;
-    if (valid) {
-      s = __ldg(M.row_off + r);
-      n = __ldg(M.row_off + r + 1) - s;
-      const uint32_t mm = __ldg(M.row_minmax + r);
-      wlo = mm & 0xFFFFu;
-      whi = mm >> 16;
-    }
-    if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
-    __syncthreads();
-    uint4 xr[XV];
-    auto load_x = [&](int k0) {
-#pragma unroll
-      for (int u = 0; u < XV; ++u) {
-        const int i = tid + u * DTHREADS, nn = i / (DT_KC / 8), c8 = i % (DT_KC / 8);
-        xr[u] = (nn < nt && k0 + c8 * 8 < P.cols)
-                    ? x_chunk8_cols(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8, P.cols - k0 - c8 * 8)
-                    : make_uint4(0u, 0u, 0u, 0u);
-      }
-    };
-    load_x(0);
-    for (int k = 0; k < nk; ++k) {
-      const int k0 = k * DT_KC;
-      if (k > 0) {  // the previous chunk's MMAs must be done reading W / X (the last chunk's are awaited below)
-        mbar_wait(mma_mb, mma_phase);
-        mma_phase ^= 1u;
-      }
-      // ---- x tile
-#pragma unroll
-      for (int u = 0; u < XV; ++u) {
-        const int i = tid + u * DTHREADS, nn = i / (DT_KC / 8), c8 = i % (DT_KC / 8);
-        const uint32_t a = x_s + (uint32_t)(c8 >> 3) * (BN * 128u) + (uint32_t)nn * 128u +
-                           ((uint32_t)((c8 & 7) ^ (nn & 7)) << 4);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(xr[u].x), "r"(xr[u].y), "r"(xr[u].z),
-                     "r"(xr[u].w));
-      }
-      if (k + 1 < nk) load_x(k0 + DT_KC);
-      // ---- W tile: zero my 128-byte slice (block q of my row), rotated so the
-      // lanes of a warp hit different banks
-#pragma unroll
-      for (int b = q; b < KB; b += DT_LPR) {
-        const uint32_t wrow = w_s + (uint32_t)b * (DT_ROWS * 128u) + (uint32_t)rr * 128u;
-#pragma unroll
-        for (int c16 = 0; c16 < 8; ++c16) sts_zero16(wrow + 16u * (uint32_t)((c16 + lane) & 7));
-      }
-      // ---- my share of the row's codewords for this chunk
-      int ia = 0, ca = 0, ib = n;
-      if (valid) {
-        if (k > 0) {
-          const uint32_t pa = __ldg(cpp + (size_t)r * nb + k * cps - 1);
-          ia = (int)(pa >> 16);
-          ca = (int)(pa & 0xFFFFu);
-        }
-        if (k + 1 < nk) ib = min(n, (int)(__ldg(cpp + (size_t)r * nb + (k + 1) * cps - 1) >> 16) + 1);
-      }
-      const int len = max(0, ib - ia);
-      const int p0 = ia + (q * len) / DT_LPR, p1 = ia + ((q + 1) * len) / DT_LPR;
-      // pass 1: lengths, in blocks of 8 independent loads + lookups; the first
-      // block's entries stay in registers for pass 2
-      uint32_t e0[8];
-      int sum = 0;
-      for (int pb = p0; pb < p1; pb += 8) {
-        uint32_t cc[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) cc[u] = pb + u < p1 ? (uint32_t)__ldg(cwp + s + pb + u) : 0u;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t en = pb + u < p1 ? (cc[u] < H ? lds_u32(tab_s + 4 * cc[u]) : __ldg(P.gtab + cc[u])) : 0u;
-          if (pb == p0) e0[u] = en;
-          sum += (int)(en >> 28) * 2;
-        }
-      }
-      int incl = sum;  // 4-lane inclusive scan (the lanes of a row are consecutive)
-#pragma unroll
-      for (int d = 1; d < DT_LPR; d <<= 1) {
-        const int v = __shfl_up_sync(FULL_MASK, incl, d, DT_LPR);
-        if (q >= d) incl += v;
-      }
-      int col = ca + incl - sum - k0;  // chunk-relative start column of my first codeword
-      // pass 2: the non-zero values
-      for (int pb = p0; pb < p1; pb += 8) {
-        uint32_t ee[8];
-        if (pb == p0) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) ee[u] = e0[u];
-        } else {
-          uint32_t cc[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) cc[u] = pb + u < p1 ? (uint32_t)__ldg(cwp + s + pb + u) : 0u;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            ee[u] = pb + u < p1 ? (cc[u] < H ? lds_u32(tab_s + 4 * cc[u]) : __ldg(P.gtab + cc[u])) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t en = ee[u];  // 0 past the part: no value, length 0
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
-            const int vk = col + (int)(f >> 2);
-            if (en != 0u && f != 0x7Fu && (unsigned)vk < (unsigned)DT_KC)
-              sts_u16(w_s + (uint32_t)(vk >> 6) * (DT_ROWS * 128u) + (uint32_t)rr * 128u +
-                          ((((uint32_t)vk & 63u) * 2u) ^ rx),
-                      ((en >> (24 + j)) & 1u) ? whi : wlo);
-          }
-          col += (int)(en >> 28) * 2;
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb) {
-#pragma unroll
-          for (int kb = 0; kb < KB; ++kb) {
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              const uint64_t da =
-                  sw128_desc(w_s + (uint32_t)kb * (DT_ROWS * 128u) + (uint32_t)mb * (128u * 128u) + (uint32_t)ks * 32u);
-              const uint64_t db = sw128_desc(x_s + (uint32_t)kb * (BN * 128u) + (uint32_t)ks * 32u);
-              const uint32_t accf = (k > 0 || kb > 0 || ks > 0) ? 1u : 0u;
-              asm volatile(
-                  "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
-                      tmem + (uint32_t)mb * BN),
-                  "l"(da), "l"(db), "r"(idesc), "r"(accf));
-            }
-          }
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mma_mb)
-                     : "memory");
-      }
-    }
-    mbar_wait(mma_mb, mma_phase);  // the item's last MMAs: accumulators final
-    mma_phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    {  // epilogue: warp -> (TMEM lane quarter = 32 rows, row block, column slice of tokens)
-      constexpr int SPL = 4 / MB;  // column slices per (row block, quarter)
-      constexpr int CW = BN / SPL;
-      uint32_t v[CW];
-      const int quarter = warp & 3, mbk = (warp >> 2) % MB, slice = (warp >> 2) / MB;
-      const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)mbk * BN + (uint32_t)slice * CW;
-      if (CW == 32) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8 % CW]), "=r"(v[9 % CW]), "=r"(v[10 % CW]), "=r"(v[11 % CW]), "=r"(v[12 % CW]),
-              "=r"(v[13 % CW]), "=r"(v[14 % CW]), "=r"(v[15 % CW]), "=r"(v[16 % CW]), "=r"(v[17 % CW]),
-              "=r"(v[18 % CW]), "=r"(v[19 % CW]), "=r"(v[20 % CW]), "=r"(v[21 % CW]), "=r"(v[22 % CW]),
-              "=r"(v[23 % CW]), "=r"(v[24 % CW]), "=r"(v[25 % CW]), "=r"(v[26 % CW]), "=r"(v[27 % CW]),
-              "=r"(v[28 % CW]), "=r"(v[29 % CW]), "=r"(v[30 % CW]), "=r"(v[31 % CW])
-            : "r"(ta));
-      } else if (CW == 16) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8 % CW]), "=r"(v[9 % CW]), "=r"(v[10 % CW]), "=r"(v[11 % CW]), "=r"(v[12 % CW]),
-              "=r"(v[13 % CW]), "=r"(v[14 % CW]), "=r"(v[15 % CW])
-            : "r"(ta));
-      } else {
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                       "=r"(v[7])
-                     : "r"(ta));
-      }
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int row = rb * DT_ROWS + mbk * 128 + 32 * quarter + lane;
-      if (row < P.rows) {
-#pragma unroll
-        for (int j = 0; j < CW; ++j) {
-          const int nn = slice * CW + j;
-          if (nn >= nt) break;
-          const int64_t t = s_tok[nn];
-          const float vv = bf16_round_dev(__uint_as_float(v[j]));
-          if (P.y_mode == QMOE_Y_RELU_BF16) {
-            reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(vv, 0.f)) >> 16);
-          } else if (P.y_mode == QMOE_Y_STORE_F32) {
-            reinterpret_cast<float*>(P.y)[t * P.ldy + row] = vv + 0.f;
-          } else {
-            float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
-            *yp = *yp + vv;
-          }
-        }
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // TMEM read before the next item's first MMA; token ids reused
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
 // ------------------------------------------------------------------ row-walk kernel (v3)
@@ -734,7 +452,6 @@ __global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
-bool al16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
 
 }  // namespace
 
@@ -768,88 +485,34 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.ldy = ldy;
   const int BN = tokens_per_block;
   P.cp_log2 = 7;  // DeviceMatrix.build_colpoints: 128-column points
-  P.dbg = getenv("QMOE_DENSE_DBG") ? atoi(getenv("QMOE_DENSE_DBG")) : 0;
-  if (!getenv("QMOE_DENSE_V2")) {  // row-walk kernel
-    // shape: rows per item (= threads) x columns per chunk x CTAs per SM; the
-    // hot table gets the rest of shared memory (its hit rate matters: the
-    // codeword ranks are spread, 16K entries cover ~80%, 32K ~91%)
-    int RWR = 128, RWK = 64, RWB = 4;
-    if (const char* sh = getenv("QMOE_DENSE_RW")) sscanf(sh, "%dx%dx%d", &RWR, &RWK, &RWB);
-    const size_t wbytes = (size_t)RWR * RWK * 2 + 1024, xbytes = (size_t)(RWK / 64) * BN * 128;
-    const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
-    const size_t static_smem = 1024, per_cta = (size_t)d->max_smem_optin / RWB - (RWB > 1 ? 1024 : 0);
-    if (wbytes + xbytes + plan + static_smem + 4096 > per_cta)
-      return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts for the dense pass");
-    int H = (int)((per_cta - wbytes - xbytes - plan - static_smem) / 4);
-    H = std::min(H, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE) & ~255;
-    P.H = std::max(H, 256);
-    P.w_off = P.H * 4;
-    P.x_off = P.w_off + (int)wbytes;
-    P.plan_off = P.x_off + (int)xbytes;
-    const size_t smem = (size_t)P.plan_off + plan;
-    const int grid = RWB * d->num_sms;
-#define QMOE_RW_LAUNCH(BNv, Rv, Kv, Bv)                                                                        \
-  do {                                                                                                       \
-    CK(cudaFuncSetAttribute(dense_rw_kernel<BNv, Rv, Kv, Bv>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                            (int)smem),                                                                      \
-       "attr");                                                                                              \
-    dense_rw_kernel<BNv, Rv, Kv, Bv><<<grid, Rv, smem, S(stream)>>>(P);                                      \
-  } while (0)
-    auto is = [&](int r, int k, int b) { return RWR == r && RWK == k && RWB == b; };
-    if (BN == 64) {
-      if (is(512, 64, 1)) QMOE_RW_LAUNCH(64, 512, 64, 1);
-      else if (is(512, 128, 1)) QMOE_RW_LAUNCH(64, 512, 128, 1);
-      else if (is(256, 128, 2)) QMOE_RW_LAUNCH(64, 256, 128, 2);
-      else if (is(256, 64, 2)) QMOE_RW_LAUNCH(64, 256, 64, 2);
-      else if (is(256, 64, 3)) QMOE_RW_LAUNCH(64, 256, 64, 3);
-      else if (is(128, 64, 4)) QMOE_RW_LAUNCH(64, 128, 64, 4);
-      else return qmoe::fail(QMOE_EINVAL, "QMOE_DENSE_RW: unknown shape");
-    } else {
-      if (is(512, 64, 1)) QMOE_RW_LAUNCH(32, 512, 64, 1);
-      else if (is(512, 128, 1)) QMOE_RW_LAUNCH(32, 512, 128, 1);
-      else if (is(256, 128, 2)) QMOE_RW_LAUNCH(32, 256, 128, 2);
-      else if (is(256, 64, 2)) QMOE_RW_LAUNCH(32, 256, 64, 2);
-      else if (is(256, 64, 3)) QMOE_RW_LAUNCH(32, 256, 64, 3);
-      else if (is(128, 64, 4)) QMOE_RW_LAUNCH(32, 128, 64, 4);
-      else return qmoe::fail(QMOE_EINVAL, "QMOE_DENSE_RW: unknown shape");
-    }
-#undef QMOE_RW_LAUNCH
-    CK(cudaGetLastError(), "dense_rw_kernel launch");
-    return QMOE_OK;
-  }
-  // v2 (QMOE_DENSE_V2): 128 rows x 256-column chunks (4 lanes per row) or 256 x 128 (QMOE_DENSE_SHAPE)
-  const bool tall = getenv("QMOE_DENSE_SHAPE") && std::string(getenv("QMOE_DENSE_SHAPE")) == "256x128";
-  const int R = tall ? 256 : 128, KC = tall ? 128 : 256;  // rows per item x columns per chunk
-  const size_t wbytes = (size_t)R * KC * 2 + 1024, xbytes = (size_t)(KC / 64) * BN * 128;  // + 1 KB: SW128 alignment
+  // row-walk kernel: 128 rows per item (= threads) x 64-column chunks x 4
+  // CTAs per SM (measured best of 128/256/512 x 64/128 x 1-4); the hot table
+  // gets the rest of shared memory (its hit rate matters: the codeword ranks
+  // are spread, 16K entries cover ~80%, 32K ~91%)
+  constexpr int RWR = 128, RWK = 64, RWB = 4;
+  const size_t wbytes = (size_t)RWR * RWK * 2 + 1024, xbytes = (size_t)(RWK / 64) * BN * 128;
   const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
-  const size_t static_smem = 1024;
-  if (wbytes + xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
+  const size_t static_smem = 1024, per_cta = (size_t)d->max_smem_optin / RWB - (RWB > 1 ? 1024 : 0);
+  if (wbytes + xbytes + plan + static_smem + 4096 > per_cta)
     return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts for the dense pass");
-  int H = (int)((d->max_smem_optin - wbytes - xbytes - plan - static_smem) / 4);
+  int H = (int)((per_cta - wbytes - xbytes - plan - static_smem) / 4);
   H = std::min(H, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE) & ~255;
-  H = std::max(H, 256);
-  P.H = H;
-  P.w_off = H * 4;
+  P.H = std::max(H, 256);
+  P.w_off = P.H * 4;
   P.x_off = P.w_off + (int)wbytes;
   P.plan_off = P.x_off + (int)xbytes;
   const size_t smem = (size_t)P.plan_off + plan;
-  const int grid = d->num_sms;
-#define QMOE_DENSE_LAUNCH(BNv, Rv, KCv)                                                                      \
-  do {                                                                                                     \
-    CK(cudaFuncSetAttribute(dense_tc_kernel<BNv, Rv, KCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), \
-       "attr");                                                                                            \
-    dense_tc_kernel<BNv, Rv, KCv><<<grid, DTHREADS, smem, S(stream)>>>(P);                                 \
-  } while (0)
-  if (tall) {
-    if (BN == 64) QMOE_DENSE_LAUNCH(64, 256, 128);
-    else QMOE_DENSE_LAUNCH(32, 256, 128);
+  const int grid = RWB * d->num_sms;
+  if (BN == 64) {
+    CK(cudaFuncSetAttribute(dense_rw_kernel<64, RWR, RWK, RWB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem), "attr");
+    dense_rw_kernel<64, RWR, RWK, RWB><<<grid, RWR, smem, S(stream)>>>(P);
   } else {
-    if (BN == 64) QMOE_DENSE_LAUNCH(64, 128, 256);
-    else QMOE_DENSE_LAUNCH(32, 128, 256);
+    CK(cudaFuncSetAttribute(dense_rw_kernel<32, RWR, RWK, RWB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem), "attr");
+    dense_rw_kernel<32, RWR, RWK, RWB><<<grid, RWR, smem, S(stream)>>>(P);
   }
-#undef QMOE_DENSE_LAUNCH
-  CK(cudaGetLastError(), "dense_moe_kernel launch");
-  (void)al16;
+  CK(cudaGetLastError(), "dense_rw_kernel launch");
   return QMOE_OK;
 }
 

@@ -77,6 +77,17 @@ __device__ __forceinline__ void flag_bad_row(int32_t* bad, int row) {
   }
 }
 
+// Row segments of the streaming kernels (kernel-private checkpoints): segment
+// j of a row [s, e) split in 2^lg starts at the equal split s + j*n/2^lg
+// rounded UP to a multiple of 8 codewords (a 16-byte group of the stream), so
+// only a row's first and last groups are shared with neighbouring rows.
+// Boundaries nest: seg_start(s, e, j, lg) == seg_start(s, e, 2j, lg + 1).
+__device__ __forceinline__ int seg_start(int s, int e, int j, int lg) {
+  if (j == 0) return s;
+  const int b = (s + ((j * (e - s)) >> lg) + 7) & ~7;
+  return b < e ? b : e;
+}
+
 // ================================================================ row walker
 // Warp-per-row decode schedule shared by decompress and the fused matvec.
 // A row's codewords are split into 32 contiguous lane segments of K = ceil(n/32)

@@ -393,11 +393,11 @@ __device__ __forceinline__ int4 block_scan_excl(int4 v, int4* wsum, int4* total)
   return make_int4(b.x + incl.x - v.x, b.y + incl.y - v.y, b.z + incl.z - v.z, b.w + incl.w - v.w);
 }
 
-// lanes per row of a run: the override, bounded (RAW) by the checkpoint
-// granularity the matrix stores (M.lg); PACKED matrices take any lg
+// lanes per row of a run: the override, bounded by the checkpoint
+// granularity the matrix stores (M.lg)
 __device__ __forceinline__ int plan_lg(const qmoe_matrix& M, int lg_over) {
   if (lg_over < 0) return M.lg;
-  return M.row_id ? lg_over : min(lg_over, M.lg);
+  return min(lg_over, M.lg);
 }
 
 __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restrict__ assign, int T, int E,
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(const int32_t* __restric
       U.ck = M.ck;
       U.row_id = M.row_id;
       const int rlg = plan_lg(M, pass ? lg_wo : lg_wi);
-      U.lg = M.row_id ? rlg : (rlg | (M.lg << 8));  // RAW: checkpoint stride in bits 8-15
+      U.lg = rlg | (M.lg << 8);  // checkpoint stride in bits 8-15
       U.cols = M.cols;
       U.row0 = 0;
       U.row1 = M.rows;
@@ -531,17 +531,19 @@ __global__ void remap_kernel(const uint16_t* __restrict__ in, int64_t n, const u
 __global__ void checkpoints_kernel(const uint32_t* __restrict__ tab, const uint16_t* __restrict__ cw,
                                    const int32_t* __restrict__ row_off, int64_t rows, int64_t cols, int lg,
                                    uint16_t* ck, int32_t* bad) {
+  // thread per row: the start column of segments 1 .. G-1 (qmoe_device.cuh
+  // seg_start: group-aligned boundaries)
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int G = 1 << lg;
-  const int s = __ldg(row_off + r), e = __ldg(row_off + r + 1), n = e - s;
-  int j = 1, next = G > 1 ? s + ((1 * n) >> lg) : e;
+  const int s = __ldg(row_off + r), e = __ldg(row_off + r + 1);
+  int j = 1, next = G > 1 ? seg_start(s, e, 1, lg) : e;
   int off = 0;
   for (int k = s; k < e; ++k) {
     while (j < G && k == next) {
       ck[r * (G - 1) + j - 1] = (uint16_t)min(off, 65535);
       ++j;
-      next = s + ((j * n) >> lg);
+      next = seg_start(s, e, j, lg);
     }
     off += int(__ldg(tab + __ldg(cw + k)) & 31u);
   }
@@ -550,35 +552,6 @@ __global__ void checkpoints_kernel(const uint32_t* __restrict__ tab, const uint1
     ++j;
   }
   if (off != cols && bad) {
-    atomicAdd(bad, 1);
-    atomicMin(bad + 1, (int)r);
-  }
-}
-
-// ================================================================ packed layout
-// qmoe_pack (include/qmoe.h): thread per sorted row copies the row's stream
-// into whole 8-codeword groups (padding with codeword 0 — entry 0, no value),
-// records the start column of every group, the row's levels and its id.
-__global__ void pack_kernel(const uint32_t* __restrict__ tab, const uint16_t* __restrict__ cw,
-                            const int32_t* __restrict__ row_off, const uint32_t* __restrict__ mm, int64_t rows,
-                            int64_t cols, const int32_t* __restrict__ order, const int32_t* __restrict__ gstart,
-                            uint16_t* __restrict__ pcw, uint32_t* __restrict__ pmm, uint16_t* __restrict__ pck,
-                            uint16_t* __restrict__ rid, int32_t* bad) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
-  const int r = order[i];
-  const int s = row_off[r], n = row_off[r + 1] - s;
-  const int g0 = gstart[i], m = gstart[i + 1] - g0;
-  pmm[i] = mm[r];
-  rid[i] = (uint16_t)r;
-  int off = 0;
-  for (int k = 0; k < 8 * m; ++k) {
-    const uint16_t c = k < n ? cw[s + k] : (uint16_t)0;
-    pcw[(int64_t)8 * g0 + k] = c;
-    if ((k & 7) == 0) pck[g0 + (k >> 3)] = (uint16_t)min(off, 65535);
-    if (k < n) off += int(__ldg(tab + c) & 31u);
-  }
-  if ((off != cols || m != (n + 7) / 8) && bad) {
     atomicAdd(bad, 1);
     atomicMin(bad + 1, (int)r);
   }
@@ -776,21 +749,6 @@ int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matr
                                                  d_runs_wo, d_n,
                                                  d_expert_count, d_order, stage);
   CK(cudaGetLastError(), "moe_plan_kernel");
-  return QMOE_OK;
-}
-
-int qmoe_pack(qmoe_dict_t d, const uint32_t* d_table, const uint16_t* d_cw, const int32_t* d_row_off,
-              const uint32_t* d_mm, int64_t rows, int64_t cols, const int32_t* d_order, const int32_t* d_gstart,
-              uint16_t* d_pcw, uint32_t* d_pmm, uint16_t* d_pck, uint16_t* d_rid, int32_t* d_bad, void* stream) {
-  if (bad_dict(d) || rows < 0 || cols < 0 || cols > 65535 || rows > 65536 || !d_order || !d_gstart || !d_pcw ||
-      !d_pmm || !d_pck || !d_rid)
-    return qmoe::fail(QMOE_EINVAL, "bad argument (rows <= 65536, cols <= 65535)");
-  if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "packed layout needs a <=3-non-zero dictionary");
-  if (rows == 0) return QMOE_OK;
-  pack_kernel<<<(int)((rows + 127) / 128), 128, 0, S(stream)>>>(d_table ? d_table : d->d_mtab, d_cw, d_row_off, d_mm,
-                                                                 rows, cols, d_order, d_gstart, d_pcw, d_pmm, d_pck,
-                                                                 d_rid, d_bad);
-  CK(cudaGetLastError(), "pack_kernel");
   return QMOE_OK;
 }
 

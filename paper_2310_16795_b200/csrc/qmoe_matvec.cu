@@ -1,26 +1,27 @@
 // Fused dictionary-decode + matvec (codec.py:196-244 semantics) for sm_100a.
 //
-// seg_matvec_kernel — the product path for dictionaries whose entries hold
-// <= 3 non-zero values (the default p0 = 0.885 dictionary).
+// pipe_matvec_kernel — the product path for dictionaries whose entries hold
+// <= 3 non-zero values (the default p0 = 0.885 dictionary); the fused MoE
+// step (moe_step_kernel) runs the same walk in its wi and wo phases.
 //
 //   Work.  A launch walks a list of RUNS (qmoe_work): rows [row0, row1) of one
 //   compressed matrix applied to 1..2 tokens. A run is cut into TASKS of one
-//   warp each: 32 lanes = 32/G rows x G row SEGMENTS (G = 2^lg from the
-//   matrix's checkpoints; segment j of a row = codewords [s + j*n/G,
-//   s + (j+1)*n/G) starting at column ck[j]). The persistent grid (one
-//   1024-thread CTA per SM) splits the global task range evenly; a CTA stages
-//   the x rows of each run it touches once in shared memory (fp32; two tokens
-//   interleaved as float2) and its 32 warps stride over that run's tasks.
-//   Row metadata is read per lane; row sums are reduced over the G lanes of a
-//   row with shuffles (fixed order, deterministic) and bf16-rounded once
-//   (codec.py:243).
+//   warp each: 32 lanes = 32/G rows x G row SEGMENTS (G = 2^lg; segment
+//   boundaries group-aligned, seg_start in qmoe_device.cuh, start columns from
+//   the matrix's kernel-private checkpoints). The persistent grid (one
+//   768-thread CTA per SM) splits the global task range evenly; a CTA stages
+//   the x rows of a window of runs once in shared memory (fp32; two tokens
+//   interleaved as float2) and its warps claim that window's tasks
+//   dynamically. Row sums are reduced over the G lanes of a row with shuffles
+//   (fixed order, deterministic) and bf16-rounded once (codec.py:243).
 //
 //   Stream.  Each lane reads its segment in aligned 8-codeword (16-byte)
 //   groups with ld.global.nc.L1::no_allocate, two groups ahead of use.
-//   Codewords of a group outside the lane's segment are replaced by codeword
-//   0, whose entry (dictionary entry 0 = one zero pair; codebooks pin it to
-//   rank 0) has no non-zero value: the segment start column is pre-shifted by
-//   2 per masked leading codeword, masked trailing codewords add nothing.
+//   Codewords of a group outside the lane's segment (only a row's first and
+//   last group) are replaced by codeword 0, whose entry (dictionary entry 0 =
+//   one zero pair; codebooks pin it to rank 0) has no non-zero value: the
+//   segment start column is pre-shifted by 2 per masked leading codeword,
+//   masked trailing codewords add nothing.
 //
 //   Decode.  The entry table (variant 1 of the matvec tables, qmoe_internal.h)
 //   is byte-addressable: byte j = 4 * position of non-zero j (0x7F unused),
@@ -75,7 +76,6 @@ struct Run {
   const int32_t* ro;
   const uint32_t* mm;
   const uint16_t* ck;
-  const uint16_t* rid;  // PACKED layout when non-null
   int cols, row0, row1, lg, cklg, ntok, task0;
   int tok[NT_STREAM];
 };
@@ -90,7 +90,6 @@ __device__ __forceinline__ Run get_run(const SegParams& P, int r) {
     R.ro = W.row_off;
     R.mm = W.row_minmax;
     R.ck = W.ck;
-    R.rid = W.row_id;
     R.cols = W.cols;
     R.row0 = W.row0;
     R.row1 = W.row1;
@@ -105,7 +104,6 @@ __device__ __forceinline__ Run get_run(const SegParams& P, int r) {
     R.ro = P.single.row_off;
     R.mm = P.single.row_minmax;
     R.ck = nullptr;
-    R.rid = nullptr;
     R.cols = P.single.cols;
     R.row0 = 0;
     R.row1 = P.single.rows;
@@ -129,11 +127,11 @@ __device__ __forceinline__ uint64_t stream_policy() {
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ uint4 ld_group(const uint16_t* cw, int g) {
+__device__ __forceinline__ uint4 ld_group_ptr(const uint4* gp) {
   uint4 a;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
-               : "l"(cw + (size_t)g * GRP), "l"(stream_policy()));
+               : "l"(gp), "l"(stream_policy()));
   return a;
 }
 
@@ -199,7 +197,8 @@ __device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
 }
 
 // Entries of the 8 codewords of a group (lookup stage). MASKED: vm bit u set
-// = codeword u belongs to the lane's segment; the others decode as entry 0.
+// = codeword u belongs to the lane's segment; the others decode as entry 0
+// (one zero pair, no value: dictionary entry 0, pinned to rank 0 by codebooks).
 template <bool MASKED>
 __device__ __forceinline__ void lookup_group(uint32_t (&e)[GRP], const uint4 q, uint32_t vm, uint32_t tab_s,
                                              uint32_t H, const uint32_t* __restrict__ gtab) {
@@ -210,6 +209,12 @@ __device__ __forceinline__ void lookup_group(uint32_t (&e)[GRP], const uint4 q, 
     if (MASKED) c = ((vm >> u) & 1u) ? c : 0u;
     e[u] = c < H ? lds_u32(tab_s + 4 * c) : __ldg(gtab + c);
   }
+}
+__device__ __forceinline__ void lookup_any(uint32_t (&e)[GRP], const uint4 q, uint32_t vm, uint32_t tab_s, uint32_t H,
+                                           const uint32_t* __restrict__ gtab) {
+  // the masked variant only where some lane of the warp is at a row edge
+  if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(e, q, vm, tab_s, H, gtab);
+  else lookup_group<true>(e, q, vm, tab_s, H, gtab);
 }
 
 // Apply stage: per used slot one x gather + FMA. xa = shared address of x at
@@ -239,11 +244,6 @@ __device__ __forceinline__ void apply_group(const uint32_t (&e)[GRP], uint32_t& 
   }
 }
 
-__device__ __forceinline__ uint32_t seg_vm(int lo, int hi) {
-  const int l = max(0, lo), h = min(GRP, max(0, hi));
-  return ((1u << h) - 1u) & ~((1u << l) - 1u);
-}
-
 template <int NT>
 __device__ __forceinline__ void store_row(const SegParams& P, const Run& R, int row, const float (&sum)[NT]) {
 #pragma unroll
@@ -264,226 +264,21 @@ __device__ __forceinline__ void store_row(const SegParams& P, const Run& R, int 
   }
 }
 
-// PACKED layout task: 32 / G consecutive sorted rows x G segments of whole
-// groups; no masking (padding codewords decode to entry 0), lanes whose
-// segment is shorter than the warp's longest simply idle.
-template <int NT>
-__device__ __forceinline__ void run_task_packed(const SegParams& P, const Run& R, int task, uint32_t xs_s,
-                                                uint32_t tab_s) {
-  const int lane = threadIdx.x & 31;
-  const int lg = R.lg, G = 1 << lg;
-  const int i = R.row0 + (task << (5 - lg)) + (lane >> lg);
-  const int seg = lane & (G - 1);
-  int ga = 0, ng = 0, col = 0;
-  uint32_t mm = 0;
-  if (i < R.row1) {
-    const int gs = __ldg(R.ro + i), m = __ldg(R.ro + i + 1) - gs;
-    ga = gs + ((seg * m) >> lg);
-    ng = gs + (((seg + 1) * m) >> lg) - ga;
-    col = seg && ng ? (int)__ldg(R.ck + ga) : 0;
-    mm = __ldg(R.mm + i);
-  }
-  const int maxg = __reduce_max_sync(FULL_MASK, ng);
-  const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
-  uint32_t xa = xs_s + (uint32_t)col * (NT == 1 ? 4u : 8u);
-  float acc[3][NT];
-#pragma unroll
-  for (int j = 0; j < 3; ++j)
-#pragma unroll
-    for (int q = 0; q < NT; ++q) acc[j][q] = 0.f;
-  const uint32_t H = (uint32_t)P.H;
-  const uint32_t* gtab = P.gtab;
-  if (maxg > 0) {
-    // pipeline: group k+2 loading, group k+1 looked up, group k applied
-    const uint16_t* cw = R.cw;
-    const int glast = ga + max(ng, 1) - 1;
-    uint4 q1 = ld_group(cw, min(ga + 1, glast));
-    uint32_t ea[GRP], eb[GRP];
-    if (ng > 0) lookup_group<false>(ea, ld_group(cw, ga), 0xFFu, tab_s, H, gtab);
-    for (int k = 0;;) {
-      uint4 q2 = ld_group(cw, min(ga + k + 2, glast));
-      if (k + 1 < ng) lookup_group<false>(eb, q1, 0xFFu, tab_s, H, gtab);
-      if (k < ng) apply_group<NT>(ea, xa, lmin, lmax, acc);
-      if (++k >= maxg) break;
-      q1 = ld_group(cw, min(ga + k + 2, glast));
-      if (k + 1 < ng) lookup_group<false>(ea, q2, 0xFFu, tab_s, H, gtab);
-      if (k < ng) apply_group<NT>(eb, xa, lmin, lmax, acc);
-      if (++k >= maxg) break;
-    }
-  }
-  float sum[NT];
-#pragma unroll
-  for (int q = 0; q < NT; ++q) {
-    sum[q] = (acc[0][q] + acc[1][q]) + acc[2][q];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1)
-      if (d < G) sum[q] += __shfl_xor_sync(FULL_MASK, sum[q], d);
-  }
-  if (i >= R.row1 || seg != 0) return;
-  store_row<NT>(P, R, (int)__ldg(R.rid + i), sum);
-}
-
-template <int NT>
-__device__ __forceinline__ void run_task(const SegParams& P, const Run& R, int task, uint32_t xs_s, uint32_t tab_s) {
-  const int lane = threadIdx.x & 31;
-  const int lg = R.lg, G = 1 << lg;
-  const int r = R.row0 + (task << (5 - lg)) + (lane >> lg);
-  const int seg = lane & (G - 1);
-  int A = 0, B = 0, off = 0;
-  uint32_t mm = 0;
-  if (r < R.row1) {
-    const int s = __ldg(R.ro + r), e = __ldg(R.ro + r + 1);
-    const int n = e - s;
-    A = s + ((seg * n) >> lg);
-    B = s + (((seg + 1) * n) >> lg);
-    off = seg ? (int)__ldg(R.ck + (size_t)r * ((1 << R.cklg) - 1) + (seg << (R.cklg - lg)) - 1) : 0;
-    mm = __ldg(R.mm + r);
-  }
-  const bool has = B > A;
-  const int g0 = has ? A / GRP : 0;
-  const int glast = has ? (B - 1) / GRP : 0;
-  const int ng = has ? glast - g0 + 1 : 0;
-  const int maxg = __reduce_max_sync(FULL_MASK, ng);
-  const float lmin = __uint_as_float(mm << 16), lmax = __uint_as_float(mm & 0xFFFF0000u);
-  // masked leading codewords decode as entry 0 (z_bytes of columns, no value)
-  const uint32_t offb = (uint32_t)(off * 4) - (uint32_t)((A - g0 * GRP) * P.z_bytes);
-  uint32_t xa = xs_s + (NT == 1 ? offb : 2 * offb);
-  float acc[3][NT];
-#pragma unroll
-  for (int j = 0; j < 3; ++j)
-#pragma unroll
-    for (int q = 0; q < NT; ++q) acc[j][q] = 0.f;
-  const uint32_t H = (uint32_t)P.H;
-  const uint32_t* gtab = P.gtab;
-  if (maxg > 0) {
-    // pipeline: group i+2 loading, group i+1 looked up, group i applied
-    const uint16_t* cw = R.cw;
-    int lo = A - g0 * GRP, hi = B - g0 * GRP;  // segment in codewords relative to group i
-    uint4 q1 = ld_group(cw, min(g0 + 1, glast));
-    uint32_t ea[GRP], eb[GRP];
-    {
-      const uint4 q0 = ld_group(cw, g0);
-      const uint32_t vm = seg_vm(lo, hi);
-      if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(ea, q0, vm, tab_s, H, gtab);
-      else lookup_group<true>(ea, q0, vm, tab_s, H, gtab);
-    }
-    for (int i = 0;;) {
-      // groups past this lane's segment re-read its last group (mask 0)
-      uint4 q2 = ld_group(cw, min(g0 + i + 2, glast));
-      if (i + 1 < maxg) {
-        const uint32_t vm = seg_vm(lo - GRP, hi - GRP);
-        if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(eb, q1, vm, tab_s, H, gtab);
-        else lookup_group<true>(eb, q1, vm, tab_s, H, gtab);
-      }
-      apply_group<NT>(ea, xa, lmin, lmax, acc);
-      if (++i >= maxg) break;
-      lo -= GRP;
-      hi -= GRP;
-      q1 = ld_group(cw, min(g0 + i + 2, glast));
-      if (i + 1 < maxg) {
-        const uint32_t vm = seg_vm(lo - GRP, hi - GRP);
-        if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(ea, q2, vm, tab_s, H, gtab);
-        else lookup_group<true>(ea, q2, vm, tab_s, H, gtab);
-      }
-      apply_group<NT>(eb, xa, lmin, lmax, acc);
-      if (++i >= maxg) break;
-      lo -= GRP;
-      hi -= GRP;
-    }
-  }
-  float sum[NT];
-#pragma unroll
-  for (int q = 0; q < NT; ++q) {
-    sum[q] = (acc[0][q] + acc[1][q]) + acc[2][q];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1)
-      if (d < G) sum[q] += __shfl_xor_sync(FULL_MASK, sum[q], d);
-  }
-  if (r >= R.row1 || seg != 0) return;
-  store_row<NT>(P, R, r, sum);
-}
-
-template <bool PACKED>
-__global__ void __launch_bounds__(THREADS, 1) seg_matvec_kernel(SegParams P) {
-  uint32_t* tab = reinterpret_cast<uint32_t*>(seg_smem);
-  char* xs = reinterpret_cast<char*>(seg_smem + (size_t)P.H * 4);
-  __shared__ int s_run;
-
-  int n_runs, total;
-  if (P.runs) {
-    n_runs = min(P.n_runs[0], P.max_runs);
-    total = P.n_runs[1];
-  } else {
-    n_runs = (int)((P.ntok_single + NT_STREAM - 1) / NT_STREAM);
-    total = n_runs * run_tasks(P.single.rows, 0);
-  }
-  if (n_runs <= 0) return;
-  const int t_begin = (int)((int64_t)total * blockIdx.x / gridDim.x);
-  const int t_end = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
-  if (t_begin >= t_end) return;
-  {  // hot table prefix: vectorised copy by all threads
-    const uint4* src = reinterpret_cast<const uint4*>(P.gtab);
-    uint4* dst = reinterpret_cast<uint4*>(tab);
-    for (int i = threadIdx.x; i < P.H / 4; i += THREADS) dst[i] = __ldg(src + i);
-  }
-  if (threadIdx.x == 0) {  // run holding t_begin: last run with task0 <= t_begin
-    int lo = 0, hi = n_runs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (get_run(P, mid).task0 <= t_begin) lo = mid;
-      else hi = mid - 1;
-    }
-    s_run = lo;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  int t = t_begin;
-  for (int ri = s_run; ri < n_runs && t < t_end; ++ri) {
-    const Run R = get_run(P, ri);
-    const int r_end = R.task0 + run_tasks(R.row1 - R.row0, R.lg);
-    if (r_end <= t) continue;
-    const int a = t, b = min(t_end, r_end);
-    // stage x of the run's tokens as fp32 (two tokens interleaved)
-    __syncthreads();  // previous run's tasks are done with xs
-    if (R.ntok > 1) {
-      float2* x2 = reinterpret_cast<float2*>(xs);
-      for (int i = threadIdx.x; i < P.xcap; i += THREADS) {
-        float v0 = 0.f, v1 = 0.f;
-        if (i < R.cols) {
-          v0 = load_x(P.x, P.x_bf16, (int64_t)R.tok[0] * P.ldx + i);
-          v1 = load_x(P.x, P.x_bf16, (int64_t)R.tok[1] * P.ldx + i);
-        }
-        x2[i] = make_float2(v0, v1);
-      }
-    } else {
-      float* x1 = reinterpret_cast<float*>(xs);
-      for (int i = threadIdx.x; i < P.xcap; i += THREADS)
-        x1[i] = i < R.cols ? load_x(P.x, P.x_bf16, (int64_t)R.tok[0] * P.ldx + i) : 0.f;
-    }
-    __syncthreads();
-    const uint32_t tab_s = smem_base(), xs_s = tab_s + (uint32_t)P.H * 4;
-    for (int k = a + warp; k < b; k += NWARPS) {
-      if (PACKED) {
-        if (R.ntok > 1) run_task_packed<2>(P, R, k - R.task0, xs_s, tab_s);
-        else run_task_packed<1>(P, R, k - R.task0, xs_s, tab_s);
-      } else {
-        if (R.ntok > 1) run_task<2>(P, R, k - R.task0, xs_s, tab_s);
-        else run_task<1>(P, R, k - R.task0, xs_s, tab_s);
-      }
-    }
-    t = b;
-  }
-}
-
-// ----------------------------------------------------------------- pipelined raw kernel
-// pipe_matvec_kernel — the RAW-layout product path. Same decode/apply stages
-// as above, but each warp treats the lane segments of its successive tasks as
-// ONE continuous stream of codeword groups: the next task's row metadata is
-// loaded a whole task ahead, and its first groups are loaded and looked up
-// during the current task's last steps, so no task pays a dependent DRAM
-// round trip at its start. A CTA stages the x rows of every run of its task
-// range up front (a window of up to WIN_RUNS runs / the x budget), so there is
-// no barrier between runs inside a window.
+// ----------------------------------------------------------------- pipelined streaming walk
+// pipe_matvec_kernel / the fused step's phases. A CTA stages the x rows of
+// every run of its task range up front (a window of up to WIN_RUNS runs / the
+// x budget), so there is no barrier between runs inside a window; each warp
+// claims TASKS (32/G rows x G segments of one run) and treats the lane
+// segments of its successive tasks as ONE continuous stream of codeword
+// groups: the next task's row metadata is loaded a whole task ahead, and its
+// first groups are loaded and looked up during the current task's last
+// steps, so no task pays a dependent DRAM round trip at its start.
+//
+// Segments (kernel-private layout, qmoe_checkpoints): segment j of a row
+// [s, e) split in G = 2^lg starts at codeword seg_start(s, e, j, lg) — the
+// equal split s + j*n/G rounded UP to a multiple of 8 codewords, so only the
+// row's first and last 16-byte groups are shared with neighbouring rows (no
+// partial groups inside a row), and the boundaries nest across lg.
 constexpr int WIN_RUNS = 16;
 constexpr int WARP_PLAN_MAX = 256;  // fused step: single-warp dispatcher plan up to this many tokens
 
@@ -497,51 +292,51 @@ struct WinRun {
 };
 
 struct Lane {  // one lane's segment of one task
-  int A, B, off, row;
+  const uint4* gp;  // first group
+  int ng;           // groups (0: nothing)
+  uint32_t xoffb;   // x byte offset of the first group's first codeword (NT = 1 units)
+  uint32_t vmm;     // codeword masks of the first (bits 0-7) and last (bits 8-15) group
+  int row;          // output row (-1: none)
   uint32_t mm;
 };
 
-__device__ __forceinline__ Lane lane_task(const WinRun& W, int k) {
+__device__ __forceinline__ Lane lane_task(const WinRun& W, int k, int z_bytes) {
   const int lane = threadIdx.x & 31;
-  const int lg = W.lg, G = 1 << lg;
+  const int lg = W.lg;
   const int r = W.row0 + ((k - W.task0) << (5 - lg)) + (lane >> lg);
-  const int seg = lane & (G - 1);
-  Lane L{0, 0, 0, -1, 0u};
+  const int seg = lane & ((1 << lg) - 1);
+  Lane L{reinterpret_cast<const uint4*>(W.cw), 0, 0u, 0u, -1, 0u};
   if (r < W.row1) {
     const int s = __ldg(W.ro + r), e = __ldg(W.ro + r + 1);
-    const int n = e - s;
-    L.A = s + ((seg * n) >> lg);
-    L.B = s + (((seg + 1) * n) >> lg);
-    L.off = seg ? (int)__ldg(W.ck + (size_t)r * ((1 << W.cklg) - 1) + (seg << (W.cklg - lg)) - 1) : 0;
+    const int A = seg_start(s, e, seg, lg), B = seg_start(s, e, seg + 1, lg);
+    const int off = seg ? (int)__ldg(W.ck + (size_t)r * ((1 << W.cklg) - 1) + (seg << (W.cklg - lg)) - 1) : 0;
     L.mm = __ldg(W.mm + r);
     L.row = r;
+    if (B > A) {
+      const int g0 = A >> 3;
+      L.gp = reinterpret_cast<const uint4*>(W.cw) + g0;
+      L.ng = ((B - 1) >> 3) - g0 + 1;
+      // masked leading codewords decode as entry 0 (z_bytes of columns each)
+      L.xoffb = (uint32_t)(off * 4) - (uint32_t)((A & 7) * z_bytes);
+      L.vmm = ((0xFFu << (A & 7)) & 0xFFu) | ((0xFFu >> ((8 - (B & 7)) & 7)) << 8);
+    }
   }
   return L;
 }
 
-__device__ __forceinline__ int lane_groups(const Lane& L) { return L.B > L.A ? (L.B - 1) / GRP - L.A / GRP + 1 : 0; }
-
-__device__ __forceinline__ uint4 lane_load(const uint16_t* cw, const Lane& L, int i) {
-  if (L.B <= L.A) return make_uint4(0u, 0u, 0u, 0u);
-  const int g0 = L.A / GRP, gl = (L.B - 1) / GRP;
-  return ld_group(cw, min(g0 + i, gl));
+__device__ __forceinline__ uint4 lane_load(const Lane& L, int i) {
+  // groups past the lane's segment re-read its last group (masked to nothing)
+  return ld_group_ptr(L.gp + max(0, min(i, L.ng - 1)));
 }
 
 __device__ __forceinline__ uint32_t lane_vm(const Lane& L, int i) {
-  const int base = (L.A / GRP + i) * GRP;
-  return seg_vm(L.A - base, L.B - base);
+  uint32_t vm = i == 0 ? L.vmm & 0xFFu : 0xFFu;
+  if (i == L.ng - 1) vm &= L.vmm >> 8;
+  return i < L.ng ? vm : 0u;
 }
 
-__device__ __forceinline__ void lookup_any(uint32_t (&e)[GRP], const uint4 q, uint32_t vm, uint32_t tab_s, uint32_t H,
-                                           const uint32_t* __restrict__ gtab) {
-  if (__all_sync(FULL_MASK, vm == 0xFFu)) lookup_group<false>(e, q, vm, tab_s, H, gtab);
-  else lookup_group<true>(e, q, vm, tab_s, H, gtab);
-}
-
-// Run sources of pipe_range: the device run list of a grouped launch, or the
-// per-CTA shared-memory plan of the fused MoE step.
-// What the (serial) window builder needs of a run; the pointers are filled
-// afterwards, one thread per run of the window, so their loads overlap.
+// What the window builder needs of a run; the pointers are filled
+// afterwards, one lane per run of the window, so their loads overlap.
 struct RunMeta {
   int task0, task1, ntok, cols;
 };
@@ -624,6 +419,71 @@ __device__ __forceinline__ void trace_stamp(unsigned long long* trace, int k) {
   }
 }
 
+// One step of a warp's group stream: apply `cur` (group i of the current
+// task), look up the next group into `nxt`, load the one after into q2.
+template <int NT>
+__device__ __forceinline__ void walk_step(const uint32_t (&cur)[GRP], uint32_t (&nxt)[GRP], uint32_t& xa, float lmin,
+                                          float lmax, float (&acc)[3][2], uint4 q1, uint32_t vm_next, uint32_t tab_s,
+                                          uint32_t H, const uint32_t* __restrict__ gtab) {
+  lookup_any(nxt, q1, vm_next, tab_s, H, gtab);
+  if (NT == 1) {
+    float a1[3][1] = {{acc[0][0]}, {acc[1][0]}, {acc[2][0]}};
+    apply_group<1>(cur, xa, lmin, lmax, a1);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) acc[j][0] = a1[j][0];
+  } else {
+    apply_group<2>(cur, xa, lmin, lmax, acc);
+  }
+}
+
+// The task walk of one warp for NT tokens per run: groups 0..maxg-1 of task
+// c (entries of group 0 in ea, raw group 1 — or the next task's group 0 when
+// maxg < 2 — in q1), prefetching the next task's first groups at the end.
+// Returns with ea = entries of the next task's group 0 and q1 = its raw
+// group 1 (or the task after's group 0) when has_n.
+template <int NT>
+__device__ __forceinline__ void walk_task(const Lane& c, int maxgc, const Lane& n, bool has_n, int& maxgn,
+                                          bool& nready, uint32_t (&ea)[GRP], uint4& q1, uint32_t xa,
+                                          float (&sum)[2], uint32_t tab_s, uint32_t H,
+                                          const uint32_t* __restrict__ gtab) {
+  const float lmin = __uint_as_float(c.mm << 16), lmax = __uint_as_float(c.mm & 0xFFFF0000u);
+  float acc[3][2];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) acc[j][0] = acc[j][1] = 0.f;
+  uint32_t eb[GRP];
+  // raw element i + 2 of the stream (this task, then the next)
+  auto prefetch = [&](int i) -> uint4 {
+    if (i + 2 < maxgc) return lane_load(c, i + 2);
+    if (has_n) {
+      if (!nready) {
+        maxgn = __reduce_max_sync(FULL_MASK, n.ng);
+        nready = true;
+      }
+      if (i + 2 - maxgc < maxgn) return lane_load(n, i + 2 - maxgc);
+    }
+    return make_uint4(0u, 0u, 0u, 0u);
+  };
+  auto vm_of = [&](int i) -> uint32_t {  // mask of element i + 1
+    return i + 1 < maxgc ? lane_vm(c, i + 1) : lane_vm(n, 0);
+  };
+  int i = 0;
+  for (;;) {  // two elements per trip: no register rotation between the entry buffers
+    uint4 q2 = prefetch(i);
+    walk_step<NT>(ea, eb, xa, lmin, lmax, acc, q1, (i + 1 < maxgc || has_n) ? vm_of(i) : 0u, tab_s, H, gtab);
+    if (++i >= maxgc) {
+      q1 = q2;
+#pragma unroll
+      for (int u = 0; u < GRP; ++u) ea[u] = eb[u];  // once per task
+      break;
+    }
+    q1 = prefetch(i);
+    walk_step<NT>(eb, ea, xa, lmin, lmax, acc, q2, (i + 1 < maxgc || has_n) ? vm_of(i) : 0u, tab_s, H, gtab);
+    if (++i >= maxgc) break;
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) sum[q] = (acc[0][q] + acc[1][q]) + acc[2][q];
+}
+
 // Walk global tasks [t_begin, t_end) of the runs `src` provides (task0
 // ascending): windows of runs whose x slots fit P.xbytes are staged at once,
 // then every warp walks its tasks with the cross-task pipeline.
@@ -638,9 +498,9 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
   }
   const uint32_t xs_s = tab_s + (uint32_t)P.H * 4;
   char* xs = reinterpret_cast<char*>(seg_smem + (size_t)P.H * 4);
-  const int warp = threadIdx.x >> 5;
   const uint32_t H = (uint32_t)P.H;
   const uint32_t* gtab = P.gtab;
+  const int z_bytes = P.z_bytes;
   WinRun* win = S.win;
   int t = t_begin;
   bool first = true;
@@ -718,28 +578,28 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     const bool active = k < wend;
     int wc = 0, wn = 0, kn = 0, maxgc = 0, maxgn = 0;
     bool has_n = false, nready = false;
-    Lane c{0, 0, 0, -1, 0u}, n{0, 0, 0, -1, 0u};
-    uint32_t ea[GRP], eb[GRP];
+    Lane c{nullptr, 0, 0u, 0u, -1, 0u}, n{nullptr, 0, 0u, 0u, -1, 0u};
+    uint32_t ea[GRP];
     uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = make_uint4(0u, 0u, 0u, 0u);
     if (active) {  // first tasks' row metadata: needs no x
       while (win[wc].task1 <= k) ++wc;
-      c = lane_task(win[wc], k);
+      c = lane_task(win[wc], k, z_bytes);
       wn = wc;
       kn = claim_task(&S.next);
       has_n = kn < wend;
       if (has_n) {
         while (win[wn].task1 <= kn) ++wn;
-        n = lane_task(win[wn], kn);
+        n = lane_task(win[wn], kn, z_bytes);
       }
     }
     // wi: the x rows are ready — their loads go out together with the
     // metadata loads above (one round trip for both)
     if (!COHERENT_X) stage_x();
     if (active) {  // first codeword groups
-      maxgc = __reduce_max_sync(FULL_MASK, lane_groups(c));
-      q0 = lane_load(win[wc].cw, c, 0);
-      if (maxgc >= 2) q1 = lane_load(win[wc].cw, c, 1);
-      else q1 = has_n ? lane_load(win[wn].cw, n, 0) : make_uint4(0u, 0u, 0u, 0u);
+      maxgc = __reduce_max_sync(FULL_MASK, c.ng);
+      q0 = lane_load(c, 0);
+      if (maxgc >= 2) q1 = lane_load(c, 1);
+      else q1 = has_n ? lane_load(n, 0) : make_uint4(0u, 0u, 0u, 0u);
     }
     if (tab_bar) {
       table_fill_wait(tab_bar);
@@ -761,47 +621,18 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
     if (active) {
       for (;;) {
         const WinRun& W = win[wc];
-        const int NTc = W.ntok > 1 ? 2 : 1;
-        const float lmin = __uint_as_float(c.mm << 16), lmax = __uint_as_float(c.mm & 0xFFFF0000u);
-        const uint32_t offb = (uint32_t)(c.off * 4) - (uint32_t)((c.A - (c.A / GRP) * GRP) * P.z_bytes);
-        uint32_t xa = xs_s + (uint32_t)W.xoff + (NTc == 1 ? offb : 2 * offb);
-        float acc[3][2];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) acc[j][0] = acc[j][1] = 0.f;
-        for (int i = 0; i < maxgc; ++i) {
-          // prefetch element i + 2 of the stream (this task, then the next)
-          uint4 q2 = make_uint4(0u, 0u, 0u, 0u);
-          if (i + 2 < maxgc) {
-            q2 = lane_load(W.cw, c, i + 2);
-          } else if (has_n) {
-            if (!nready) {
-              maxgn = __reduce_max_sync(FULL_MASK, lane_groups(n));
-              nready = true;
-            }
-            if (i + 2 - maxgc < maxgn) q2 = lane_load(win[wn].cw, n, i + 2 - maxgc);
-          }
-          // look element i + 1 up (raw in q1)
-          if (i + 1 < maxgc) lookup_any(eb, q1, lane_vm(c, i + 1), tab_s, H, gtab);
-          else if (has_n) lookup_any(eb, q1, lane_vm(n, 0), tab_s, H, gtab);
-          // apply element i
-          if (NTc == 1) {
-            float a1[3][1] = {{acc[0][0]}, {acc[1][0]}, {acc[2][0]}};
-            apply_group<1>(ea, xa, lmin, lmax, a1);
-#pragma unroll
-            for (int j = 0; j < 3; ++j) acc[j][0] = a1[j][0];
-          } else {
-            apply_group<2>(ea, xa, lmin, lmax, acc);
-          }
-#pragma unroll
-          for (int u = 0; u < GRP; ++u) ea[u] = eb[u];
-          q1 = q2;
+        float sum[2];
+        if (W.ntok > 1) {
+          const uint32_t xa = xs_s + (uint32_t)W.xoff + 2 * c.xoffb;
+          walk_task<2>(c, maxgc, n, has_n, maxgn, nready, ea, q1, xa, sum, tab_s, H, gtab);
+        } else {
+          const uint32_t xa = xs_s + (uint32_t)W.xoff + c.xoffb;
+          walk_task<1>(c, maxgc, n, has_n, maxgn, nready, ea, q1, xa, sum, tab_s, H, gtab);
         }
         // row sums over the G lanes of a row (fixed order), bf16 epilogue
-        float sum[2];
         const int G = 1 << W.lg;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          sum[q] = (acc[0][q] + acc[1][q]) + acc[2][q];
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1)
             if (d < G) sum[q] += __shfl_xor_sync(FULL_MASK, sum[q], d);
@@ -815,7 +646,7 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
         }
         if (!has_n) break;
         // advance: next becomes current; load the task after it
-        if (!nready) maxgn = __reduce_max_sync(FULL_MASK, lane_groups(n));
+        if (!nready) maxgn = __reduce_max_sync(FULL_MASK, n.ng);
         c = n;
         wc = wn;
         maxgc = maxgn;
@@ -825,11 +656,11 @@ __device__ __forceinline__ void pipe_range(const SegParams& P, const Src& src, i
         nready = false;
         if (has_n) {
           while (win[wn].task1 <= kn) ++wn;
-          n = lane_task(win[wn], kn);
+          n = lane_task(win[wn], kn, z_bytes);
         }
         // pipeline invariant: ea = entries(c, 0); q1 = raw(c, 1) if maxgc >= 2,
         // else raw(next, 0) — not prefetched yet in that case
-        if (maxgc < 2) q1 = has_n ? lane_load(win[wn].cw, n, 0) : make_uint4(0u, 0u, 0u, 0u);
+        if (maxgc < 2) q1 = has_n ? lane_load(n, 0) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
     t = wend;
@@ -886,7 +717,6 @@ struct PlanRuns {
     R.ro = M.row_off;
     R.mm = M.row_minmax;
     R.ck = M.ck;
-    R.rid = nullptr;
     R.cols = M.cols;
     R.row0 = 0;
     R.row1 = M.rows;
@@ -1299,42 +1129,23 @@ unsigned long long* g_trace_host = nullptr;  // qmoe_debug_step_trace buffer (de
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int hot_override() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("QMOE_HOT_ENTRIES");
-    v = e ? atoi(e) : -1;
-  }
-  return v;
-}
-
-int launch_seg(const qmoe_dict* d, SegParams& P, bool packed, int max_cols, int ntmax, int grid, int hot_want,
-               cudaStream_t st) {
+int launch_seg(const qmoe_dict* d, SegParams& P, int max_cols, int ntmax, int grid, int hot_want, cudaStream_t st) {
   P.xcap = ((max_cols + 32 + 15) / 16) * 16;
   const size_t slot = (size_t)std::max(1, ntmax) * P.xcap * 4;
   // the pipelined kernel stages several runs' x at once (up to ~48 KB)
-  const size_t xbytes = packed || getenv("QMOE_SEG_V1") ? slot : std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
+  const size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
   P.xbytes = (int)xbytes;
   const size_t static_smem = 2048;  // kernels' static __shared__ (run window)
   if (xbytes + static_smem + 4096 > (size_t)d->max_smem_optin)
     return qmoe::fail(QMOE_EUNSUPPORTED, "cols too large for the shared-memory x staging buffer");
   int H = (int)((d->max_smem_optin - xbytes - static_smem - 256) / 4);
-  if (hot_override() >= 0) hot_want = hot_override();
   H = std::min(H, std::min(hot_want, QMOE_DICT_SIZE));
   H = std::max(H & ~255, 256);
   P.H = H;
   const size_t smem = (size_t)H * 4 + xbytes;
-  if (packed) {
-    CK(cudaFuncSetAttribute(seg_matvec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    seg_matvec_kernel<true><<<grid, THREADS, smem, st>>>(P);
-  } else if (getenv("QMOE_SEG_V1")) {
-    CK(cudaFuncSetAttribute(seg_matvec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    seg_matvec_kernel<false><<<grid, THREADS, smem, st>>>(P);
-  } else {
-    CK(cudaFuncSetAttribute(pipe_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    pipe_matvec_kernel<<<grid, THREADS, smem, st>>>(P);
-  }
-  CK(cudaGetLastError(), "seg_matvec_kernel launch");
+  CK(cudaFuncSetAttribute(pipe_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+  pipe_matvec_kernel<<<grid, THREADS, smem, st>>>(P);
+  CK(cudaGetLastError(), "pipe_matvec_kernel launch");
   return QMOE_OK;
 }
 
@@ -1485,7 +1296,7 @@ static int fused_common(qmoe_dict_t d, const uint16_t* d_cw, const int32_t* d_ro
     // small launches stage a smaller hot table (the fill is per CTA)
     const int64_t est_cw = rows * cols / 24 + rows;
     const int want = (int)std::min<int64_t>(QMOE_DICT_SIZE, std::max<int64_t>(4096, est_cw / grid * 2));
-    const int rc = launch_seg(d, P, false, (int)cols, ntok > 1 ? 2 : 1, grid, want, S(stream));
+    const int rc = launch_seg(d, P, (int)cols, ntok > 1 ? 2 : 1, grid, want, S(stream));
     if (rc == QMOE_OK && d_bad) {
       // rows must have been validated (qmoe_validate_rows); nothing further to flag
     }
@@ -1625,7 +1436,7 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   SP.counters = d_counters;
   SP.order_out = d_order;
   SP.count_out = d_expert_count;
-  SP.w2 = getenv("QMOE_W2") ? atoi(getenv("QMOE_W2")) : 11;  // experiment override
+  SP.w2 = 11;  // split weight of a 2-token run (a 1-token run weighs 8; measured)
   const int maxc = std::max(d_model, d_ff);
   const size_t slot = (size_t)2 * 4 * (((maxc + 32) + 3) & ~3);
   const size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
@@ -1636,8 +1447,7 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   if (xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
     return qmoe::fail(QMOE_EUNSUPPORTED, "step too large for the fused kernel's shared memory (use the grouped path)");
   int H = (int)((d->max_smem_optin - xbytes - plan - static_smem - 256) / 4);
-  int want = hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE;
-  if (hot_override() >= 0) want = hot_override();
+  const int want = hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE;
   H = std::max(std::min(H, std::min(want, QMOE_DICT_SIZE)) & ~255, 256);
   SP.wi.H = SP.wo.H = H;
   SP.wi.xbytes = SP.wo.xbytes = (int)xbytes;
@@ -1653,7 +1463,7 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the wo phase waits on other CTAs
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = getenv("QMOE_NO_COOP") ? 0 : 1;
+  cfg.numAttrs = 1;
   const cudaError_t le = cudaLaunchKernelEx(&cfg, moe_step_kernel, SP);
   if (le == cudaErrorCooperativeLaunchTooLarge) {  // SMs not all available: caller falls back
     (void)cudaGetLastError();
@@ -1667,8 +1477,6 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
                         int32_t max_work, int32_t max_cols, int32_t max_ntok, const void* d_x, int x_dtype,
                         int64_t ldx, void* d_y, int y_mode, int64_t ldy, int32_t hot_entries, int32_t* d_bad,
                         void* stream) {
-  const bool packed = (y_mode & QMOE_RUNS_PACKED) != 0;
-  y_mode &= ~QMOE_RUNS_PACKED;
   if (!d || !d->d_stab || !d_work || !d_n_work || max_work < 0 || max_cols <= 0 || max_ntok < 1 ||
       max_ntok > QMOE_NT_MAX || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16) ||
       (y_mode != QMOE_Y_ACCUM_F32 && y_mode != QMOE_Y_RELU_BF16 && y_mode != QMOE_Y_STORE_F32))
@@ -1690,10 +1498,10 @@ int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work*
     P.y = d_y;
     P.y_mode = y_mode;
     P.ldy = ldy;
-    return launch_seg(d, P, packed, max_cols, max_ntok, d->num_sms, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE,
+    return launch_seg(d, P, max_cols, max_ntok, d->num_sms, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE,
                       S(stream));
   }
-  if (d_table || packed) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks / packed runs need a <=3-non-zero dictionary");
+  if (d_table) return qmoe::fail(QMOE_EUNSUPPORTED, "codebooks need a <=3-non-zero dictionary");
   GeneralParams G{};
   G.words = d->d_words;
   G.work = d_work;

@@ -21,7 +21,6 @@ wo matvec through moepack.codec.fused_matvec) up to the matvec tolerance.
 from __future__ import annotations
 
 import ctypes
-import os
 import threading
 
 import numpy as np
@@ -36,11 +35,16 @@ class CompressedMoELayer:
     all DeviceMatrix on one device."""
 
     def __init__(self, wi: list[DeviceMatrix], wo: list[DeviceMatrix], dic: Dictionary, max_tokens: int = 64,
-                 tokens_per_unit: int = 2, codebook: bool = True):
+                 tokens_per_unit: int = 2, codebook: bool = True, fused: bool = True, dense: str = "auto"):
+        """dense: "auto" (decode-then-MMA from DENSE_MIN_TOKENS tokens per
+        touched expert), "never" or "always"; fused: one cooperative launch
+        per streaming step (else plan kernel + two grouped passes)."""
         import torch
 
         if len(wi) != len(wo) or not wi:
             raise ValueError("need matching wi/wo lists")
+        if dense not in ("auto", "never", "always"):
+            raise ValueError("dense must be 'auto', 'never' or 'always'")
         self.E = len(wi)
         self.d_ff, self.d_model = wi[0].rows, wi[0].cols
         for a, b in zip(wi, wo):
@@ -48,54 +52,65 @@ class CompressedMoELayer:
                 raise ValueError("expert shapes disagree")
             if a.bad_rows or b.bad_rows:
                 raise ValueError("expert matrix failed row validation")
-        self.wi, self.wo, self.dic = wi, wo, dic
         self.device = wi[0].cw.device
         self.handle = dic.device_handle(self.device.index)
-        # layer-level frequency codebook (kernel-private stream re-indexing)
+        sparse = bool(dic.device_info(self.device.index)["sparse_path"])
+        self._sparse_path = sparse
+        # layer-level frequency codebook (kernel-private stream re-indexing).
+        # Matrices cached on a host CompressedMatrix (c.to_device) are shared
+        # with the drop-in API, which reads them in dictionary order: the layer
+        # re-indexes private copies of their streams instead.
         self.codebook = None
-        if codebook and dic.device_info(self.device.index)["sparse_path"]:
+        if codebook and sparse:
             from .codebook import Codebook
 
             mats = list(wi) + list(wo)
             if all(m.codebook is None for m in mats):
+                wi = [m.private_copy() if m.shared else m for m in wi]
+                wo = [m.private_copy() if m.shared else m for m in wo]
+                mats = list(wi) + list(wo)
                 self.codebook = Codebook(dic, mats)
                 self.codebook.apply(mats)
             elif len({id(m.codebook) for m in mats}) == 1:
                 self.codebook = mats[0].codebook
-        import os
-
-        self.packed = (bool(dic.device_info(self.device.index)["sparse_path"])
-                       and os.environ.get("QMOE_LAYOUT", "raw") == "packed")
+        self.wi, self.wo, self.dic = wi, wo, dic
         # mean 8-codeword groups per row (wi, wo): lane-segment sizing
         self.mean_groups = tuple(float(np.mean([m.n_codewords / max(1, m.rows) / 8 for m in ms])) for ms in (wi, wo))
-        # most lanes per row a step may use: segments of >= ~2 groups
-        # one level finer than that: tiny steps (generation) split rows further
-        boost = int(os.environ.get("QMOE_LG_BOOST", 1))
-        self.max_lg = tuple(max(0, min(self.MAX_LG, int(np.floor(np.log2(max(1.0, mg / 2)))) + boost))
+        # most lanes per row a step may use: segments of >= ~2 groups, one
+        # level finer than that (tiny generation steps split rows further)
+        self.max_lg = tuple(max(0, min(self.MAX_LG, int(np.floor(np.log2(max(1.0, mg / 2)))) + 1))
                             for mg in self.mean_groups)
-        for kind, ms in enumerate((wi, wo)):  # kernel-private PACKED layout (or row checkpoints)
+        for kind, ms in enumerate((wi, wo)):  # kernel-private row checkpoints
             for m in ms:
-                if self.packed:
-                    if m.packed is None:
-                        m.build_layout(dic)
-                elif m.ck is None and m.lg == 0 and self.max_lg[kind] > 0:
+                if m.ck is None and m.lg == 0 and self.max_lg[kind] > 0:
                     # checkpoints for 2^max_lg lanes per row; a run may use any 2^lg <= that
                     m.build_checkpoints(dic, lg=self.max_lg[kind])
         self._colpts_ready = all(m.colpts is not None for m in list(wi) + list(wo))
+        self.mats = None
         self._write_descriptors()
-        self.tokens_per_unit = min(int(os.environ.get("QMOE_NTU", tokens_per_unit)), _lib.NT_STREAM)
+        self.tokens_per_unit = min(int(tokens_per_unit), _lib.NT_STREAM)
         self.expert_bytes = np.array([wi[e].compressed_bytes + wo[e].compressed_bytes for e in range(self.E)],
                                      np.int64)
         self._lanes = {}
         self._T = max_tokens
-        # one cooperative launch per step (sparse dictionaries, RAW layout)
-        self.fused = (not self.packed and bool(dic.device_info(self.device.index)["sparse_path"])
-                      and os.environ.get("QMOE_FUSED", "1") == "1")
+        self._retired = []
+        self._stages = {}
+        self.dense_mode = dense
+        # one cooperative launch per step (sparse dictionaries)
+        self.fused = sparse and fused
         self._alloc(max_tokens)
 
     def _alloc(self, T: int) -> None:
+        """(Re)allocate the per-step device buffers for up to T tokens. CUDA
+        graphs captured earlier (the host API's per-T graphs, or a caller's)
+        hold raw pointers to the previous buffers, so those are retired — kept
+        alive with the layer — instead of freed: a replay of an old graph
+        stays consistent with the buffers it was captured on."""
         import torch
 
+        if hasattr(self, "h"):
+            self._retired.append((self.units_wi, self.units_wo, self.n_units, self.expert_count, self.order,
+                                  self.h, self.bad, self.counters))
         self.max_tokens = T
         self.max_units = max(1, T)  # runs per pass: one per expert token chunk <= T
         dev = self.device
@@ -111,15 +126,21 @@ class CompressedMoELayer:
         self.counters = torch.zeros(max(1, T) + 1, dtype=torch.int32, device=dev)  # fused step (self-resetting)
 
     def _write_descriptors(self) -> None:
-        """Device array of qmoe_matrix descriptors (wi_e = 2e, wo_e = 2e + 1)."""
+        """Device array of qmoe_matrix descriptors (wi_e = 2e, wo_e = 2e + 1).
+        Rewritten IN PLACE once allocated (e.g. when the decode-then-MMA column
+        points are added), so graphs already holding its address stay valid."""
         import torch
 
         descs = (_lib.QmoeMatrix * (2 * self.E))()
         for e in range(self.E):
             descs[2 * e] = _lib.QmoeMatrix(*self.wi[e].descriptor())
             descs[2 * e + 1] = _lib.QmoeMatrix(*self.wo[e].descriptor())
-        raw = np.frombuffer(bytes(descs), dtype=np.uint8)
-        self.mats = torch.from_numpy(raw.copy()).to(self.device)
+        raw = torch.from_numpy(np.frombuffer(bytes(descs), dtype=np.uint8).copy())
+        if getattr(self, "mats", None) is None:
+            self.mats = raw.to(self.device)
+        else:
+            torch.cuda.current_stream(self.device).synchronize()  # no step in flight reads it
+            self.mats.copy_(raw)
 
     @staticmethod
     def _aligned_rows(x) -> bool:
@@ -146,21 +167,15 @@ class CompressedMoELayer:
             runs = self._runs_est(T)
             out = []
             for kind, (rows, mg) in enumerate(((self.d_ff, self.mean_groups[0]), (self.d_model, self.mean_groups[1]))):
-                cap = 5 if self.packed else min(m.lg for m in (self.wi if kind == 0 else self.wo))
-                caps = getattr(self, "_caps", [0, 0])
-                caps[kind] = cap
-                self._caps = caps
+                cap = min(m.lg for m in (self.wi if kind == 0 else self.wo))
                 lg = 0
-                base_min = float(os.environ.get("QMOE_MIN_SEG_GROUPS", 2.0))  # experiment
+                base_min = 2.0
                 while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES:
                     min_groups = base_min if runs * rows * (1 << lg) >= self.LANES // 4 else base_min / 2
                     if mg / (1 << (lg + 1)) < min_groups:
                         break
                     lg += 1
                 out.append(lg)
-            for kind, key in enumerate(("QMOE_LG_WI", "QMOE_LG_WO")):  # experiment overrides
-                if key in os.environ:
-                    out[kind] = min(int(os.environ[key]), self._caps[kind])  # checkpoints bound it
             hit = self._lanes[T] = tuple(out)
         return hit
 
@@ -187,9 +202,6 @@ class CompressedMoELayer:
             _lib.ptr(self.units_wi), _lib.ptr(self.units_wo),
             _lib.ptr(self.n_units), _lib.ptr(self.expert_count), _lib.ptr(self.order), _lib.stream_ptr(stream)))
 
-    def _flag(self) -> int:
-        return _lib.QMOE_RUNS_PACKED if self.packed else 0
-
     def _table(self) -> int:
         return self.codebook.table.data_ptr() if self.codebook is not None else 0
 
@@ -200,14 +212,14 @@ class CompressedMoELayer:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
             self.handle, self._table(), _lib.ptr(self.units_wi), _lib.ptr(self.n_units), self.max_units,
             self.d_model, self.tokens_per_unit, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h),
-            _lib.QMOE_Y_RELU_BF16 | self._flag(), self.h.stride(0), self.hot_entries(self._T, True),
+            _lib.QMOE_Y_RELU_BF16, self.h.stride(0), self.hot_entries(self._T, True),
             _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def pass_wo(self, out, stream=None) -> None:
         _lib.check(_lib.lib.qmoe_grouped_matvec(
             self.handle, self._table(), _lib.ptr(self.units_wo), self.n_units.data_ptr() + 8, self.max_units,
             self.d_ff, self.tokens_per_unit, _lib.ptr(self.h), _lib.QMOE_X_BF16, self.h.stride(0), _lib.ptr(out),
-            _lib.QMOE_Y_STORE_F32 | self._flag(), out.stride(0), self.hot_entries(self._T, False),
+            _lib.QMOE_Y_STORE_F32, out.stride(0), self.hot_entries(self._T, False),
             _lib.ptr(self.bad), _lib.stream_ptr(stream)))
 
     def forward_device(self, x, assign, out=None, stream=None):
@@ -273,13 +285,9 @@ class CompressedMoELayer:
         streaming path)."""
         import torch
 
-        sparse = getattr(self, "_sparse_path", None)
-        if sparse is None:  # a property of the dictionary: ask the library once
-            sparse = self._sparse_path = bool(self.dic.device_info(self.device.index)["sparse_path"])
-        if self.packed or not sparse:
+        if not self._sparse_path or self.dense_mode == "never":
             return False
-        mode = os.environ.get("QMOE_DENSE", "auto")
-        want = mode == "1" if mode in ("0", "1") else T / self._runs_est(T) >= self.DENSE_MIN_TOKENS
+        want = self.dense_mode == "always" or T / self._runs_est(T) >= self.DENSE_MIN_TOKENS
         if want and not self._colpts_ready:
             if torch.cuda.is_current_stream_capturing():
                 return False
@@ -294,7 +302,7 @@ class CompressedMoELayer:
         import torch
 
         T = self._T
-        bn = int(os.environ.get("QMOE_DENSE_BN", 64 if T / self._runs_est(T) > 24 else 32))
+        bn = 64 if T / self._runs_est(T) > 24 else 32
         rows, cols = (self.d_ff, self.d_model) if which == 0 else (self.d_model, self.d_ff)
         xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
         _lib.check(_lib.lib.qmoe_dense_moe_pass(
@@ -361,7 +369,7 @@ class CompressedMoELayer:
         if x.ndim != 2 or x.shape[1] != self.d_model or a.shape != (T,):
             raise ValueError(f"expected x (T, {self.d_model}) and assign (T,)")
         key = (T, self.use_dense(T))  # the captured graph holds one path
-        st = self._stages.get(key) if hasattr(self, "_stages") else None
+        st = self._stages.get(key)
         if st is None:
             st = self._host_stage(T, key)
         np.copyto(st["xv"], x)
@@ -393,8 +401,6 @@ class CompressedMoELayer:
         (measured: tools/e2e_breakdown.py)."""
         import torch
 
-        if not hasattr(self, "_stages"):
-            self._stages = {}
         if len(self._stages) >= self.GRAPH_CACHE:
             self._stages.pop(next(iter(self._stages)))
         xb = T * self.d_model * 4

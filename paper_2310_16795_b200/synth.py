@@ -2,10 +2,17 @@
 
 Recipe: W ~ N(0, 0.02^2) fp32 per expert matrix, make_grid +
 RTN to ternary (GPU rtn_kernel, bit-exact with quantize.rtn_quantize), then the
-GPU encoder (bit-exact with codec.encode). All experts of one kind (wi or wo)
-are encoded as ONE stacked matrix — rows are independent, so the stream of
-each expert is exactly what encoding it alone gives — then split into
-per-expert DeviceMatrix views.
+GPU encoder (bit-exact with codec.encode). Two weight sources:
+  build_layer         device-generated weights (torch.randn): fast, for the
+                      pools of distinct layers the benchmarks rotate through;
+  build_layer_seeded  the survey's host recipe, W = N(0, 0.02^2) drawn from
+                      numpy default_rng(SeedSequence([base, layer, e, m]))
+                      (m = 0 wi, 1 wo) — what the reference CPU path can
+                      regenerate bit for bit (bench.py's reference arm and
+                      parity leg).
+All experts of one kind (wi or wo) are encoded as ONE stacked matrix — rows
+are independent, so the stream of each expert is exactly what encoding it
+alone gives — then split into per-expert DeviceMatrix views.
 """
 
 from __future__ import annotations
@@ -40,6 +47,30 @@ def _stacked(E: int, rows: int, cols: int, seed: int, dic: Dictionary, device, c
             mats.append(DeviceMatrix(rows, cols, cw, r, m, dic.hash64))
         del big, mm
     return mats
+
+
+def seeded_weights(base: int, layer: int, e: int, m: int, rows: int, cols: int):
+    """SURVEY 8(d) recipe: fp32 N(0, 0.02^2) of expert e's matrix m (0 wi, 1 wo)."""
+    import numpy as np
+
+    rng = np.random.default_rng(np.random.SeedSequence([base, layer, e, m]))
+    return (rng.normal(size=(rows, cols)) * 0.02).astype(np.float32)
+
+
+def build_layer_seeded(E: int, d_model: int, d_ff: int, base: int, layer: int, dic: Dictionary, device=None,
+                       max_tokens: int = 64) -> CompressedMoELayer:
+    """A layer from the host recipe (seeded_weights), RTN + encoded on the GPU."""
+    import torch
+
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    mats = ([], [])
+    for m, (rows, cols) in enumerate(((d_ff, d_model), (d_model, d_ff))):
+        for e in range(E):
+            w = torch.from_numpy(seeded_weights(base, layer, e, m, rows, cols)).to(device)
+            codes, mm = rtn_quantize_device(w)
+            del w
+            mats[m].append(encode_device(codes, mm, dic))
+    return CompressedMoELayer(mats[0], mats[1], dic, max_tokens=max_tokens)
 
 
 def build_layer(E: int, d_model: int, d_ff: int, seed: int, dic: Dictionary, device=None,

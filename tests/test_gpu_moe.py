@@ -184,8 +184,6 @@ def test_moe_dense_decode_then_mma_vs_oracle(dic, odic, T):
     """Batched regime: decode-then-MMA passes (qmoe_dense_moe_pass) — several
     row blocks, K chunks with straddling codewords, experts with 0, < 32 and
     > 64 tokens — against the composed oracle and the streaming path."""
-    import os
-
     rng = np.random.default_rng(T + 7)
     E, d_model, d_ff = 4, 320, 1100  # 1100 rows: 3 row blocks (last partial); 320 cols: 5 chunks
     wi, wo, host = [], [], []
@@ -201,20 +199,14 @@ def test_moe_dense_decode_then_mma_vs_oracle(dic, odic, T):
     layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
     x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
     assign = np.where(np.arange(T) % 5 == 0, 1, rng.integers(0, 3, size=T)).astype(np.int32)  # expert 3: no tokens
-    os.environ["QMOE_DENSE"] = "1"
-    try:
-        y = layer.forward(x, assign)
-    finally:
-        os.environ.pop("QMOE_DENSE")
+    layer.dense_mode = "always"
+    y = layer.forward(x, assign)
     y_ref = O.moe_layer(x, assign, host, odic)
     d = bf16_ulp_diff(y, y_ref)
     assert d.max() <= 2, d.max()
     assert np.mean(d == 0) >= 0.99
-    os.environ["QMOE_DENSE"] = "0"
-    try:
-        y_stream = layer.forward(x, assign)
-    finally:
-        os.environ.pop("QMOE_DENSE")
+    layer.dense_mode = "never"
+    y_stream = layer.forward(x, assign)
     assert bf16_ulp_diff(y, y_stream).max() <= 2
 
 
@@ -237,8 +229,6 @@ def test_fused_step_equals_grouped_passes_and_plan(dic, T):
     """The single-launch step (qmoe_moe_step) runs the same decode with the same
     lanes as the plan kernel + two grouped passes: outputs must be bit-identical,
     and its dispatcher outputs (stable per-expert order, counts) exact."""
-    import os
-
     rng = np.random.default_rng(100 + T)
     E, d_model, d_ff = 6, 192, 640
     wi, wo, _ = _random_layer(dic, rng, E, d_model, d_ff, T)
@@ -252,13 +242,9 @@ def test_fused_step_equals_grouped_passes_and_plan(dic, T):
     order = np.argsort(np.where(ok, a_np, E), kind="stable")[: ok.sum()]
     assert np.array_equal(layer.order[: ok.sum()].cpu().numpy(), order)
     assert np.array_equal(layer.expert_count.cpu().numpy(), np.bincount(a_np[ok], minlength=E))
-    os.environ["QMOE_FUSED"] = "0"
-    try:
-        layer2 = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
-        assert not layer2.fused
-        y_grouped = layer2.forward_device(x, a)
-    finally:
-        os.environ.pop("QMOE_FUSED")
+    layer2 = q.CompressedMoELayer(wi, wo, dic, max_tokens=T, fused=False)
+    assert not layer2.fused
+    y_grouped = layer2.forward_device(x, a)
     assert torch.equal(y_fused, y_grouped)  # incl. zero rows for tokens without an expert
     assert torch.all(y_fused[~torch.from_numpy(ok).cuda()] == 0)
     # a second step with the same layer reuses the self-resetting counters
@@ -267,35 +253,10 @@ def test_fused_step_equals_grouped_passes_and_plan(dic, T):
     assert int(layer.counters.abs().sum()) == 0
 
 
-def test_packed_layout_matches_oracle(dic, odic):
-    """Kernel-private PACKED layout (length-sorted, group-aligned rows, per-group
-    columns; QMOE_LAYOUT=packed) against the composed oracle."""
-    import os
-
-    rng = np.random.default_rng(7)
-    E, d_model, d_ff = 3, 256, 768
-    os.environ["QMOE_LAYOUT"] = "packed"
-    try:
-        wi, wo, host = _random_layer(dic, rng, E, d_model, d_ff, 16)
-        layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=16)
-        assert layer.packed and not layer.fused
-        x = q.bf16_round(rng.normal(size=(16, d_model)).astype(np.float32))
-        assign = rng.integers(0, E, size=16).astype(np.int32)
-        y = layer.forward(x, assign)
-    finally:
-        os.environ.pop("QMOE_LAYOUT")
-    y_ref = O.moe_layer(x, assign, host, odic)
-    d = bf16_ulp_diff(y, y_ref)
-    assert d.max() <= 2
-    assert np.mean(d == 0) >= 0.99
-
-
 def test_fused_plan_many_experts(dic):
     """The fused step's warp plan sorts (expert, token) keys: with hundreds of
     experts (nothing in it scales with E) the stable order, counts and outputs
     still match the grouped path."""
-    import os
-
     rng = np.random.default_rng(77)
     E, d_model, d_ff, T = 600, 64, 128, 160
     wi, wo, _ = _random_layer(dic, rng, E, d_model, d_ff, T)
@@ -309,12 +270,8 @@ def test_fused_plan_many_experts(dic):
     order = np.argsort(np.where(ok, a_np, E), kind="stable")[: ok.sum()]
     assert np.array_equal(layer.order[: ok.sum()].cpu().numpy(), order)
     assert np.array_equal(layer.expert_count.cpu().numpy(), np.bincount(a_np[ok], minlength=E))
-    os.environ["QMOE_FUSED"] = "0"
-    try:
-        layer2 = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
-        y_grouped = layer2.forward_device(x, a)
-    finally:
-        os.environ.pop("QMOE_FUSED")
+    layer2 = q.CompressedMoELayer(wi, wo, dic, max_tokens=T, fused=False)
+    y_grouped = layer2.forward_device(x, a)
     assert torch.equal(y_fused[ok], y_grouped[ok])
 
 
@@ -342,8 +299,6 @@ def test_dense_pass_ignores_row_padding(dic, odic):
     """The hidden rows are padded to a 16-byte stride and the padding is never
     written: the decode-then-MMA pass must not read it into the MMA (NaN bit
     patterns there would poison whole accumulators: 0 * NaN = NaN)."""
-    import os
-
     rng = np.random.default_rng(41)
     E, d_model, d_ff, T = 3, 96, 300, 90  # d_ff % 8 != 0: padded hidden rows
     wi, wo, host = [], [], []
@@ -360,11 +315,8 @@ def test_dense_pass_ignores_row_padding(dic, odic):
     layer.h.fill_(float("nan"))
     x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
     assign = rng.integers(0, E, size=T).astype(np.int32)
-    os.environ["QMOE_DENSE"] = "1"
-    try:
-        y = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
-    finally:
-        os.environ.pop("QMOE_DENSE")
+    layer.dense_mode = "always"
+    y = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
     y_ref = O.moe_layer(x, assign, host, odic)
     d = bf16_ulp_diff(y.cpu().numpy(), y_ref)
     assert np.isfinite(y.cpu().numpy()).all()

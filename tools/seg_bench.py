@@ -30,7 +30,7 @@ def runs_for(mats, ntok, ldx, lg=None):
     t = 0
     for i, m in enumerate(mats):
         d = m.descriptor()
-        mlg = d[7] if lg is None else (lg if d[8] else (lg | (d[7] << 8)))
+        mlg = d[7] if lg is None else (lg | (d[7] << 8))
         recs[i] = _lib.QmoeWork(d[0], d[1], d[2], d[3], m.cols, 0, m.rows, mlg, ntok, t, d[8],
                                 tuple([0, 1 % max(1, ntok), 0, 0][:4]))
         t += ((m.rows << (mlg & 0xFF)) + 31) >> 5
@@ -39,30 +39,25 @@ def runs_for(mats, ntok, ldx, lg=None):
     return raw, n, t
 
 
-def bench(rows, cols, lg=None, ntok=1, iters=20, hot=None, packed=True):
+def bench(rows, cols, lg=None, ntok=1, iters=20, hot=None, packed=False):
     per = 2 * rows * cols // 24 + 8 * rows
     E = max(8, int(4.5 * L2 / per))
     mats = _stacked(E, rows, cols, seed=rows + cols, dic=dic, device=dev)
     cb = Codebook(dic, mats)
     cb.apply(mats)
     for m in mats:
-        if packed:
-            m.build_layout(dic)
-        else:
-            m.build_checkpoints(dic, 3)
+        m.build_checkpoints(dic, 3)
     nbytes = sum(m.compressed_bytes for m in mats)
     ncw = sum(m.n_codewords for m in mats)
     x = torch.randn(2, cols, device=dev).to(torch.bfloat16)
     y = torch.zeros(2, rows, device=dev)
     raw, n, tasks = runs_for(mats, ntok, x.stride(0), lg)
-    flag = _lib.QMOE_RUNS_PACKED if packed else 0
+    flag = 0
     # all matrices in one launch is one "step"; y rows are overwritten per matrix (timing only)
     def launch():
         _lib.check(_lib.lib.qmoe_grouped_matvec(h, _lib.ptr(cb.table), _lib.ptr(raw), _lib.ptr(n), len(mats), cols,
                                                  ntok, _lib.ptr(x), _lib.QMOE_X_BF16, x.stride(0), _lib.ptr(y),
                                                  _lib.QMOE_Y_STORE_F32 | flag, y.stride(0), 0, 0, _lib.stream_ptr()))
-    if hot is not None:
-        os.environ["QMOE_HOT_ENTRIES"] = str(hot)
     launch()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -72,8 +67,8 @@ def bench(rows, cols, lg=None, ntok=1, iters=20, hot=None, packed=True):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
-    lgv = (lg if lg is not None else mats[0].packed["lg"]) if packed else lg
-    print(f"{'packed' if packed else 'raw'} {rows}x{cols} E={E} lg={lgv} ntok={ntok} tasks={tasks}: {ms:.3f} ms  {ncw / ms / 1e6:.1f} Gcw/s  "
+    lgv = lg
+    print(f"raw {rows}x{cols} E={E} lg={lgv} ntok={ntok} tasks={tasks}: {ms:.3f} ms  {ncw / ms / 1e6:.1f} Gcw/s  "
           f"{E * rows * cols / ms / 1e9:.2f} Tw/s  {nbytes / ms / 1e6:.1f} GB/s (hit@H {cb.hit_rate(45000):.3f})",
           flush=True)
     del mats, cb
