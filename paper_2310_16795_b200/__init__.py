@@ -22,6 +22,7 @@ from .codec import (
     pad_to_even,
     read_checkpoint,
     read_checkpoint_device,
+    read_stacked_device,
     simulate_warp_row,
     write_checkpoint,
 )
@@ -39,7 +40,7 @@ from .dictionary import (
     unpack_decode_words,
 )
 from .errors import ConfigError, CorruptionError, DictionaryMismatchError, MoepackError, TierCapacityError
-from .moe import CompressedMoELayer
+from .moe import CompressedMoELayer, load_moe_layer
 from .pipeline import DeviceRouter, RouterSim
 from .quantize import QuantGrid, TernaryMatrix, make_grid, reconstruction_levels, rtn_quantize, rtn_quantize_device
 from .stats import RateReport, compression_rate, natural_sparsity, sample_ternary, theoretical_limit

@@ -616,40 +616,119 @@ def write_checkpoint(c: CompressedMatrix, path: str) -> None:
         fh.write(c.codewords.astype("<u2").tobytes())
 
 
-def read_checkpoint(path: str) -> CompressedMatrix:
-    """Strict reader (codec.py:354-391): magic, header arrays, monotone
-    offsets from zero, exact total size, then validate()."""
-    with open(path, "rb") as fh:
-        blob = fh.read()
-    if len(blob) < len(CHECKPOINT_MAGIC) + 24 or not blob.startswith(CHECKPOINT_MAGIC):
+def _parse_checkpoint(blob: np.ndarray):
+    """Strict QMOE0001 parse (codec.py:354-391) over a uint8 buffer, same
+    checks, order and messages as the reference; returns views into blob."""
+    if len(blob) < len(CHECKPOINT_MAGIC) + 24 or bytes(blob[: len(CHECKPOINT_MAGIC)]) != CHECKPOINT_MAGIC:
         raise CorruptionError("not a checkpoint file (bad magic)")
     pos = len(CHECKPOINT_MAGIC)
     rows, cols, dict_hash = struct.unpack_from("<QQQ", blob, pos)
     pos += 24
     if len(blob) < pos + 4 * (rows + 1) + 4 * rows:
         raise CorruptionError("checkpoint truncated in header arrays")
-    row_off = np.frombuffer(blob, dtype="<i4", count=rows + 1, offset=pos).astype(np.int32)
+    row_off = np.frombuffer(blob, dtype="<i4", count=rows + 1, offset=pos)
+    off_pos = pos
     pos += 4 * (rows + 1)
-    row_minmax = np.frombuffer(blob, dtype="<u2", count=2 * rows, offset=pos).astype(np.uint16).reshape(rows, 2)
+    row_minmax = np.frombuffer(blob, dtype="<u2", count=2 * rows, offset=pos).reshape(rows, 2)
+    mm_pos = pos
     pos += 4 * rows
     if row_off[0] != 0 or np.any(np.diff(row_off) < 0):
         raise CorruptionError("checkpoint row offsets are not monotone from zero")
     n = int(row_off[-1])
     if len(blob) != pos + 2 * n:
         raise CorruptionError("checkpoint size disagrees with row offsets")
-    cw = np.frombuffer(blob, dtype="<u2", count=n, offset=pos).astype(np.uint16)
-    c = CompressedMatrix(int(rows), int(cols), cw, row_off, row_minmax, int(dict_hash))
+    cw = np.frombuffer(blob, dtype="<u2", count=n, offset=pos)
+    return int(rows), int(cols), int(dict_hash), row_off, row_minmax, cw, (off_pos, mm_pos, pos)
+
+
+def read_checkpoint(path: str) -> CompressedMatrix:
+    """Strict reader (codec.py:354-391): magic, header arrays, monotone
+    offsets from zero, exact total size, then validate()."""
+    with open(path, "rb") as fh:
+        blob = np.frombuffer(fh.read(), dtype=np.uint8)
+    rows, cols, dict_hash, row_off, row_minmax, cw, _ = _parse_checkpoint(blob)
+    c = CompressedMatrix(rows, cols, cw.astype(np.uint16), row_off.astype(np.int32),
+                         row_minmax.astype(np.uint16), dict_hash)
     c.validate()
     return c
 
 
-def read_checkpoint_device(path: str, dic: Dictionary, device=None) -> DeviceMatrix:
-    """Loader straight to HBM: parse + validate on the host,
-    one H2D copy per array, GPU row validation."""
-    c = read_checkpoint(path)
-    if c.dict_hash != dic.hash64:
+def _read_pinned(path: str):
+    """The whole file in pinned host memory (torch uint8) + a numpy view."""
+    import os
+
+    torch = _torch()
+    size = os.path.getsize(path)
+    buf = torch.empty(max(1, size), dtype=torch.uint8, pin_memory=True)
+    view = buf.numpy()[:size]
+    with open(path, "rb") as fh:
+        got = fh.readinto(memoryview(view))
+    if got != size:
+        raise CorruptionError("checkpoint changed while reading")
+    return buf, view
+
+
+def _validate_many(mats, dic: Dictionary) -> None:
+    """Device row-length validation of several matrices, one sync."""
+    torch = _torch()
+    if not mats:
+        return
+    dev = mats[0].cw.device
+    bad = torch.tensor([0, INT32_MAX] * len(mats), dtype=torch.int32, device=dev)
+    h = dic.device_handle(dev.index)
+    for i, m in enumerate(mats):
+        _lib.check(_lib.lib.qmoe_validate_rows(h, _lib.ptr(m.cw), _lib.ptr(m.row_off), m.rows, m.cols,
+                                               bad.data_ptr() + 8 * i, _lib.stream_ptr()))
+    b = bad.view(-1, 2).cpu().numpy()
+    for m, (n, first) in zip(mats, b):
+        m.bad_rows, m.first_bad = int(n), (int(first) if n else None)
+
+
+def _load_device(path: str, dic: Dictionary, device, rows_per_part=None):
+    """Pinned read + strict parse + hash check + ONE host-to-device copy of
+    the file; the matrix (or its row blocks of rows_per_part rows, stacked
+    by rows as the reference CLI writes them) as aligned DeviceMatrix
+    arrays carved out of the device copy, then validated on the GPU."""
+    torch = _torch()
+    buf, blob = _read_pinned(path)
+    rows, cols, dict_hash, row_off, _, _, (off_pos, mm_pos, cw_pos) = _parse_checkpoint(blob)
+    if cols % 2 != 0:
+        raise CorruptionError("invalid compressed matrix shape")
+    if dict_hash != dic.hash64:
         raise DictionaryMismatchError("checkpoint was encoded against a different dictionary")
-    dm = c.to_device(dic, device)
-    if dm.bad_rows:
+    R = rows if rows_per_part is None else int(rows_per_part)
+    if rows and (R <= 0 or rows % R != 0):
+        raise ValueError(f"{rows} stacked rows are not a multiple of rows_per_expert = {R}")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    blob_d = buf[: len(blob)].to(dev, non_blocking=True)  # the one H2D copy
+    ro_all = blob_d[off_pos: off_pos + 4 * (rows + 1)].view(torch.int32)
+    mm_all = blob_d[mm_pos: mm_pos + 4 * rows].view(torch.int32)
+    cw_all = blob_d[cw_pos:].view(torch.int16)
+    parts = []
+    for p0 in range(0, rows, R) if rows else [0]:
+        p1 = min(rows, p0 + R)
+        s, e = int(row_off[p0]), int(row_off[p1])
+        parts.append(DeviceMatrix(p1 - p0, cols, _lib.padded_copy(cw_all[s:e]),
+                                  _lib.padded_copy(ro_all[p0: p1 + 1] - s), _lib.padded_copy(mm_all[p0:p1]),
+                                  dict_hash))
+    _validate_many(parts, dic)
+    del blob_d
+    if any(m.bad_rows for m in parts):
         raise _row_len_error()
-    return dm
+    return parts
+
+
+def read_checkpoint_device(path: str, dic: Dictionary, device=None) -> DeviceMatrix:
+    """Loader straight to HBM (format codec.py:341-391): the
+    file is read into pinned memory, parsed and checked on the host exactly as
+    read_checkpoint (then DictionaryMismatchError), copied to the device in
+    one transfer and row-validated on the GPU (CorruptionError)."""
+    return _load_device(path, dic, device)[0]
+
+
+def read_stacked_device(path: str, dic: Dictionary, rows_per_expert: int, device=None) -> list:
+    """A stacked multi-expert checkpoint (experts' matrices concatenated by
+    rows into one QMOE0001 file, reference cli.py:150-153 / :194-201, with
+    rows_per_expert from its report) -> one DeviceMatrix per expert, carved
+    from a single host-to-device copy."""
+    return _load_device(path, dic, device, rows_per_expert)

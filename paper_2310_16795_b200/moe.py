@@ -28,6 +28,7 @@ import numpy as np
 from . import _lib
 from .codec import DeviceMatrix
 from .dictionary import Dictionary
+from .errors import CorruptionError as CorruptionError_
 
 
 class CompressedMoELayer:
@@ -442,3 +443,34 @@ class CompressedMoELayer:
     def touched_bytes(self, assign: np.ndarray) -> int:
         """Compressed bytes one step must stream: each distinct expert once."""
         return int(self.expert_bytes[np.unique(np.asarray(assign))].sum())
+
+
+def load_moe_layer(wi_path: str, wo_path: str, dic: Dictionary, max_tokens: int = 64, device=None,
+                   rows_per_expert: tuple[int, int] | None = None, **layer_kw) -> CompressedMoELayer:
+    """A compressed MoE layer from two stacked checkpoints:
+    every expert's wi (d_ff x d_model) stacked by rows in one QMOE0001 file
+    and every wo (d_model x d_ff) in another — what the reference CLI writes
+    for a stacked quantized layer (cli.py:150-153 _stack_quantized, :194-201
+    encode + write_checkpoint, rows_per_expert in its report). d_model = the
+    wi file's cols, d_ff = the wo file's cols, E = wi rows / d_ff. Each file is
+    read into pinned memory, checked exactly as read_checkpoint, copied to the
+    device once and split into per-expert matrices (codec.read_stacked_device)."""
+    import struct
+
+    from .codec import read_stacked_device
+
+    shapes = []
+    for path in (wi_path, wo_path):
+        with open(path, "rb") as fh:
+            head = np.frombuffer(fh.read(32), dtype=np.uint8)
+        if len(head) < 32 or bytes(head[:8]) != b"QMOE0001":
+            raise CorruptionError_("not a checkpoint file (bad magic)")
+        shapes.append(struct.unpack_from("<QQ", head, 8))
+    (wi_rows, d_model), (wo_rows, d_ff) = shapes
+    if d_ff == 0 or d_model == 0 or wi_rows % d_ff or wo_rows % d_model or wi_rows // d_ff != wo_rows // d_model:
+        raise ValueError(f"stacked checkpoints disagree: wi {wi_rows}x{d_model}, wo {wo_rows}x{d_ff}")
+    if rows_per_expert is not None and tuple(rows_per_expert) != (d_ff, d_model):
+        raise ValueError(f"rows_per_expert {tuple(rows_per_expert)} != (d_ff, d_model) = ({d_ff}, {d_model})")
+    wi = read_stacked_device(wi_path, dic, d_ff, device)
+    wo = read_stacked_device(wo_path, dic, d_model, device)
+    return CompressedMoELayer(wi, wo, dic, max_tokens=max_tokens, **layer_kw)

@@ -20,8 +20,14 @@ Every fixture records what reference call produced it:
   misc.json         compression_rate (stats.py:103-114), theoretical_limit
   routing.npz       RouterSim.assign hash / argmax (+skew) (pipeline.py:164-182)
                     on bf16 tokens (the GPU router's parity vectors)
+  stacked_wi.bin,   a stacked multi-expert MoE layer as the reference CLI writes
+  stacked_wo.bin,   one (cli.py:150-153 _stack_quantized, :194-201 encode +
+  stacked.npz       write_checkpoint; rows_per_expert in the report): all
+                    experts' wi stacked by rows in one QMOE0001 file, the wo
+                    likewise; stacked.npz = tokens, routing and the composed
+                    fused_matvec outputs
 
-`python tests/golden/make_golden.py routing` regenerates routing.npz only.
+`python tests/golden/make_golden.py routing|stacked` regenerates one fixture.
 """
 
 from __future__ import annotations
@@ -235,9 +241,40 @@ def make_routing() -> None:
     print("routing.npz written")
 
 
+def make_stacked() -> None:
+    dic = generate_dictionary(PairDistribution(0.885))
+    E, d_model, d_ff, T = 6, 96, 224, 24
+    quant = {0: [], 1: []}
+    for e in range(E):
+        for m, (rows, cols) in enumerate([(d_ff, d_model), (d_model, d_ff)]):
+            quant[m].append(rtn_matrix([13, 0, e, m], rows, cols))
+    stacked = {}
+    for m, name in ((0, "wi"), (1, "wo")):  # cli.py:150-153, 194-201
+        st = TernaryMatrix(codes=np.concatenate([t.codes for t in quant[m]], axis=0),
+                           row_minmax=np.concatenate([t.row_minmax for t in quant[m]], axis=0))
+        c = encode(st, dic, workers=2)
+        write_checkpoint(c, os.path.join(HERE, f"stacked_{name}.bin"))
+        stacked[m] = c
+    x = bf16_round(np.random.default_rng(31).normal(size=(T, d_model)).astype(np.float32))
+    assign = RouterSim(num_experts=E, rule="argmax", seed=0).assign(x)
+    assign[5] = -1  # a token without an expert: zero output row
+    per = {(e, m): encode(quant[m][e], dic) for e in range(E) for m in (0, 1)}
+    y = np.zeros((T, d_model), np.float32)
+    for e in range(E):
+        for p in np.flatnonzero(assign == e):
+            h = np.maximum(fused_matvec(per[(e, 0)], x[p], dic), 0.0)
+            y[p] = fused_matvec(per[(e, 1)], h, dic)
+    np.savez_compressed(os.path.join(HERE, "stacked.npz"), x=x, assign=assign, y=y, E=np.int64(E),
+                        d_model=np.int64(d_model), d_ff=np.int64(d_ff))
+    print("stacked_*.bin / stacked.npz written")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["routing"]:
         make_routing()
+    elif sys.argv[1:] == ["stacked"]:
+        make_stacked()
     else:
         main()
         make_routing()
+        make_stacked()
