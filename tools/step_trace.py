@@ -6,7 +6,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2310_16795_b200 as q
 from paper_2310_16795_b200 import _lib
-from paper_2310_16795_b200.synth import WORKLOADS, build_layer
+from paper_2310_16795_b200.synth import WORKLOADS, build_layer  # noqa: F401
 
 dev = torch.device("cuda", 0)
 dic = q.generate_dictionary()
