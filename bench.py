@@ -479,11 +479,55 @@ def single_matrix_api(dic, dev, rows=768, cols=3072, n=64):
         q.fused_matvec(c, xh, dic)
     host_us = (time.perf_counter() - t0) / 200 * 1e6
     nbytes = float(np.mean([m.compressed_bytes for m in mats]))
-    del mats
+    # the paper's Listing-1 kernel on the same cold matrices
+    from paper_2310_16795_b200.codec import paper_matvec_device
+
+    g2 = torch.cuda.CUDAGraph()
+    for m in mats[:1]:
+        paper_matvec_device(m, dic, x, y)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g2):
+        for m in mats:
+            paper_matvec_device(m, dic, x, y)
+    listing1_us = _time_graphs([g2], 5, 2) * 1e3 / n
+    del mats, g2
     torch.cuda.empty_cache()
     return {"api": "fused_matvec (drop-in, batch 1)", "shape": f"{rows}x{cols}", "device_us_per_call": dev_us,
+            "paper_listing1_us_per_call": listing1_us,
             "device_GBps": nbytes / dev_us / 1e3, "host_us_per_call": host_us,
             "host_what": "numpy x in, numpy y out, matrix uploaded once (cached)"}
+
+
+def decompress_at_scale(dic, dev, hbm_peak, rows=98304, cols=3072):
+    """decompress (codec.py:175-193) throughput: ONE launch over a stacked
+    compressed matrix (128 Switch-base wo experts' rows, 25 MB compressed,
+    302 MB of u8 codes out). Algorithmic bytes = B + rows*cols."""
+    import torch
+
+    from paper_2310_16795_b200.codec import decompress_device, encode_device
+    from paper_2310_16795_b200.quantize import rtn_quantize_device
+
+    w = torch.randn((rows, cols), device=dev) * 0.02
+    codes, mm = rtn_quantize_device(w)
+    del w
+    big = encode_device(codes, mm, dic)
+    del codes
+    out, _ = decompress_device(big, dic)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        out, _ = decompress_device(big, dic)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    nbytes = big.compressed_bytes + rows * cols
+    res = {"kernel": "decompress_kernel (one launch)", "rows": rows, "cols": cols, "ms": ms,
+           "weights_per_s": rows * cols / ms * 1e3, "GBps": nbytes / ms / 1e6, "frac_of_hbm": nbytes / ms / 1e6 / hbm_peak,
+           "bytes": "compressed B + rows*cols u8 codes written"}
+    del big, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def profiled_traffic():
@@ -737,9 +781,10 @@ def main():
     # ---- the decode + matvec kernel at scale (first half of the metric): one
     # grouped launch over a pool (> 4x L2) of distinct 768x3072 matrices
     # (Switch-base wo shape, 4 lanes per row), 1 token, cold
-    at_scale = config1 = None
+    at_scale = config1 = decomp = None
     if not args.profile:
         at_scale = matvec_at_scale(dic, dev, hbm_peak)
+        decomp = decompress_at_scale(dic, dev, hbm_peak)
         config1 = single_matrix_api(dic, dev)
         config1["bf16_cublas_gemv"] = [bf16_gemv(768, 3072, dev, hbm_peak), bf16_gemv(3072, 768, dev, hbm_peak)]
 
@@ -778,6 +823,7 @@ def main():
             "per_token": per_token,
             "parity": parity,
             "kernel_at_scale": at_scale,
+            "decompress_at_scale": decomp,
             "config1_single_matrix": config1,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -940,7 +986,11 @@ def ep_main(args, world, rank, local):
             "tokens_per_s": T * world * args.steps / t_sec, "pct_peak": 100 * per_gpu / hbm_peak,
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": hbm_peak, "unit": "GB/s",
                          "frac": per_gpu / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "whole EP step per GPU (fused local step + NCCL exchange)"},
+                         "kernel": "whole EP step per GPU (fused local step + NCCL exchange)",
+                         "exchange_bytes_per_rank_step": {
+                             "dispatch": world * T * (d_model * 2 + 4), "combine": world * T * d_model * 2,
+                             "what": "fixed slots: T per destination rank, bf16 token rows + int32 expert ids "
+                                     "out, bf16 output rows back (NVLink / NVSwitch)"}},
             "e2e": {"value": e2e_bytes / e2e_sec / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": int(xs[0].nbytes + asg[0].nbytes),
                     "d2h_bytes_per_step": int(T * d_model * 4), "tokens_per_s": T * world * args.steps / e2e_sec,

@@ -18,6 +18,7 @@ from . import _lib
 from .bf16 import bf16_bits_to_f32, f32_to_bf16_bits
 
 MODE_TERNARY = "ternary"
+MODE_2BIT = "2bit"  # the reference's 2-bit grid (quantize.py:24-25): named, not supported (ternary codec only)
 
 
 def reconstruction_levels(mode: str, row_minmax: np.ndarray) -> np.ndarray:
