@@ -1054,8 +1054,9 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       // one rounding; every CTA evaluates the same k identically) — 64-bit
       // integer division is a long emulated sequence on the plan's critical path
       const int k = blockIdx.x + (lane & 1);
-      const int64_t target =
-          (int64_t)__ddiv_rz((double)wpre[nch] * (double)tpr * (double)k, (double)gridDim.x);
+      const int64_t num = (int64_t)wpre[nch] * tpr * k;
+      const int64_t target = num < INT_MAX ? (int64_t)((uint32_t)num / gridDim.x)  // the usual case: 32-bit
+                                           : (int64_t)__ddiv_rz((double)num, (double)gridDim.x);
       int lo = 0, hi = nch;  // last run with wpre[r] * tpr <= target
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;

@@ -3,7 +3,8 @@
 forward's launch pattern), CUDA events. Prints one line per T:
   T step_us GB/s
 Usage: [QMOE_LIB_PATH=variants/x/libqmoe.so] python tools/moe_sweep.py [T ...]
-Env: WORKLOAD (default switch-base-128), HOT (per-step hot-table cap)."""
+Env: WORKLOAD (default switch-base-128), HOT (per-step hot-table cap),
+LG="wi,wo" (lanes per row override)."""
 import os
 import sys
 
@@ -25,6 +26,10 @@ while pool < 4 * L2:
     lay = build_layer(E, d_model, d_ff, seed=len(layers), dic=dic, device=dev, max_tokens=max(Ts))
     if "HOT" in os.environ:
         lay.STEP_HOT_MAX = int(os.environ["HOT"])
+    if "LG" in os.environ:  # "wi,wo": lanes per row (log2) for every T (bounded by the checkpoints)
+        lgs = tuple(min(int(v), c) for v, c in zip(os.environ["LG"].split(","), lay.max_lg))
+        for T in Ts:
+            lay._lanes[T] = lgs
     layers.append(lay)
     pool += int(lay.expert_bytes.sum())
 L = len(layers)
@@ -70,5 +75,5 @@ for T in Ts:
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (reps * nch * C)
     nbytes = np.mean([layers[i % L].touched_bytes(asg[i % nb]) for i in range(nch * C)])
-    print(f"{lib} {wl} T={T} step {us:.2f} us  {nbytes / us / 1e3:.1f} GB/s", flush=True)
+    print(f"{lib} {wl} lg={layers[0].lanes_per_row(T)} T={T} step {us:.2f} us  {nbytes / us / 1e3:.1f} GB/s", flush=True)
     del graphs
