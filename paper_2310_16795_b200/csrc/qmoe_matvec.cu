@@ -810,7 +810,11 @@ __device__ __forceinline__ int warp_plan_sort(const int32_t* __restrict__ assign
     k[j] = (t < T && e >= 0 && e < E) ? ((uint32_t)e << 8) | (uint32_t)t : 0xFFFFFFFFu;
   }
 #pragma unroll
+  // the sorting network only needs to span the first pow2 >= T positions
+  // (the rest hold invalid keys, already in place): small steps sort fast
+  const int kmax = T <= 1 ? 1 : (2 << (31 - __clz(T - 1)));
   for (int kk = 2; kk <= 32 * NPL; kk <<= 1) {
+    if (kk > kmax) break;
 #pragma unroll
     for (int jd = kk >> 1; jd > 0; jd >>= 1) {
       if (jd < NPL) {
@@ -1082,9 +1086,9 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     const int tb = s_split[0], te = s_split[1];
     PlanRuns src{runs4, nch, S.mats, 0, S.lg_wi, S.tasks_wi, nullptr, 0, S.d_model};
     pipe_range<PlanRuns, false>(S.wi, src, tb, te, PS, tab_s, &tab_bar);
-    __threadfence();  // this thread's h stores before the CTA's release below
-    __syncthreads();
+    __syncthreads();  // the CTA's h stores, then one gpu-scope release by thread 0 (cumulative)
     if (threadIdx.x == 0 && tb < te) {
+      __threadfence();
       for (int r = tb / S.tasks_wi; r * S.tasks_wi < te; ++r) {
         const int a = max(tb, r * S.tasks_wi), b = min(te, (r + 1) * S.tasks_wi);
         atomicAdd(S.counters + 1 + r, b - a);

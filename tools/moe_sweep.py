@@ -24,8 +24,9 @@ L2 = 126 << 20
 layers, pool = [], 0
 while pool < 4 * L2:
     lay = build_layer(E, d_model, d_ff, seed=len(layers), dic=dic, device=dev, max_tokens=max(Ts))
-    if "HOT" in os.environ:
+    if "HOT" in os.environ:  # hot-table entries staged per step (overrides the size rule)
         lay.STEP_HOT_MAX = int(os.environ["HOT"])
+        lay.hot_entries = lambda T, wi, h=int(os.environ["HOT"]): h
     if "LG" in os.environ:  # "wi,wo": lanes per row (log2) for every T (bounded by the checkpoints)
         lgs = tuple(min(int(v), c) for v, c in zip(os.environ["LG"].split(","), lay.max_lg))
         for T in Ts:
