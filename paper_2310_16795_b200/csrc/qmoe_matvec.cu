@@ -800,7 +800,7 @@ __device__ __forceinline__ int block_excl_scan2(int v, int w, int& wtot, int2* w
 template <int NPL>
 __device__ __forceinline__ int warp_plan_sort(const int32_t* __restrict__ assign, int T, int E, int ntu, int w2,
                                               int* order, int* runs4, int* wpre, int* count_out, int32_t* order_out,
-                                              bool write_out) {
+                                              bool write_out, int* nvalid_out = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t k[NPL];
 #pragma unroll
@@ -912,6 +912,12 @@ __device__ __forceinline__ int warp_plan_sort(const int32_t* __restrict__ assign
   }
   const int total = __shfl_sync(FULL_MASK, rinc, 31);
   if (lane == 31) wpre[total] = winc;
+  if (nvalid_out) {  // tokens with an expert (valid keys sort first)
+    int nv = 0;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) nv += __popc(__ballot_sync(FULL_MASK, k[j] != 0xFFFFFFFFu));
+    if (lane == 0) *nvalid_out = nv;
+  }
   return total;
 }
 
@@ -936,6 +942,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   // ---- 1. plan
   bool wpre_ready = false;
   __shared__ int s_nch;
+  __shared__ int s_nvalid;  // tokens with an expert
   if (T <= WARP_PLAN_MAX) {
     // one warp sorts the (expert, token) keys; no work proportional to E.
     // (Block 0 publishes the plan after its wo phase, off the critical path.)
@@ -943,13 +950,17 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       const bool wo = false;
       int n;
       if (T <= 32)
-        n = warp_plan_sort<1>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+        n = warp_plan_sort<1>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+                                   &s_nvalid);
       else if (T <= 64)
-        n = warp_plan_sort<2>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+        n = warp_plan_sort<2>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+                                   &s_nvalid);
       else if (T <= 128)
-        n = warp_plan_sort<4>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+        n = warp_plan_sort<4>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+                                   &s_nvalid);
       else
-        n = warp_plan_sort<8>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo);
+        n = warp_plan_sort<8>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+                                   &s_nvalid);
       if (threadIdx.x == 0) s_nch = n;
     }
     wpre_ready = true;
@@ -1027,6 +1038,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     }
     if (blockIdx.x == 0 && S.order_out)
       for (int t = threadIdx.x; t < start[E]; t += THREADS) S.order_out[t] = order[t];
+    if (threadIdx.x == 0) s_nvalid = start[E];
 
   }
   __syncthreads();
@@ -1108,7 +1120,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   // outputs (per-expert counts, the stable expert-major token order)
   __syncthreads();
   trace_stamp(S.wi.trace, 3);
-  {
+  if (s_nvalid < T) {  // some token has no expert
     float* y = reinterpret_cast<float*>(S.wo.y);
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
       const int e = __ldg(S.assign + t);
@@ -1116,27 +1128,21 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
         for (int i = threadIdx.x; i < S.d_model; i += THREADS) y[(int64_t)t * S.wo.ldy + i] = 0.f;
     }
   }
-  if (wpre_ready && blockIdx.x == 0) {
+  if (wpre_ready && blockIdx.x == 0 && (S.count_out || S.order_out)) {  // on request (nullable outputs)
     if (S.count_out)
       for (int e = threadIdx.x; e < E; e += THREADS) S.count_out[e] = 0;
     __syncthreads();
-    int nvalid = 0;  // tokens with an expert: the sum of the runs' token counts
-    for (int r = threadIdx.x; r < nch; r += THREADS) {
-      if (S.count_out) atomicAdd(S.count_out + runs4[4 * r], runs4[4 * r + 1]);
-      nvalid += runs4[4 * r + 1];
-    }
-    __shared__ int s_nvalid;
-    if (threadIdx.x == 0) s_nvalid = 0;
-    __syncthreads();
-    if (nvalid) atomicAdd(&s_nvalid, nvalid);
-    __syncthreads();
+    if (S.count_out)
+      for (int r = threadIdx.x; r < nch; r += THREADS) atomicAdd(S.count_out + runs4[4 * r], runs4[4 * r + 1]);
     if (S.order_out)
       for (int t = threadIdx.x; t < s_nvalid; t += THREADS) S.order_out[t] = order[t];
   }
-  // ---- 5. last CTA re-arms the counters
+  // ---- 5. last CTA re-arms the counters (acq_rel: this CTA's counter reads
+  // are done before its arrival; the last arriver sees everyone's)
   if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(S.counters, 1) == (int)gridDim.x - 1) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(S.counters) : "memory");
+    if (old == (int)gridDim.x - 1) {
       for (int r = 0; r < nch; ++r) S.counters[1 + r] = 0;
       S.counters[0] = 0;
       __threadfence();

@@ -97,6 +97,10 @@ class CompressedMoELayer:
         self._retired = []
         self._stages = {}
         self.dense_mode = dense
+        # the fused step publishes its dispatcher plan (self.order /
+        # self.expert_count, as qmoe_moe_plan) only on request: it costs the
+        # step's tail
+        self.publish_plan = False
         # one cooperative launch per step (sparse dictionaries)
         self.fused = sparse and fused
         self._alloc(max_tokens)
@@ -276,7 +280,7 @@ class CompressedMoELayer:
             with torch.cuda.stream(stream):
                 out.zero_()
 
-    DENSE_MIN_TOKENS = 7.0  # tokens per touched expert above which decode-then-MMA wins (measured: 6 -> streaming, 8 -> dense)
+    DENSE_MIN_TOKENS = 10.0  # tokens per touched expert from which decode-then-MMA wins (measured round 2: 8 -> streaming, 12 -> dense)
 
     def use_dense(self, T: int) -> bool:
         """Batched regime: each expert block decoded once and multiplied with
@@ -324,7 +328,8 @@ class CompressedMoELayer:
         _lib.check(_lib.lib.qmoe_moe_step_gated(
             self.handle, self._table(), _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit,
             lg_wi, lg_wo, self.d_model, self.d_ff, _lib.ptr(x), xt, x.stride(0), _lib.ptr(self.h), self.h.stride(0),
-            _lib.ptr(out), out.stride(0), _lib.ptr(self.counters), _lib.ptr(self.order), _lib.ptr(self.expert_count),
+            _lib.ptr(out), out.stride(0), _lib.ptr(self.counters),
+            _lib.ptr(self.order) if self.publish_plan else 0, _lib.ptr(self.expert_count) if self.publish_plan else 0,
             min(self.STEP_HOT_MAX, max(self.hot_entries(T, True), self.hot_entries(T, False))), _lib.ptr(gate),
             _lib.stream_ptr(stream)))
 

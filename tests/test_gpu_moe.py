@@ -57,6 +57,7 @@ def test_moe_random_layer_vs_oracle(dic, odic, T):
             pair.append((rows, cols, c.codewords, c.row_off, c.row_minmax))
         host.append(tuple(pair))
     layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=4)
+    layer.publish_plan = True  # the dispatcher outputs are checked below
     x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
     assign = q.RouterSim(E, rule="argmax", seed=1, skew=0.5 if T > 50 else 0.0).assign(x)
     y = layer.forward(x, assign)
@@ -233,6 +234,7 @@ def test_fused_step_equals_grouped_passes_and_plan(dic, T):
     E, d_model, d_ff = 6, 192, 640
     wi, wo, _ = _random_layer(dic, rng, E, d_model, d_ff, T)
     layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+    layer.publish_plan = True
     assert layer.fused
     x = torch.from_numpy(q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))).cuda().to(torch.bfloat16)
     a_np = rng.integers(-1, E + 1, size=T).astype(np.int32)  # -1 and E: no expert (dropped)
@@ -261,6 +263,7 @@ def test_fused_plan_many_experts(dic):
     E, d_model, d_ff, T = 600, 64, 128, 160
     wi, wo, _ = _random_layer(dic, rng, E, d_model, d_ff, T)
     layer = q.CompressedMoELayer(wi, wo, dic, max_tokens=T)
+    layer.publish_plan = True
     assert layer.fused
     x = torch.from_numpy(q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))).cuda().to(torch.bfloat16)
     a_np = np.where(rng.random(T) < 0.5, rng.integers(0, 8, size=T), rng.integers(-2, E + 2, size=T)).astype(np.int32)

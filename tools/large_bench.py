@@ -1,6 +1,6 @@
 """Config 3 (Switch-large-128, batched tokens): MoE step time of the
-decode-then-MMA path vs the streaming path vs bf16 (cuBLAS grouped/looped and
-HBM speed-of-light). Experiment harness; numbers go to DESIGN.md."""
+decode-then-MMA path vs the streaming path vs bf16 (grouped bf16 GEMM and HBM
+speed-of-light). Experiment harness; numbers go to DESIGN.md."""
 import os, sys, json
 import numpy as np
 import torch
@@ -57,21 +57,24 @@ for T in [int(t) for t in sys.argv[1:]] or [256, 1024, 4096]:
     ad = [torch.from_numpy(a).to(dev) for a in asg]
     outs = [torch.empty((T, d_model), device=dev) for _ in range(L)]
     res = {}
-    for mode in ("1", "0"):
-        os.environ["QMOE_DENSE"] = mode
-        res["dense" if mode == "1" else "stream"] = timed(
+    for mode in ("always", "never"):
+        for lay in layers:
+            lay.dense_mode = mode
+        res["dense" if mode == "always" else "stream"] = timed(
             lambda i: layers[i % L].forward_device(xd[i % 2], ad[i % 2], out=outs[i % L]), 2 * L)
-    os.environ.pop("QMOE_DENSE")
-    # bf16: per-expert cuBLAS GEMMs over the expert's tokens (index_select / index_copy), CUDA graph
-    plans = [[(int(e), torch.from_numpy(np.flatnonzero(a == e)).to(dev)) for e in np.unique(a)] for a in asg]
+    # bf16: tokens sorted by expert, two grouped bf16 GEMMs (torch._grouped_mm), CUDA graph
+    plans = []
+    for a in asg:
+        plans.append((torch.from_numpy(np.argsort(a, kind="stable")).to(dev),
+                      torch.from_numpy(np.cumsum(np.bincount(a, minlength=E)).astype(np.int32)).to(dev)))
     yb = [torch.empty((T, d_model), device=dev, dtype=torch.bfloat16) for _ in range(2)]
 
     def bf16_step(i):
         b = i % 2
-        for e, idx in plans[b]:
-            h = torch.relu(xd[b].index_select(0, idx) @ Wi[e].t())
-            yb[b].index_copy_(0, idx, h @ Wo[e].t())
-    res["bf16_cublas"] = timed(bf16_step, 2)
+        order, offs = plans[b]
+        h = torch.relu(torch._grouped_mm(xd[b].index_select(0, order), Wi.transpose(1, 2), offs=offs))
+        yb[b].index_copy_(0, order, torch._grouped_mm(h, Wo.transpose(1, 2), offs=offs))
+    res["bf16_grouped_gemm"] = timed(bf16_step, 2)
     ne = np.mean([len(np.unique(a)) for a in asg])
     res["bf16_sol"] = ne * 2 * d_model * d_ff * 2 / (peak * 1e9) * 1e6
     cbytes = np.mean([layers[0].touched_bytes(a) for a in asg])
