@@ -275,8 +275,10 @@ int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matr
  * waiting only for its own wi run (d_y rows of ldy = bf16(wo_e h_t), f32).
  * Experts: d_mats[2e] = wi_e (d_ff x d_model), d_mats[2e+1] = wo_e, RAW layout;
  * lg_wi / lg_wo <= the checkpoint lg every wi / wo matrix stores.
- * d_counters: int32[T + 1], zero before the first call; the kernel leaves it
- * zeroed. d_order / d_expert_count (nullable) receive the plan as in
+ * d_counters: int32[2C + 4] for steps of T <= C tokens, zero before the first
+ * call except d_counters[2] = C (two parity sets of C per-run counters after
+ * a 64-bit arrival ticket; the kernel keeps them consistent across calls with
+ * no reset). d_order / d_expert_count (nullable) receive the plan as in
  * qmoe_moe_plan. QMOE_EUNSUPPORTED when E and T do not fit the shared-memory
  * plan (use the grouped path). */
 int qmoe_moe_step(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_assign, int32_t T,

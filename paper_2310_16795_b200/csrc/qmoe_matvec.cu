@@ -699,15 +699,20 @@ __global__ void __launch_bounds__(THREADS, 1) pipe_matvec_kernel(SegParams P) {
 //      relu(bf16(wi_e x_t)) stored bf16; each CTA then publishes how many
 //      tasks of each run it finished (release: fence + atomic add);
 //   3. wo phase: before staging a run's h rows a CTA waits until all of that
-//      run's wi tasks are published (acquire), then y = bf16(wo_e h_t);
-//   4. the last CTA to finish re-zeroes the counters for the next step.
+//      run's wi tasks are published (acquire), then y = bf16(wo_e h_t).
+// Counters need no end-of-step reset: each CTA takes an arrival ticket at its
+// start (64-bit atomic, latency hidden by the plan); ticket / grid = the step
+// number s, whose parity picks one of two counter sets; every CTA zeroes its
+// slice of the OTHER set (last used by step s - 1, next used by step s + 1 —
+// both separated from step s by kernel boundaries), so no step ends with a
+// grid-wide release / re-arm round trip.
 // One table fill, no launch gaps, and the wi tail overlaps the wo start.
 struct PlanRuns {
   const int* runs4;  // shared: per run {expert, ntok, tok0, tok1}
   int n;
   const qmoe_matrix* mats;
   int pass, lg, tasks_per_run;
-  const int* counters;  // wo: counters[1 + r] reaches `need` when run r's wi tasks are done
+  const int* counters;  // wo: counters[r] reaches `need` when run r's wi tasks are done
   int need;
   int cols;  // columns of every matrix of this pass
   __device__ __forceinline__ Run get(int r) const {
@@ -738,7 +743,7 @@ struct PlanRuns {
     if (!counters) return;
     for (;;) {
       int v;
-      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(counters + 1 + r));
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(counters + r));
       if (v >= need) break;
       __nanosleep(128);
     }
@@ -752,7 +757,7 @@ struct StepParams {
   const qmoe_matrix* mats;
   int lg_wi, lg_wo, tasks_wi, tasks_wo;
   int d_model, d_ff;
-  int32_t* counters;  // int32[T + 1], zero at launch: [0] = CTAs done, [1 + r] = wi tasks done of run r
+  int32_t* counters;  // {u64 arrival tickets, capacity C, -, int32[C] set 0, int32[C] set 1}
   int32_t* order_out;
   int32_t* count_out;
   int plan_off;       // byte offset of the plan area in dynamic shared memory
@@ -939,6 +944,12 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   __shared__ __align__(8) uint64_t tab_bar;
   trace_stamp(S.wi.trace, 0);
   table_fill_async(PW.gtab, PW.H, &tab_bar);  // overlaps the plan below
+  __shared__ unsigned long long s_ticket;
+  if (threadIdx.x == 32) {  // arrival ticket (consumed after the plan: its latency is hidden)
+    unsigned long long t;
+    asm volatile("atom.add.relaxed.gpu.u64 %0, [%1], 1;" : "=l"(t) : "l"(S.counters) : "memory");
+    s_ticket = t;
+  }
   // ---- 1. plan
   bool wpre_ready = false;
   __shared__ int s_nch;
@@ -1093,6 +1104,14 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   __syncthreads();
   trace_stamp(S.wi.trace, 1);
   const uint32_t tab_s = smem_base();
+  // this step's counter set (step parity); zero my slice of the other one
+  const int ccap = S.counters[2];
+  const int parity = (int)((s_ticket / gridDim.x) & 1ull);
+  int32_t* cnt_cur = S.counters + 4 + parity * ccap;
+  {
+    int32_t* oth = S.counters + 4 + (parity ^ 1) * ccap;
+    for (int i = blockIdx.x * THREADS + threadIdx.x; i < ccap; i += gridDim.x * THREADS) oth[i] = 0;
+  }
   // ---- 2. wi phase
   {
     const int tb = s_split[0], te = s_split[1];
@@ -1103,7 +1122,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       __threadfence();
       for (int r = tb / S.tasks_wi; r * S.tasks_wi < te; ++r) {
         const int a = max(tb, r * S.tasks_wi), b = min(te, (r + 1) * S.tasks_wi);
-        atomicAdd(S.counters + 1 + r, b - a);
+        atomicAdd(cnt_cur + r, b - a);
       }
     }
     trace_stamp(S.wi.trace, 2);
@@ -1111,7 +1130,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   // ---- 3. wo phase
   {
     const int tb = s_split[2], te = s_split[3];
-    PlanRuns src{runs4, nch, S.mats, 1, S.lg_wo, S.tasks_wo, S.counters, S.tasks_wi, S.d_ff};
+    PlanRuns src{runs4, nch, S.mats, 1, S.lg_wo, S.tasks_wo, cnt_cur, S.tasks_wi, S.d_ff};
     pipe_range<PlanRuns, true>(S.wo, src, tb, te, PS, tab_s);
   }
   // ---- 4. off the critical path: tokens without an expert (ids outside
@@ -1136,17 +1155,6 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       for (int r = threadIdx.x; r < nch; r += THREADS) atomicAdd(S.count_out + runs4[4 * r], runs4[4 * r + 1]);
     if (S.order_out)
       for (int t = threadIdx.x; t < s_nvalid; t += THREADS) S.order_out[t] = order[t];
-  }
-  // ---- 5. last CTA re-arms the counters (acq_rel: this CTA's counter reads
-  // are done before its arrival; the last arriver sees everyone's)
-  if (threadIdx.x == 0) {
-    int old;
-    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(S.counters) : "memory");
-    if (old == (int)gridDim.x - 1) {
-      for (int r = 0; r < nch; ++r) S.counters[1 + r] = 0;
-      S.counters[0] = 0;
-      __threadfence();
-    }
   }
 }
 

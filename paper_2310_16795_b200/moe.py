@@ -128,7 +128,9 @@ class CompressedMoELayer:
         ldh = (self.d_ff + 7) // 8 * 8  # 16-byte aligned hidden rows (bulk staging)
         self.h = _lib.padded_empty(max(1, T) * ldh, torch.bfloat16, dev).view(max(1, T), ldh)[:, : self.d_ff]
         self.bad = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
-        self.counters = torch.zeros(max(1, T) + 1, dtype=torch.int32, device=dev)  # fused step (self-resetting)
+        # fused step: {u64 arrival tickets, capacity C, -, 2 x C per-run counters} (qmoe_moe_step)
+        self.counters = torch.zeros(2 * max(1, T) + 4, dtype=torch.int32, device=dev)
+        self.counters[2] = max(1, T)
 
     def _write_descriptors(self) -> None:
         """Device array of qmoe_matrix descriptors (wi_e = 2e, wo_e = 2e + 1).
