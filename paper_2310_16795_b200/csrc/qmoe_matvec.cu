@@ -282,6 +282,10 @@ __device__ __forceinline__ void store_row(const SegParams& P, const Run& R, int 
 // partial groups inside a row), and the boundaries nest across lg.
 constexpr int WIN_RUNS = 16;
 constexpr int WARP_PLAN_MAX = 256;  // fused step: single-warp dispatcher plan up to this many tokens
+// ... but above this many tokens the block-scan plan is faster unless E is
+// large (its loops are E-proportional; measured: T = 160 / 256 with E = 128:
+// 93.6 -> 86.3 / 126 -> 120 us; E = 2048: 362 -> 519 us)
+constexpr int WARP_PLAN_SMALL_E_MAX = 128, WARP_PLAN_LARGE_E = 512;
 
 struct WinRun {
   const uint16_t* cw;
@@ -762,6 +766,7 @@ struct StepParams {
   int32_t* count_out;
   int plan_off;       // byte offset of the plan area in dynamic shared memory
   int w2;             // split weight of a 2-token run (a 1-token run weighs 8)
+  int warp_plan;      // 1: single-warp sorting plan, 0: block-scan plan (see WARP_PLAN_*)
 };
 
 __device__ __forceinline__ int block_excl_scan2(int v, int w, int& wtot, int2* wsum, int* tot) {
@@ -933,7 +938,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   const int E = S.E, T = S.T, ntu = S.ntu;
   // plan area: [cnt E | start E+1 | choff E+1] (block-scan plan only), then
   // order T | runs4 4T | wpre T+1 (weighted run prefix)
-  const int ecells = T <= WARP_PLAN_MAX ? 0 : 3 * E + 2;
+  const int ecells = S.warp_plan ? 0 : 3 * E + 2;
   int* cnt = reinterpret_cast<int*>(seg_smem + S.plan_off);
   int* start = cnt + E;
   int* choff = start + E + 1;
@@ -954,7 +959,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   bool wpre_ready = false;
   __shared__ int s_nch;
   __shared__ int s_nvalid;  // tokens with an expert
-  if (T <= WARP_PLAN_MAX) {
+  if (S.warp_plan) {
     // one warp sorts the (expert, token) keys; no work proportional to E.
     // (Block 0 publishes the plan after its wo phase, off the critical path.)
     if (threadIdx.x < 32) {
@@ -1474,8 +1479,9 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   const int maxc = std::max(d_model, d_ff);
   const size_t slot = (size_t)2 * 4 * (((maxc + 32) + 3) & ~3);
   const size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
-  // the single-warp plan (T <= WARP_PLAN_MAX) needs no per-expert arrays
-  const size_t ecells = T <= WARP_PLAN_MAX ? 0 : (size_t)3 * E + 2;
+  // the single-warp plan needs no per-expert arrays
+  SP.warp_plan = T <= WARP_PLAN_SMALL_E_MAX || (T <= WARP_PLAN_MAX && E > WARP_PLAN_LARGE_E);
+  const size_t ecells = SP.warp_plan ? 0 : (size_t)3 * E + 2;
   const size_t plan = ((ecells + 1 + 6 * (size_t)T) * 4 + 15) & ~(size_t)15;
   const size_t static_smem = 2048;
   if (xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
