@@ -532,9 +532,9 @@ def decompress_at_scale(dic, dev, hbm_peak, rows=98304, cols=3072):
 
 def profiled_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/roofline_r01.json), or None."""
+    capture (profiles/roofline_r02.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "roofline_r01.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "roofline_r02.json")) as fh:
             d = json.load(fh)
         return d.get("dram_bytes_per_launch"), d
     except Exception:
@@ -811,7 +811,7 @@ def main():
                          "ms_per_launch_source": ("timed region / K (one fused kernel per step)" if fused
                                                   else "eager back-to-back launches"),
                          "eager_ms_per_launch": eager_ms,
-                         "traffic_source": "profiles/roofline_r01.json (ncu --set full, dram__bytes_read+write per "
+                         "traffic_source": "profiles/roofline_r02.json (ncu --set full, dram__bytes_read+write per "
                                            "launch of the same kernel on the same workload)"},
             "bf16_baseline": {"ms_per_step_cublas": bf16_ms, "cublas_impl": bf16_impl,
                               "ms_per_step_hbm_sol": bf16_sol_ms,
