@@ -740,7 +740,26 @@ def main():
                              "(graphs of 10 layer steps, cold pool) vs uncompressed bf16 cuBLAS gemv -> relu -> "
                              "gemv over a cold pool of experts"}
 
-    # ---- parity of the timed path + CPU baseline (oracle port on this host),
+    # ---- the pool as a model (config 5's structure on this workload): L
+    # residual blocks, each = device hash router + ONE fused launch computing
+    # x + moe(x) in bf16, the whole forward one CUDA graph; vs L x the bf16
+    # expert FFN per token measured above
+    model_fwd = None
+    if rank == 0 and world == 1 and not args.profile:
+        routers = [q.DeviceRouter(q.RouterSim(E, rule="hash", seed=100 + l), d_model) for l in range(L)]
+        model = q.CompressedMoEModel(layers, routers)
+        model_fwd = {"layers": L, "routing": "RouterSim hash per layer, on the device (bit-exact)"}
+        for Tm in (1, T):
+            xm = xd[0][:Tm].contiguous()
+            gm = _capture(lambda: model.forward_device(xm))
+            ms_f = _time_graphs([gm], 10, 3)
+            model_fwd[f"T{Tm}"] = {"forward_us": ms_f * 1e3, "us_per_layer": ms_f * 1e3 / L,
+                                   "tokens_per_s": Tm / ms_f * 1e3}
+            del gm
+        if per_token:
+            model_fwd["bf16_cublas_T1_forward_us"] = per_token["bf16_cublas_us_per_token"] * L
+
+
     # rank 0 at N=1 only: layer 0 (the survey's seeded weights) on batch 0,
     # all T tokens, through the composed CPU oracle on the device streams
     cpu = parity = None
@@ -821,6 +840,7 @@ def main():
                                       "bf16 GEMM over the touched experts in a CUDA graph), and its HBM "
                                       "speed-of-light (bf16 bytes of the touched experts / measured HBM peak)"},
             "per_token": per_token,
+            "model_forward": model_fwd,
             "parity": parity,
             "kernel_at_scale": at_scale,
             "decompress_at_scale": decomp,

@@ -105,8 +105,10 @@ enum {
   QMOE_Y_ACCUM_F32 = 0,     /* y (f32) += bf16(dot)                       (codec.py:243) */
   QMOE_Y_RELU_BF16 = 1,     /* y (bf16) = relu(bf16(dot)) — the FFN hidden h, written
                                once from zero: equals relu(fused_matvec(wi, x, y=0)) */
-  QMOE_Y_STORE_F32 = 2      /* y (f32) = 0 + bf16(dot): accumulate into a zero y
+  QMOE_Y_STORE_F32 = 2,     /* y (f32) = 0 + bf16(dot): accumulate into a zero y
                                without reading it */
+  QMOE_Y_RESID_BF16 = 3     /* fused step only (qmoe_moe_step_resid): y (bf16) =
+                               bf16(x + gate * bf16(dot)), the layer's residual add */
 };
 
 /* ------------------------------------------------------------------ host-only
@@ -298,6 +300,17 @@ int qmoe_moe_step_gated(qmoe_dict_t dict, const uint32_t* d_table, const int32_t
                         int32_t lg_wo, int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype,
                         int64_t ldx, uint16_t* d_h, int64_t ldh, float* d_y, int64_t ldy,
                         int32_t* d_counters, int32_t* d_order, int32_t* d_expert_count,
+                        int32_t hot_entries, const float* d_gate, void* stream);
+
+/* One residual MoE block of a model forward in one launch (SURVEY §8 (f),
+ * config 5): as qmoe_moe_step_gated on bf16 tokens d_x, but the output is the
+ * next layer's input, d_out (bf16, rows of ldo) = bf16(x + gate * bf16(wo_e
+ * h_t)) — x's row for tokens without an expert. d_gate nullable (gate 1).
+ * d_out must not alias d_x. */
+int qmoe_moe_step_resid(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_assign, int32_t T,
+                        int32_t E, const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi,
+                        int32_t lg_wo, int32_t d_model, int32_t d_ff, const uint16_t* d_x, int64_t ldx,
+                        uint16_t* d_h, int64_t ldh, uint16_t* d_out, int64_t ldo, int32_t* d_counters,
                         int32_t hot_entries, const float* d_gate, void* stream);
 
 /* Top-1 router on the device, replaces RouterSim.assign

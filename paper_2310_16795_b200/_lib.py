@@ -48,7 +48,7 @@ class QmoeWork(ctypes.Structure):
                 ("tok", i32 * NT_MAX)]
 
 
-QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16, QMOE_Y_STORE_F32 = 0, 1, 2
+QMOE_Y_ACCUM_F32, QMOE_Y_RELU_BF16, QMOE_Y_STORE_F32, QMOE_Y_RESID_BF16 = 0, 1, 2, 3
 
 
 WORK_BYTES = ctypes.sizeof(QmoeWork)
@@ -84,6 +84,8 @@ _SIGS = {
                                      i64, vp, i64, vp, vp, vp, i32, vp]),
     "qmoe_moe_step_gated": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, ctypes.c_int, i64,
                                            vp, i64, vp, i64, vp, vp, vp, i32, vp, vp]),
+    "qmoe_moe_step_resid": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, i64, vp, i64,
+                                           vp, i64, vp, i32, vp, vp]),
     "qmoe_route_scratch": (i64, [i32, i32, i32]),
     "qmoe_ep_slots": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "qmoe_ep_combine": (ctypes.c_int, [vp, vp, i32, i32, vp, vp]),

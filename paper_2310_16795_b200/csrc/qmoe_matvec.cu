@@ -67,7 +67,9 @@ struct SegParams {
   int64_t ldy;
   int xcap;                   // x elements staged per token
   int xbytes;                 // x staging bytes (pipe kernel: several runs' slots)
-  const float* gate;          // STORE_F32 only, nullable: y = gate[t] * bf16(dot)
+  const float* gate;          // STORE_F32 / RESID_BF16, nullable: o = gate[t] * bf16(dot)
+  const uint16_t* resid;      // RESID_BF16: y (bf16) = bf16(resid[t] + o), rows of ldr
+  int64_t ldr;
   unsigned long long* trace;  // fused step debug stamps (qmoe_debug_step_trace), nullable
 };
 
@@ -258,6 +260,11 @@ __device__ __forceinline__ void store_row(const SegParams& P, const Run& R, int 
       float o = v + 0.f;  // == 0 + v
       if (P.gate) o *= __ldg(P.gate + t);
       reinterpret_cast<float*>(P.y)[t * P.ldy + row] = o;
+    } else if (P.y_mode == QMOE_Y_RESID_BF16) {  // the layer's residual add, fused
+      float o = v + 0.f;
+      if (P.gate) o *= __ldg(P.gate + t);
+      const float r = __uint_as_float((uint32_t)P.resid[t * P.ldr + row] << 16);
+      reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(bf16_round_dev(r + o)) >> 16);
     } else {
       float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
       *yp = *yp + v;
@@ -1144,12 +1151,17 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   // outputs (per-expert counts, the stable expert-major token order)
   __syncthreads();
   trace_stamp(S.wi.trace, 3);
-  if (s_nvalid < T) {  // some token has no expert
-    float* y = reinterpret_cast<float*>(S.wo.y);
+  if (s_nvalid < T) {  // some token has no expert: zero expert output (residual mode: the input row)
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
       const int e = __ldg(S.assign + t);
-      if (e < 0 || e >= E)
+      if (e >= 0 && e < E) continue;
+      if (S.wo.y_mode == QMOE_Y_RESID_BF16) {
+        uint16_t* y = reinterpret_cast<uint16_t*>(S.wo.y);
+        for (int i = threadIdx.x; i < S.d_model; i += THREADS) y[(int64_t)t * S.wo.ldy + i] = S.wo.resid[(int64_t)t * S.wo.ldr + i];
+      } else {
+        float* y = reinterpret_cast<float*>(S.wo.y);
         for (int i = threadIdx.x; i < S.d_model; i += THREADS) y[(int64_t)t * S.wo.ldy + i] = 0.f;
+      }
     }
   }
   if (wpre_ready && blockIdx.x == 0 && (S.count_out || S.order_out)) {  // on request (nullable outputs)
@@ -1426,11 +1438,12 @@ int qmoe_moe_step(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assig
                              nullptr, stream);
 }
 
-int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assign, int32_t T, int32_t E,
-                        const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo,
-                        int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h,
-                        int64_t ldh, float* d_y, int64_t ldy, int32_t* d_counters, int32_t* d_order,
-                        int32_t* d_expert_count, int32_t hot_entries, const float* d_gate, void* stream) {
+static int moe_step_impl(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assign, int32_t T, int32_t E,
+                         const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo,
+                         int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h,
+                         int64_t ldh, void* d_y, int64_t ldy, int32_t* d_counters, int32_t* d_order,
+                         int32_t* d_expert_count, int32_t hot_entries, const float* d_gate, const uint16_t* d_resid,
+                         int64_t ldr, void* stream) {
   if (T == 0 && d && E >= 1) return QMOE_OK;  // nothing to do (empty buffers may be null)
   if (!d || !d->d_stab || !d_assign || T < 0 || E < 1 || !d_mats || tokens_per_run < 1 ||
       tokens_per_run > NT_STREAM || lg_wi < 0 || lg_wi > 5 || lg_wo < 0 || lg_wo > 5 || d_model <= 0 ||
@@ -1457,9 +1470,11 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   SP.wo.x_bf16 = 1;
   SP.wo.ldx = ldh;
   SP.wo.y = d_y;
-  SP.wo.y_mode = QMOE_Y_STORE_F32;
+  SP.wo.y_mode = d_resid ? QMOE_Y_RESID_BF16 : QMOE_Y_STORE_F32;
   SP.wo.ldy = ldy;
   SP.wo.gate = d_gate;
+  SP.wo.resid = d_resid;
+  SP.wo.ldr = ldr;
   SP.wi.trace = SP.wo.trace = g_trace_host;
   SP.assign = d_assign;
   SP.T = T;
@@ -1511,6 +1526,28 @@ int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
   }
   CK(le, "moe_step_kernel launch");
   return QMOE_OK;
+}
+
+int qmoe_moe_step_gated(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assign, int32_t T, int32_t E,
+                        const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo,
+                        int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h,
+                        int64_t ldh, float* d_y, int64_t ldy, int32_t* d_counters, int32_t* d_order,
+                        int32_t* d_expert_count, int32_t hot_entries, const float* d_gate, void* stream) {
+  return moe_step_impl(d, d_table, d_assign, T, E, d_mats, tokens_per_run, lg_wi, lg_wo, d_model, d_ff, d_x, x_dtype,
+                       ldx, d_h, ldh, d_y, ldy, d_counters, d_order, d_expert_count, hot_entries, d_gate, nullptr, 0,
+                       stream);
+}
+
+int qmoe_moe_step_resid(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d_assign, int32_t T, int32_t E,
+                        const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo,
+                        int32_t d_model, int32_t d_ff, const uint16_t* d_x, int64_t ldx, uint16_t* d_h, int64_t ldh,
+                        uint16_t* d_out, int64_t ldo, int32_t* d_counters, int32_t hot_entries, const float* d_gate,
+                        void* stream) {
+  if (!d_x) return qmoe::fail(QMOE_EINVAL, "bad argument");
+  if (d_out == d_x && T > 0) return qmoe::fail(QMOE_EINVAL, "d_out must not alias d_x (the wi phase reads it)");
+  return moe_step_impl(d, d_table, d_assign, T, E, d_mats, tokens_per_run, lg_wi, lg_wo, d_model, d_ff, d_x,
+                       QMOE_X_BF16, ldx, d_h, ldh, d_out, ldo, d_counters, nullptr, nullptr, hot_entries, d_gate, d_x,
+                       ldx, stream);
 }
 
 int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work* d_work, const int32_t* d_n_work,

@@ -335,6 +335,22 @@ class CompressedMoELayer:
             min(self.STEP_HOT_MAX, max(self.hot_entries(T, True), self.hot_entries(T, False))), _lib.ptr(gate),
             _lib.stream_ptr(stream)))
 
+    def step_resid(self, x, assign, out, gate=None, stream=None) -> None:
+        """One residual block in one launch (qmoe_moe_step_resid): out (bf16,
+        T x d_model) = bf16(x + [gate *] moe(x)), x a bf16 CUDA tensor with
+        16-byte aligned rows; tokens without an expert pass x through."""
+        T = assign.shape[0]
+        if T > self.max_tokens:
+            self._alloc(T)
+        self._T = T
+        lg_wi, lg_wo = self.lanes_per_row(T)
+        _lib.check(_lib.lib.qmoe_moe_step_resid(
+            self.handle, self._table(), _lib.ptr(assign), T, self.E, _lib.ptr(self.mats), self.tokens_per_unit,
+            lg_wi, lg_wo, self.d_model, self.d_ff, _lib.ptr(x), x.stride(0), _lib.ptr(self.h), self.h.stride(0),
+            _lib.ptr(out), out.stride(0), _lib.ptr(self.counters),
+            min(self.STEP_HOT_MAX, max(self.hot_entries(T, True), self.hot_entries(T, False))), _lib.ptr(gate),
+            _lib.stream_ptr(stream)))
+
     def forward_routed(self, x, router, gated: bool = False, out=None, stream=None):
         """Router + layer on the device: expert ids (and, with `gated`, the
         top-1 softmax probability scaling each output row — the Switch combine;
@@ -481,3 +497,54 @@ def load_moe_layer(wi_path: str, wo_path: str, dic: Dictionary, max_tokens: int 
     wi = read_stacked_device(wi_path, dic, d_ff, device)
     wo = read_stacked_device(wo_path, dic, d_model, device)
     return CompressedMoELayer(wi, wo, dic, max_tokens=max_tokens, **layer_kw)
+
+
+class CompressedMoEModel:
+    """A stack of residual compressed MoE blocks, the synthetic model of
+    BASELINE config 5: for every layer l, expert ids (and, when gated, the
+    top-1 softmax gate) from its router on the device (pipeline.DeviceRouter,
+    the reference's RouterSim rules), then ONE fused launch computing
+    x_{l+1} = bf16(x_l + [gate *] wo_e relu(wi_e x_l)) (qmoe_moe_step_resid).
+    Activations stay bf16 in HBM; the whole forward is device-only and
+    CUDA-graph capturable (two launches per layer with hash routing, three
+    with argmax)."""
+
+    def __init__(self, layers: list, routers: list, gated: bool = False):
+        if len(layers) != len(routers) or not layers:
+            raise ValueError("need one router per layer")
+        d = layers[0].d_model
+        if any(lay.d_model != d for lay in layers) or any(r.dim != d for r in routers):
+            raise ValueError("layers and routers must share d_model")
+        self.layers, self.routers, self.gated = layers, routers, gated
+        self.d_model = d
+        self._bufs = {}
+
+    def _buffers(self, T: int, device):
+        import torch
+
+        b = self._bufs.get(T)
+        if b is None:
+            ld = (self.d_model + 7) // 8 * 8  # 16-byte aligned bf16 rows
+            b = self._bufs[T] = [_lib.padded_empty(max(1, T) * ld, torch.bfloat16, device).view(max(1, T), ld)
+                                 [:T, : self.d_model] for _ in range(2)]
+        return b
+
+    def forward_device(self, x, stream=None, keep: bool = False):
+        """x: (T, d_model) bf16 CUDA tensor -> the last layer's output (a new
+        bf16 tensor); keep=True also returns every layer's input and routing."""
+        import torch
+
+        T = x.shape[0]
+        bufs = self._buffers(T, x.device)
+        cur = bufs[0]
+        cur.copy_(x)
+        trace = []
+        for l, (lay, router) in enumerate(zip(self.layers, self.routers)):
+            nxt = bufs[(l + 1) % 2]
+            assign, gate = router(cur, gated=self.gated, stream=stream)
+            if keep:
+                trace.append((cur.clone(), assign.clone()))
+            lay.step_resid(cur, assign, nxt, gate=gate, stream=stream)
+            cur = nxt
+        out = cur.clone()
+        return (out, trace) if keep else out

@@ -1,0 +1,9 @@
+# A/B of dense-pass variants: correctness (dense tests) + config-3 timing
+for v in ${VARIANTS:-dd4 dd3 dd2}; do
+  echo "== $v"
+  QMOE_LIB_PATH=variants/$v/libqmoe.so timeout 600 python -m pytest tests/test_gpu_moe.py tests/test_gpu_fullshape.py -q -x -k "dense" 2>&1 | tail -1
+  QMOE_LIB_PATH=variants/$v/libqmoe.so timeout 600 python tools/large_bench.py 1024 4096 2>&1 | grep "^{" | python -c "
+import sys, json
+for l in sys.stdin:
+    d = json.loads(l); print(d['T'], d['step_us'])"
+done
