@@ -306,12 +306,16 @@ int qmoe_moe_step_gated(qmoe_dict_t dict, const uint32_t* d_table, const int32_t
  * config 5): as qmoe_moe_step_gated on bf16 tokens d_x, but the output is the
  * next layer's input, d_out (bf16, rows of ldo) = bf16(x + gate * bf16(wo_e
  * h_t)) — x's row for tokens without an expert. d_gate nullable (gate 1).
- * d_out must not alias d_x. */
+ * d_out must not alias d_x. With d_hash_mult (uint64[d_model], RouterSim's
+ * hash multipliers) the block routes its tokens itself with the reference's
+ * hash rule (pipeline.py:166-174, bit-exact; d_assign unused, may be NULL;
+ * the ids go to d_assign_out when non-NULL): router + block = one launch. */
 int qmoe_moe_step_resid(qmoe_dict_t dict, const uint32_t* d_table, const int32_t* d_assign, int32_t T,
                         int32_t E, const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi,
                         int32_t lg_wo, int32_t d_model, int32_t d_ff, const uint16_t* d_x, int64_t ldx,
                         uint16_t* d_h, int64_t ldh, uint16_t* d_out, int64_t ldo, int32_t* d_counters,
-                        int32_t hot_entries, const float* d_gate, void* stream);
+                        int32_t hot_entries, const float* d_gate, const uint64_t* d_hash_mult,
+                        int32_t* d_assign_out, void* stream);
 
 /* Top-1 router on the device, replaces RouterSim.assign
  * (reference pipeline.py:164-182) for x already in HBM:

@@ -85,7 +85,7 @@ _SIGS = {
     "qmoe_moe_step_gated": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, ctypes.c_int, i64,
                                            vp, i64, vp, i64, vp, vp, vp, i32, vp, vp]),
     "qmoe_moe_step_resid": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp, i64, vp, i64,
-                                           vp, i64, vp, i32, vp, vp]),
+                                           vp, i64, vp, i32, vp, vp, vp, vp]),
     "qmoe_route_scratch": (i64, [i32, i32, i32]),
     "qmoe_ep_slots": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "qmoe_ep_combine": (ctypes.c_int, [vp, vp, i32, i32, vp, vp]),

@@ -774,6 +774,8 @@ struct StepParams {
   int plan_off;       // byte offset of the plan area in dynamic shared memory
   int w2;             // split weight of a 2-token run (a 1-token run weighs 8)
   int warp_plan;      // 1: single-warp sorting plan, 0: block-scan plan (see WARP_PLAN_*)
+  const uint64_t* hash_mult;  // non-null: route in-kernel (RouterSim hash, bit-exact) instead of reading assign
+  int32_t* assign_out;        // in-kernel routing: the ids (block 0 writes them), nullable
 };
 
 __device__ __forceinline__ int block_excl_scan2(int v, int w, int& wtot, int2* wsum, int* tot) {
@@ -815,7 +817,7 @@ __device__ __forceinline__ int block_excl_scan2(int v, int w, int& wtot, int2* w
 // with E (a c2048 layer has 2048 experts). Returns the run count; lane 0..31
 // all return it.
 template <int NPL>
-__device__ __forceinline__ int warp_plan_sort(const int32_t* __restrict__ assign, int T, int E, int ntu, int w2,
+__device__ __forceinline__ int warp_plan_sort(const int32_t* assign, int T, int E, int ntu, int w2,
                                               int* order, int* runs4, int* wpre, int* count_out, int32_t* order_out,
                                               bool write_out, int* nvalid_out = nullptr) {
   const int lane = threadIdx.x & 31;
@@ -823,7 +825,7 @@ __device__ __forceinline__ int warp_plan_sort(const int32_t* __restrict__ assign
 #pragma unroll
   for (int j = 0; j < NPL; ++j) {
     const int t = lane * NPL + j;
-    const int e = t < T ? __ldg(assign + t) : -1;
+    const int e = t < T ? assign[t] : -1;  // global, or shared when routed in-kernel
     k[j] = (t < T && e >= 0 && e < E) ? ((uint32_t)e << 8) | (uint32_t)t : 0xFFFFFFFFu;
   }
 #pragma unroll
@@ -952,6 +954,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   int* order = cnt + ecells;
   int* runs4 = order + T;
   int* wpre = runs4 + 4 * T;
+  int* s_asg = wpre + T + 1;  // in-kernel routing: the T expert ids
   const SegParams& PW = S.wi;
   __shared__ __align__(8) uint64_t tab_bar;
   trace_stamp(S.wi.trace, 0);
@@ -961,6 +964,31 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     unsigned long long t;
     asm volatile("atom.add.relaxed.gpu.u64 %0, [%1], 1;" : "=l"(t) : "l"(S.counters) : "memory");
     s_ticket = t;
+  }
+  // ---- 0. in-kernel routing (RouterSim hash, pipeline.py:166-174; the
+  // route_hash_kernel arithmetic): every CTA hashes the T tokens' f32 bit
+  // patterns itself — no router launch between blocks
+  const int32_t* asg = S.assign;
+  if (S.hash_mult) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint16_t* xb = reinterpret_cast<const uint16_t*>(S.wi.x);
+    for (int t = warp; t < T; t += NWARPS) {
+      uint64_t h = 0;
+      for (int k = lane; k < S.d_model; k += 32)
+        h += (uint64_t)((uint32_t)__ldg(xb + (int64_t)t * S.wi.ldx + k) << 16) * __ldg(S.hash_mult + k);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) h += __shfl_xor_sync(FULL_MASK, h, d);
+      if (lane == 0) {
+        h ^= h >> 33;
+        h *= 0xFF51AFD7ED558CCDull;
+        h ^= h >> 33;
+        const int e = (int)(h % (uint64_t)E);
+        s_asg[t] = e;
+        if (blockIdx.x == 0 && S.assign_out) S.assign_out[t] = e;
+      }
+    }
+    __syncthreads();
+    asg = s_asg;
   }
   // ---- 1. plan
   bool wpre_ready = false;
@@ -973,16 +1001,16 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       const bool wo = false;
       int n;
       if (T <= 32)
-        n = warp_plan_sort<1>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+        n = warp_plan_sort<1>(asg, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
                                    &s_nvalid);
       else if (T <= 64)
-        n = warp_plan_sort<2>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+        n = warp_plan_sort<2>(asg, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
                                    &s_nvalid);
       else if (T <= 128)
-        n = warp_plan_sort<4>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+        n = warp_plan_sort<4>(asg, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
                                    &s_nvalid);
       else
-        n = warp_plan_sort<8>(S.assign, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
+        n = warp_plan_sort<8>(asg, T, E, ntu, S.w2, order, runs4, wpre, S.count_out, S.order_out, wo,
                                    &s_nvalid);
       if (threadIdx.x == 0) s_nch = n;
     }
@@ -991,7 +1019,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     for (int e = threadIdx.x; e < E; e += THREADS) cnt[e] = 0;
     __syncthreads();
     for (int t = threadIdx.x; t < T; t += THREADS) {
-      const int e = __ldg(S.assign + t);
+      const int e = asg[t];
       if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);
     }
     __syncthreads();
@@ -1027,7 +1055,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
       const int lane = threadIdx.x;
       for (int t0 = 0; t0 < T; t0 += 32) {
         const int t = t0 + lane;
-        const int e = t < T ? __ldg(S.assign + t) : -1;
+        const int e = t < T ? asg[t] : -1;
         const bool ok = t < T && e >= 0 && e < E;
         const unsigned peers = __match_any_sync(FULL_MASK, ok ? e : -1);
         const int rank = __popc(peers & ((1u << lane) - 1u));
@@ -1153,7 +1181,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
   trace_stamp(S.wi.trace, 3);
   if (s_nvalid < T) {  // some token has no expert: zero expert output (residual mode: the input row)
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
-      const int e = __ldg(S.assign + t);
+      const int e = asg[t];
       if (e >= 0 && e < E) continue;
       if (S.wo.y_mode == QMOE_Y_RESID_BF16) {
         uint16_t* y = reinterpret_cast<uint16_t*>(S.wo.y);
@@ -1443,9 +1471,10 @@ static int moe_step_impl(qmoe_dict_t d, const uint32_t* d_table, const int32_t* 
                          int32_t d_model, int32_t d_ff, const void* d_x, int x_dtype, int64_t ldx, uint16_t* d_h,
                          int64_t ldh, void* d_y, int64_t ldy, int32_t* d_counters, int32_t* d_order,
                          int32_t* d_expert_count, int32_t hot_entries, const float* d_gate, const uint16_t* d_resid,
-                         int64_t ldr, void* stream) {
+                         int64_t ldr, void* stream, const uint64_t* d_hash_mult = nullptr,
+                         int32_t* d_assign_out = nullptr) {
   if (T == 0 && d && E >= 1) return QMOE_OK;  // nothing to do (empty buffers may be null)
-  if (!d || !d->d_stab || !d_assign || T < 0 || E < 1 || !d_mats || tokens_per_run < 1 ||
+  if (!d || !d->d_stab || (!d_assign && !d_hash_mult) || T < 0 || E < 1 || !d_mats || tokens_per_run < 1 ||
       tokens_per_run > NT_STREAM || lg_wi < 0 || lg_wi > 5 || lg_wo < 0 || lg_wo > 5 || d_model <= 0 ||
       d_ff <= 0 || !d_h || !d_y || !d_counters || (x_dtype != QMOE_X_F32 && x_dtype != QMOE_X_BF16))
     return qmoe::fail(QMOE_EINVAL, "bad argument");
@@ -1477,6 +1506,9 @@ static int moe_step_impl(qmoe_dict_t d, const uint32_t* d_table, const int32_t* 
   SP.wo.ldr = ldr;
   SP.wi.trace = SP.wo.trace = g_trace_host;
   SP.assign = d_assign;
+  SP.hash_mult = d_hash_mult;
+  SP.assign_out = d_assign_out;
+  if (d_hash_mult && x_dtype != QMOE_X_BF16) return qmoe::fail(QMOE_EINVAL, "in-kernel routing takes bf16 tokens");
   SP.T = T;
   SP.E = E;
   SP.ntu = tokens_per_run;
@@ -1497,7 +1529,7 @@ static int moe_step_impl(qmoe_dict_t d, const uint32_t* d_table, const int32_t* 
   // the single-warp plan needs no per-expert arrays
   SP.warp_plan = T <= WARP_PLAN_SMALL_E_MAX || (T <= WARP_PLAN_MAX && E > WARP_PLAN_LARGE_E);
   const size_t ecells = SP.warp_plan ? 0 : (size_t)3 * E + 2;
-  const size_t plan = ((ecells + 1 + 6 * (size_t)T) * 4 + 15) & ~(size_t)15;
+  const size_t plan = ((ecells + 1 + 6 * (size_t)T + (d_hash_mult ? (size_t)T : 0)) * 4 + 15) & ~(size_t)15;
   const size_t static_smem = 2048;
   if (xbytes + plan + static_smem + 4096 > (size_t)d->max_smem_optin)
     return qmoe::fail(QMOE_EUNSUPPORTED, "step too large for the fused kernel's shared memory (use the grouped path)");
@@ -1542,12 +1574,13 @@ int qmoe_moe_step_resid(qmoe_dict_t d, const uint32_t* d_table, const int32_t* d
                         const qmoe_matrix* d_mats, int32_t tokens_per_run, int32_t lg_wi, int32_t lg_wo,
                         int32_t d_model, int32_t d_ff, const uint16_t* d_x, int64_t ldx, uint16_t* d_h, int64_t ldh,
                         uint16_t* d_out, int64_t ldo, int32_t* d_counters, int32_t hot_entries, const float* d_gate,
-                        void* stream) {
+                        const uint64_t* d_hash_mult, int32_t* d_assign_out, void* stream) {
   if (!d_x) return qmoe::fail(QMOE_EINVAL, "bad argument");
   if (d_out == d_x && T > 0) return qmoe::fail(QMOE_EINVAL, "d_out must not alias d_x (the wi phase reads it)");
+  if (d_hash_mult && d_gate) return qmoe::fail(QMOE_EINVAL, "the hash rule has no gate");
   return moe_step_impl(d, d_table, d_assign, T, E, d_mats, tokens_per_run, lg_wi, lg_wo, d_model, d_ff, d_x,
                        QMOE_X_BF16, ldx, d_h, ldh, d_out, ldo, d_counters, nullptr, nullptr, hot_entries, d_gate, d_x,
-                       ldx, stream);
+                       ldx, stream, d_hash_mult, d_assign_out);
 }
 
 int qmoe_grouped_matvec(qmoe_dict_t d, const uint32_t* d_table, const qmoe_work* d_work, const int32_t* d_n_work,

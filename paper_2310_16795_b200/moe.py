@@ -335,11 +335,14 @@ class CompressedMoELayer:
             min(self.STEP_HOT_MAX, max(self.hot_entries(T, True), self.hot_entries(T, False))), _lib.ptr(gate),
             _lib.stream_ptr(stream)))
 
-    def step_resid(self, x, assign, out, gate=None, stream=None) -> None:
+    def step_resid(self, x, assign, out, gate=None, stream=None, hash_mult=None, assign_out=None) -> None:
         """One residual block in one launch (qmoe_moe_step_resid): out (bf16,
         T x d_model) = bf16(x + [gate *] moe(x)), x a bf16 CUDA tensor with
-        16-byte aligned rows; tokens without an expert pass x through."""
-        T = assign.shape[0]
+        16-byte aligned rows; tokens without an expert pass x through. With
+        hash_mult (a DeviceRouter's hash multipliers) the launch routes the
+        tokens itself (RouterSim hash rule) and `assign` may be None; the ids
+        are written to assign_out when given."""
+        T = x.shape[0]
         if T > self.max_tokens:
             self._alloc(T)
         self._T = T
@@ -349,7 +352,7 @@ class CompressedMoELayer:
             lg_wi, lg_wo, self.d_model, self.d_ff, _lib.ptr(x), x.stride(0), _lib.ptr(self.h), self.h.stride(0),
             _lib.ptr(out), out.stride(0), _lib.ptr(self.counters),
             min(self.STEP_HOT_MAX, max(self.hot_entries(T, True), self.hot_entries(T, False))), _lib.ptr(gate),
-            _lib.stream_ptr(stream)))
+            _lib.ptr(hash_mult), _lib.ptr(assign_out), _lib.stream_ptr(stream)))
 
     def forward_routed(self, x, router, gated: bool = False, out=None, stream=None):
         """Router + layer on the device: expert ids (and, with `gated`, the
@@ -506,8 +509,9 @@ class CompressedMoEModel:
     the reference's RouterSim rules), then ONE fused launch computing
     x_{l+1} = bf16(x_l + [gate *] wo_e relu(wi_e x_l)) (qmoe_moe_step_resid).
     Activations stay bf16 in HBM; the whole forward is device-only and
-    CUDA-graph capturable (two launches per layer with hash routing, three
-    with argmax)."""
+    CUDA-graph capturable: ONE launch per layer with ungated hash routing (the
+    block hashes its tokens itself), three with argmax (score + select +
+    block)."""
 
     def __init__(self, layers: list, routers: list, gated: bool = False):
         if len(layers) != len(routers) or not layers:
@@ -541,10 +545,17 @@ class CompressedMoEModel:
         trace = []
         for l, (lay, router) in enumerate(zip(self.layers, self.routers)):
             nxt = bufs[(l + 1) % 2]
-            assign, gate = router(cur, gated=self.gated, stream=stream)
-            if keep:
-                trace.append((cur.clone(), assign.clone()))
-            lay.step_resid(cur, assign, nxt, gate=gate, stream=stream)
+            if router.rule == _lib.QMOE_ROUTE_HASH and not self.gated:  # router fused into the block
+                ids = torch.empty(T, dtype=torch.int32, device=x.device) if keep else None
+                xin = cur.clone() if keep else None
+                lay.step_resid(cur, None, nxt, stream=stream, hash_mult=router.mult, assign_out=ids)
+                if keep:
+                    trace.append((xin, ids))
+            else:
+                assign, gate = router(cur, gated=self.gated, stream=stream)
+                if keep:
+                    trace.append((cur.clone(), assign.clone()))
+                lay.step_resid(cur, assign, nxt, gate=gate, stream=stream)
             cur = nxt
         out = cur.clone()
         return (out, trace) if keep else out
