@@ -734,8 +734,26 @@ def main():
         ours1_us = _time_graphs(chains1, 4 * len(chains1), 3) * 1e3 / C1
         del chains1
         bf16_1_us, sol1_us = bf16_expert_token(d_model, d_ff, dev, hbm_peak)
+        # the c2048 shape (2080 / 6144): a 256-expert slice of a c2048-shaped
+        # layer (542 MB compressed, > 4x L2), one token per step, distinct
+        # experts step to step; vs the bf16 expert FFN of that shape
+        Ec, dmc, dfc = WORKLOADS["switch-c2048"]
+        lay_c = build_layer(256, dmc, dfc, seed=9, dic=dic, device=dev, max_tokens=1)
+        xc = torch.from_numpy(q.bf16_round(np.random.default_rng(3).normal(size=(64, dmc)).astype(np.float32)))
+        xc = xc.to(dev).to(torch.bfloat16)
+        ac = [torch.tensor([e], dtype=torch.int32, device=dev) for e in range(0, 256, 4)]
+        oc = torch.empty((1, dmc), device=dev)
+        gc = [_capture(lambda j=j: [lay_c.forward_device(xc[(j * 10 + u) % 64:(j * 10 + u) % 64 + 1],
+                                                         ac[(j * 10 + u) % len(ac)], out=oc) for u in range(10)])
+              for j in range(6)]
+        ours_c_us = _time_graphs(gc, 12, 3) * 1e3 / 10
+        del gc, lay_c
+        torch.cuda.empty_cache()
+        bf16_c_us, sol_c_us = bf16_expert_token(dmc, dfc, dev, hbm_peak)
         per_token = {"tokens_per_step": 1, "ours_us_per_step": ours1_us, "bf16_cublas_us_per_token": bf16_1_us,
                      "bf16_hbm_sol_us": sol1_us, "ours_vs_bf16_cublas": bf16_1_us / ours1_us,
+                     "c2048_shape": {"ours_us_per_step": ours_c_us, "bf16_cublas_us_per_token": bf16_c_us,
+                                     "bf16_hbm_sol_us": sol_c_us, "ours_vs_bf16_cublas": bf16_c_us / ours_c_us},
                      "what": "one MoE layer step for one token (routed expert wi -> ReLU -> wo): the fused step "
                              "(graphs of 10 layer steps, cold pool) vs uncompressed bf16 cuBLAS gemv -> relu -> "
                              "gemv over a cold pool of experts"}
