@@ -427,7 +427,20 @@ def matvec_at_scale(dic, dev, hbm_peak, rows=768, cols=3072, lg=2, iters=20):
     ms = e0.elapsed_time(e1) / iters
     nbytes = sum(m.compressed_bytes for m in mats)
     ncw = sum(m.n_codewords for m in mats)
+    # the instruction-issue roof: warp-instructions per codeword
+    # of this launch from the committed ncu capture, at 4 issues / SM / cycle
+    issue = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_summaries.json")) as fh:
+            inst = json.load(fh)["pipe"][0]["inst_executed"]
+        ipc = inst / ncw
+        roof = 4 * 148 * 1.965e9 / ipc
+        issue = {"warp_inst_per_codeword": ipc, "codewords_per_s": roof, "GBps": roof * nbytes / ncw / 1e9,
+                 "source": "profiles/r02_ncu_summaries.json (pipe: smsp__inst_executed of this launch shape)"}
+    except Exception:
+        pass
     out = {"kernel": "pipe_matvec_kernel (one grouped launch)", "shape": f"{rows}x{cols}", "matrices": E,
+           "issue_roof": issue,
            "ms_per_launch": ms, "codewords_per_s": ncw / ms * 1e3, "weights_per_s": E * rows * cols / ms * 1e3,
            "GBps": nbytes / ms / 1e6, "frac_of_hbm": nbytes / ms / 1e6 / hbm_peak,
            "bf16_sol_weights_per_s": hbm_peak * 1e9 / 2}

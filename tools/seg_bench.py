@@ -39,7 +39,7 @@ def runs_for(mats, ntok, ldx, lg=None):
     return raw, n, t
 
 
-def bench(rows, cols, lg=None, ntok=1, iters=20, hot=None, packed=False):
+def bench(rows, cols, lg=None, ntok=1, iters=20):
     per = 2 * rows * cols // 24 + 8 * rows
     E = max(8, int(4.5 * L2 / per))
     mats = _stacked(E, rows, cols, seed=rows + cols, dic=dic, device=dev)
@@ -78,7 +78,7 @@ def bench(rows, cols, lg=None, ntok=1, iters=20, hot=None, packed=False):
 if __name__ == "__main__":
     for rows, cols, lg in ((3072, 768, 0), (768, 3072, 2), (6144, 2080, 1), (2080, 6144, 2)):
         for ntok in (1, 2):
-            bench(rows, cols, lg=lg, ntok=ntok, packed=False)
+            bench(rows, cols, lg=lg, ntok=ntok)
     for lg in (0, 1, 2, 3):
-        bench(3072, 768, lg=lg, packed=False)
-        bench(768, 3072, lg=lg, packed=False)
+        bench(3072, 768, lg=lg)
+        bench(768, 3072, lg=lg)
