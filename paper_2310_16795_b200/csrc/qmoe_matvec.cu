@@ -1525,7 +1525,12 @@ static int moe_step_impl(qmoe_dict_t d, const uint32_t* d_table, const int32_t* 
   SP.w2 = 11;  // split weight of a 2-token run (a 1-token run weighs 8; measured)
   const int maxc = std::max(d_model, d_ff);
   const size_t slot = (size_t)2 * 4 * (((maxc + 32) + 3) & ~3);
-  const size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
+  // x staging of a window: >= one 2-token run, up to 4 runs within 48 KB —
+  // and two 2-token runs when that costs <= 56 KB (else a CTA whose task range
+  // crosses two such runs needs a second window: Switch-base-128 T = 64
+  // 49.4 -> 47.7 us; more staging than that only delays the first task)
+  size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
+  if (2 * slot <= 56 * 1024) xbytes = std::max(xbytes, 2 * slot);
   // the single-warp plan needs no per-expert arrays
   SP.warp_plan = T <= WARP_PLAN_SMALL_E_MAX || (T <= WARP_PLAN_MAX && E > WARP_PLAN_LARGE_E);
   const size_t ecells = SP.warp_plan ? 0 : (size_t)3 * E + 2;
