@@ -288,11 +288,10 @@ __device__ __forceinline__ void store_row(const SegParams& P, const Run& R, int 
 // row's first and last 16-byte groups are shared with neighbouring rows (no
 // partial groups inside a row), and the boundaries nest across lg.
 constexpr int WIN_RUNS = 16;
-constexpr int WARP_PLAN_MAX = 256;  // fused step: single-warp dispatcher plan up to this many tokens
-// ... but above this many tokens the block-scan plan is faster unless E is
-// large (its loops are E-proportional; measured: T = 160 / 256 with E = 128:
-// 93.6 -> 86.3 / 126 -> 120 us; E = 2048: 362 -> 519 us)
-constexpr int WARP_PLAN_SMALL_E_MAX = 128, WARP_PLAN_LARGE_E = 512;  // (T <= 64: warp plan faster, measured)
+// fused step: single-warp dispatcher plan (nothing proportional to E) up to
+// this many tokens, the block-scan plan above (with the sort network fully
+// unrolled the two are equal at E = 128, T = 160-256; measured)
+constexpr int WARP_PLAN_MAX = 256;
 
 struct WinRun {
   const uint16_t* cw;
@@ -1537,7 +1536,7 @@ static int moe_step_impl(qmoe_dict_t d, const uint32_t* d_table, const int32_t* 
   size_t xbytes = std::max(slot, std::min<size_t>(4 * slot, 48 * 1024));
   if (2 * slot <= 56 * 1024) xbytes = std::max(xbytes, 2 * slot);
   // the single-warp plan needs no per-expert arrays
-  SP.warp_plan = T <= WARP_PLAN_SMALL_E_MAX || (T <= WARP_PLAN_MAX && E > WARP_PLAN_LARGE_E);
+  SP.warp_plan = T <= WARP_PLAN_MAX;
   const size_t ecells = SP.warp_plan ? 0 : (size_t)3 * E + 2;
   const size_t plan = ((ecells + 1 + 6 * (size_t)T + (d_hash_mult ? (size_t)T : 0)) * 4 + 15) & ~(size_t)15;
   const size_t static_smem = 2048;
