@@ -453,6 +453,305 @@ __global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) 
 }
 
 
+// ------------------------------------------------------------------ decode-once kernel
+// Item = (expert e, 128-row block, <= BN-token block); thread = row; 64-column
+// chunks through a ring of NR = 3 W tiles (and 3 token tiles), so the decode
+// of chunk k overlaps the MMAs of chunk k - 1 and every codeword is decoded
+// exactly ONCE per item:
+//   codewords   a thread walks its row's codewords in order; chunk k takes
+//               the codewords that START before its end column. A codeword
+//               spans <= 30 columns, so its values land in tile k or k + 1
+//               (zero-filled one chunk ahead) — no revisits, no column points.
+//   entries     looked up a group (8 codewords) at a time one refill ahead
+//               (registers), then staged in a per-thread ring of 16 entries in
+//               shared memory ([slot][thread]: conflict-free); refills happen
+//               at a warp-uniform point once per chunk, not inside the
+//               divergent per-codeword loop.
+//   mma         one thread issues 4 tcgen05.mma (M 128, N BN, K 16) per chunk
+//               and commits to the chunk's ring-slot mbarrier; slot k + 1's
+//               tile is rewritten only after MMA(k - 2) completed.
+template <int BN, int NR, int MINB, int GE>
+__global__ void __launch_bounds__(128, MINB) dense_dq_kernel(DenseParams P) {
+  constexpr uint32_t WT = 128u * 128u;  // W tile: 128 rows x 64 bf16 columns (SW128)
+  constexpr uint32_t XT = BN * 128u;    // token tile: BN rows x 64 bf16 columns
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr int XP = BN * 8;              // 16-byte x pieces per chunk
+  constexpr int XV = (XP + 127) / 128;    // ... per thread
+  __shared__ __align__(8) uint64_t tab_bar, mma_bar[NR];
+  __shared__ int s_total;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_tok[BN];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t base = sbase();
+  const uint32_t tab_s = base;
+  const uint32_t w_s = (base + P.w_off + 1023u) & ~1023u;
+  const uint32_t x_s = w_s + NR * WT;
+  const uint32_t ge_s = x_s + NR * XT + 4u * (uint32_t)tid;  // entry ring: slot j at ge_s + 512 j
+  int* start = reinterpret_cast<int*>(dsm + P.plan_off);
+  int* ipre = start + P.E + 1;
+  const int E = P.E;
+  const int nrb = (P.rows + 127) / 128;
+  const int nk = (P.cols + 63) / 64;
+  const uint32_t tb_mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
+  const uint32_t mma_mb0 = (uint32_t)__cvta_generic_to_shared(&mma_bar[0]);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_mb));
+    for (int i = 0; i < NR; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma_mb0 + 8u * i));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)P.H * 4;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tb_mb), "r"(bytes) : "memory");
+    for (uint32_t o = 0; o < bytes; o += 32768u)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tab_s + o),
+          "l"(reinterpret_cast<const char*>(P.gtab) + o), "r"(min(32768u, bytes - o)), "r"(tb_mb)
+          : "memory");
+  }
+  if (warp == 2) {  // item prefix over experts: warp scan of per-expert item counts
+    int carry_t = 0, carry_i = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int c = e < E ? __ldg(P.count + e) : 0;
+      const int ni = nrb * ((c + BN - 1) / BN);
+      int it = c, ii = ni;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(FULL_MASK, it, d), b = __shfl_up_sync(FULL_MASK, ii, d);
+        if (lane >= d) {
+          it += a;
+          ii += b;
+        }
+      }
+      if (e < E) {
+        start[e] = carry_t + it - c;
+        ipre[e] = carry_i + ii - ni;
+      }
+      carry_t += __shfl_sync(FULL_MASK, it, 31);
+      carry_i += __shfl_sync(FULL_MASK, ii, 31);
+    }
+    if (lane == 0) {
+      start[E] = carry_t;
+      ipre[E] = carry_i;
+      s_total = carry_i;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  mbar_wait(tb_mb, 0);
+  const uint32_t tmem = s_tmem;
+  const int total = s_total;
+  const uint32_t H = (uint32_t)P.H;
+  const uint32_t rx = (uint32_t)(tid & 7) << 4;  // SW128 16-byte chunk swizzle of my row
+  const uint32_t wrow = w_s + (uint32_t)tid * 128u;
+  const uint32_t idesc_n0 = idesc_bf16_f32<BN>() & ~(0x3Fu << 17);  // N set per item
+  uint32_t mph = 0;  // phase parity of mma_bar[i] in bit i
+  auto mma_wait = [&](int slot) {
+    mbar_wait(mma_mb0 + 8u * slot, (mph >> slot) & 1u);
+    mph ^= 1u << slot;
+  };
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    int lo = 0, hi = E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ipre[mid] <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    const int e = lo, local = item - ipre[e];
+    const int rb = local % nrb, tb = local / nrb;
+    const int cnt = start[e + 1] - start[e];
+    const int nt = min(BN, cnt - tb * BN);
+    const int tok0 = start[e] + tb * BN;
+    const qmoe_matrix& M = P.mats[2 * e + P.pass];
+    const uint16_t* cwp = M.cw;
+    const int r = rb * 128 + tid;
+    int s = 0, n = 0;
+    uint32_t wlo = 0, whi = 0;
+    if (r < P.rows) {
+      s = __ldg(M.row_off + r);
+      n = __ldg(M.row_off + r + 1) - s;
+      const uint32_t mm = __ldg(M.row_minmax + r);
+      wlo = mm & 0xFFFFu;
+      whi = mm >> 16;
+    }
+    if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
+    // codeword cursor, indices relative to my row's first group g0: next
+    // codeword i, end iend; entries of [staged - 16, staged) in the ring,
+    // entries of group staged / 8 in flight (pe), raw group staged / 8 + 1 in q
+    const int g0 = s >> 3, glast = n > 0 ? (s + n - 1) >> 3 : g0;
+    int i = s & 7;
+    const int iend = i + n;
+    uint32_t colb = 0;  // byte offset (2 per column) of codeword i's first column
+    int staged = GE;
+    uint32_t pe[8];
+    uint4 q;
+    {
+      const uint4 q0 = ld_group_nc(cwp, g0), q1 = ld_group_nc(cwp, min(g0 + 1, glast));
+      const uint4 q2 = ld_group_nc(cwp, min(g0 + 2, glast));
+      q = ld_group_nc(cwp, min(g0 + 3, glast));
+      uint32_t e0[8], e1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        e0[u] = lookup_pred(group_cw(q0, (uint32_t)u), tab_s, H, P.gtab);
+        e1[u] = lookup_pred(group_cw(q1, (uint32_t)u), tab_s, H, P.gtab);
+        if (GE == 16) pe[u] = lookup_pred(group_cw(q2, (uint32_t)u), tab_s, H, P.gtab);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ge_s + 512u * u), "r"(e0[u]));
+        if (GE == 16) asm volatile("st.shared.u32 [%0], %1;" ::"r"(ge_s + 512u * (u + 8)), "r"(e1[u]));
+        else pe[u] = e1[u];
+      }
+      if (GE == 8) q = q2;
+    }
+    __syncthreads();  // s_tok
+    // token tiles by cp.async (16-byte pieces, zero-filled past the row end
+    // and for absent tokens; x is bf16 with ldx % 8 == 0), one commit group
+    // per chunk, waited on just before the chunk's MMA
+    // MMA N per item: the item's tokens rounded up to 16 (M = 128 needs
+    // N % 16 == 0); token-tile rows past it are neither loaded nor read
+    const int nmma = (nt + 15) & ~15;
+    const uint32_t idesc = idesc_n0 | ((uint32_t)(nmma >> 3) << 17);
+    // my pieces' token rows (fixed for the item): x row pointer, or null
+    const uint16_t* xrow[XV];
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+      const int nn = (tid + v * 128) >> 3;
+      xrow[v] = nn < nt ? reinterpret_cast<const uint16_t*>(P.x) + (int64_t)s_tok[nn] * P.ldx : nullptr;
+    }
+    auto issue_x = [&](int k, int slot) {
+      if (k < nk) {
+        const int colb0 = k * 64 + (tid & 7) * 8;  // my pieces' first column (c8 = tid & 7 for every v)
+        const int nb = 2 * max(0, min(8, P.cols - colb0));
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+          const int nn = (tid + v * 128) >> 3;
+          const uint32_t dst = x_s + (uint32_t)slot * XT + (uint32_t)nn * 128u + ((uint32_t)((tid & 7) ^ (nn & 7)) << 4);
+          if (nn < nmma)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                         "l"(xrow[v] ? xrow[v] + colb0 : reinterpret_cast<const uint16_t*>(P.x)), "r"(xrow[v] ? nb : 0)
+                         : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue_x(0, 0);
+#pragma unroll
+    for (int c16 = 0; c16 < 8; ++c16) sts_zero16(wrow + 16u * (uint32_t)((c16 + lane) & 7));  // tile 0
+    int sc = 0;  // ring slot of chunk k
+    for (int k = 0; k < nk; ++k) {
+      const int sn = sc == NR - 1 ? 0 : sc + 1;
+      if (k >= NR - 1) mma_wait(sn);  // MMA(k + 1 - NR) read tiles sn
+#pragma unroll
+      for (int c16 = 0; c16 < 8; ++c16) sts_zero16(wrow + (uint32_t)sn * WT + 16u * (uint32_t)((c16 + lane) & 7));
+      issue_x(k + 1, sn);
+      const uint32_t kendb = (uint32_t)(k + 1) * 128u;
+      const uint32_t bcur = wrow + (uint32_t)sc * WT, bnext = wrow + (uint32_t)sn * WT;
+      for (;;) {
+        // warp-uniform refill: the older staged group consumed -> stage the
+        // group in flight, look up the next, load the one after
+        if (i >= staged - GE + 8 && staged < iend) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(ge_s + 512u * (uint32_t)((staged + u) & (GE - 1))), "r"(pe[u]));
+          staged += 8;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pe[u] = lookup_pred(group_cw(q, (uint32_t)u), tab_s, H, P.gtab);
+          q = ld_group_nc(cwp, min(g0 + (staged >> 3) + 1, glast));
+        }
+        const int lim = min(staged, iend);
+        while (i < lim && colb < kendb) {
+          const uint32_t en = lds_u32(ge_s + 512u * (uint32_t)(i & (GE - 1)));
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
+            if (f != 0x7Fu) {
+              const uint32_t vb = colb + (f >> 1);
+              const uint32_t a = (vb >= kendb ? bnext : bcur) + ((vb & 127u) ^ rx);
+              sts_u16(a, ((en >> (24 + j)) & 1u) ? whi : wlo);
+            }
+          }
+          colb += (en >> 28) * 4u;
+          ++i;
+        }
+        if (__all_sync(FULL_MASK, i >= iend || colb >= kendb)) break;
+      }
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk k's token tile
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t da = sw128_desc(w_s + (uint32_t)sc * WT + (uint32_t)ks * 32u);
+          const uint64_t db = sw128_desc(x_s + (uint32_t)sc * XT + (uint32_t)ks * 32u);
+          const uint32_t accf = (k > 0 || ks > 0) ? 1u : 0u;
+          asm volatile(
+              "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+                  tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(accf));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         mma_mb0 + 8u * sc)
+                     : "memory");
+      }
+      sc = sn;
+    }
+    // the last two chunks' MMAs (earlier ones were awaited in the loop)
+    for (int kk = max(0, nk - NR + 1); kk < nk; ++kk) mma_wait(kk % NR);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // the (empty) group past the last chunk
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    {  // epilogue: warp w reads TMEM lane quarter w (rows), 32 tokens per load
+      const int row = rb * 128 + 32 * warp + lane;
+#pragma unroll
+      for (int half = 0; half < (BN + 31) / 32; ++half) {
+        if (half * 32 >= nt) break;
+        uint32_t v[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)half * 32u;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < P.rows) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int nn = half * 32 + j;
+            if (nn >= nt) break;
+            const int64_t t = s_tok[nn];
+            const float vv = bf16_round_dev(__uint_as_float(v[j]));
+            if (P.y_mode == QMOE_Y_RELU_BF16) {
+              reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(vv, 0.f)) >> 16);
+            } else if (P.y_mode == QMOE_Y_STORE_F32) {
+              reinterpret_cast<float*>(P.y)[t * P.ldy + row] = vv + 0.f;
+            } else {
+              float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
+              *yp = *yp + vv;
+            }
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // TMEM read before the next item's first MMA; token ids reused
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -489,6 +788,40 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   // CTAs per SM (measured best of 128/256/512 x 64/128 x 1-4); the hot table
   // gets the rest of shared memory (its hit rate matters: the codeword ranks
   // are spread, 16K entries cover ~80%, 32K ~91%)
+#ifndef QMOE_DENSE_RW
+  if (P.x_bf16 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(d_x) & 15) == 0) {  // decode-once kernel: DQB CTAs per SM, ring of DQR W / token tiles, 16-entry rings
+#ifndef QMOE_DQ_R
+#define QMOE_DQ_R 2
+#define QMOE_DQ_B 3
+#endif
+#ifndef QMOE_DQ_GE
+#define QMOE_DQ_GE 16
+#endif
+    constexpr int DQB = QMOE_DQ_B, DQR = QMOE_DQ_R, DGE = QMOE_DQ_GE;
+    const size_t ring = 1024 + DQR * (size_t)128 * 128 + DQR * (size_t)BN * 128 + DGE * 128 * 4;
+    const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
+    const size_t per_cta = (size_t)d->max_smem_optin / DQB - 1024 - 1024;  // minus static shared memory
+    if (ring + plan + 4096 > per_cta) return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts for the dense pass");
+    int H = (int)((per_cta - ring - plan) / 4);
+    H = std::min(H, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE) & ~255;
+    P.H = std::max(H, 256);
+    P.w_off = P.H * 4;
+    P.plan_off = P.w_off + (int)ring;
+    const size_t smem = (size_t)P.plan_off + plan;
+    const int grid = DQB * d->num_sms;
+    if (BN == 64) {
+      CK(cudaFuncSetAttribute(dense_dq_kernel<64, DQR, DQB, DGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+         "attr");
+      dense_dq_kernel<64, DQR, DQB, DGE><<<grid, 128, smem, S(stream)>>>(P);
+    } else {
+      CK(cudaFuncSetAttribute(dense_dq_kernel<32, DQR, DQB, DGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+         "attr");
+      dense_dq_kernel<32, DQR, DQB, DGE><<<grid, 128, smem, S(stream)>>>(P);
+    }
+    CK(cudaGetLastError(), "dense_dq_kernel launch");
+    return QMOE_OK;
+  }
+#endif
   constexpr int RWR = 128, RWK = 64, RWB = 4;
   const size_t wbytes = (size_t)RWR * RWK * 2 + 1024, xbytes = (size_t)(RWK / 64) * BN * 128;
   const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
