@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(128, MINB) dense_dq_kernel(DenseParams P) {
   constexpr uint32_t WT = 128u * 128u;  // W tile: 128 rows x 64 bf16 columns (SW128)
   constexpr uint32_t XT = BN * 128u;    // token tile: BN rows x 64 bf16 columns
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  static_assert(NR == 2 && WT == 0x4000u, "column cursor below assumes slot = chunk & 1, tiles 16 KB apart");
   constexpr int XP = BN * 8;              // 16-byte x pieces per chunk
   constexpr int XV = (XP + 127) / 128;    // ... per thread
   __shared__ __align__(8) uint64_t tab_bar, mma_bar[NR];
@@ -586,7 +587,11 @@ __global__ void __launch_bounds__(128, MINB) dense_dq_kernel(DenseParams P) {
     const int g0 = s >> 3, glast = n > 0 ? (s + n - 1) >> 3 : g0;
     int i = s & 7;
     const int iend = i + n;
-    uint32_t colb = 0;  // byte offset (2 per column) of codeword i's first column
+    // column cursor of codeword i: chunk index << 14 | 0x3F80 (carry bridge)
+    // | 2 * (column % 64). Adding a value's byte offset (< 128) carries across
+    // the bridge into bit 14 when it leaves the chunk, so (v & 0x407F) is its
+    // offset from the ring base: tile (chunk & 1) at 16 KB, row byte in 0..127
+    uint32_t colb = 0x3F80u;
     int staged = GE;
     uint32_t pe[8];
     uint4 q;
@@ -650,8 +655,7 @@ __global__ void __launch_bounds__(128, MINB) dense_dq_kernel(DenseParams P) {
 #pragma unroll
       for (int c16 = 0; c16 < 8; ++c16) sts_zero16(wrow + (uint32_t)sn * WT + 16u * (uint32_t)((c16 + lane) & 7));
       issue_x(k + 1, sn);
-      const uint32_t kendb = (uint32_t)(k + 1) * 128u;
-      const uint32_t bcur = wrow + (uint32_t)sc * WT, bnext = wrow + (uint32_t)sn * WT;
+      const uint32_t kendb = (uint32_t)(k + 1) << 14;
       for (;;) {
         // warp-uniform refill: the older staged group consumed -> stage the
         // group in flight, look up the next, load the one after
@@ -668,15 +672,16 @@ __global__ void __launch_bounds__(128, MINB) dense_dq_kernel(DenseParams P) {
         while (i < lim && colb < kendb) {
           const uint32_t en = lds_u32(ge_s + 512u * (uint32_t)(i & (GE - 1)));
 #pragma unroll
-          for (int j = 0; j < 3; ++j) {
+          for (int j = 0; j < 3; ++j) {  // branch-free: the store is predicated on the slot being used
             const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
-            if (f != 0x7Fu) {
-              const uint32_t vb = colb + (f >> 1);
-              const uint32_t a = (vb >= kendb ? bnext : bcur) + ((vb & 127u) ^ rx);
-              sts_u16(a, ((en >> (24 + j)) & 1u) ? whi : wlo);
-            }
+            uint32_t a;  // wrow + ((v & 0x407F) ^ rx), the mask and swizzle in one lop3
+            asm("lop3.b32 %0, %1, 0x407F, %2, 0x6A;" : "=r"(a) : "r"(colb + (f >> 1)), "r"(rx));
+            a += wrow;
+            const uint32_t v = ((en >> (24 + j)) & 1u) ? whi : wlo;
+            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 127; @p st.shared.u16 [%0], %1; }" ::"r"(a),
+                         "h"((unsigned short)v), "r"(f));
           }
-          colb += (en >> 28) * 4u;
+          colb = (colb + (en >> 28) * 4u) | 0x3F80u;
           ++i;
         }
         if (__all_sync(FULL_MASK, i >= iend || colb >= kendb)) break;
@@ -790,8 +795,8 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   // are spread, 16K entries cover ~80%, 32K ~91%)
 #ifndef QMOE_DENSE_RW
   if (P.x_bf16 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(d_x) & 15) == 0) {  // decode-once kernel: DQB CTAs per SM, ring of DQR W / token tiles, 16-entry rings
-#ifndef QMOE_DQ_R
 #define QMOE_DQ_R 2
+#ifndef QMOE_DQ_B
 #define QMOE_DQ_B 3
 #endif
 #ifndef QMOE_DQ_GE
