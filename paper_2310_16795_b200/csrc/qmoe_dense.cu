@@ -669,8 +669,10 @@ __global__ void __launch_bounds__(128, MINB) dense_dq_kernel(DenseParams P) {
           q = ld_group_nc(cwp, min(g0 + (staged >> 3) + 1, glast));
         }
         const int lim = min(staged, iend);
+        uint32_t en_n = lds_u32(ge_s + 512u * (uint32_t)(i & (GE - 1)));
         while (i < lim && colb < kendb) {
-          const uint32_t en = lds_u32(ge_s + 512u * (uint32_t)(i & (GE - 1)));
+          const uint32_t en = en_n;  // entry i, loaded an iteration ahead (i + 1 may be stale: reloaded above)
+          en_n = lds_u32(ge_s + 512u * (uint32_t)((i + 1) & (GE - 1)));
 #pragma unroll
           for (int j = 0; j < 3; ++j) {  // branch-free: the store is predicated on the slot being used
             const uint32_t f = __byte_perm(en, 0u, 0x4440u + j);
