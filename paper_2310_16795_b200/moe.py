@@ -282,7 +282,7 @@ class CompressedMoELayer:
             with torch.cuda.stream(stream):
                 out.zero_()
 
-    DENSE_MIN_TOKENS = 10.0  # tokens per touched expert from which decode-then-MMA wins (measured round 2: 8 -> streaming, 12 -> dense)
+    DENSE_MIN_TOKENS = 6.0  # tokens per touched expert from which decode-then-MMA wins (measured round 2, decode-once kernel: 4 -> streaming, 6 -> dense)
 
     def use_dense(self, T: int) -> bool:
         """Batched regime: each expert block decoded once and multiplied with
