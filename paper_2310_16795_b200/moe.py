@@ -126,7 +126,10 @@ class CompressedMoELayer:
         self.order = torch.zeros(max(1, T), dtype=torch.int32, device=dev)
         # FFN hidden: relu(bf16(wi @ x)) per token, bf16 rows (wo-pass x)
         ldh = (self.d_ff + 7) // 8 * 8  # 16-byte aligned hidden rows (bulk staging)
-        self.h = _lib.padded_empty(max(1, T) * ldh, torch.bfloat16, dev).view(max(1, T), ldh)[:, : self.d_ff]
+        hb = _lib.padded_empty(max(1, T) * ldh, torch.bfloat16, dev).view(max(1, T), ldh)
+        if ldh > self.d_ff:
+            hb[:, self.d_ff:].zero_()  # row padding: defined bytes for the dense pass's 16-byte tail copies
+        self.h = hb[:, : self.d_ff]
         self.bad = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
         # fused step: {u64 arrival tickets, capacity C, -, 2 x C per-run counters} (qmoe_moe_step)
         self.counters = torch.zeros(2 * max(1, T) + 4, dtype=torch.int32, device=dev)

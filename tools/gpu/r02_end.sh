@@ -14,7 +14,7 @@ import seg_bench as S
 S.bench(768, 3072, lg=2, ntok=1, iters=3)
 PY
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:pipe_matvec -s 1 -c 1 -o gpurun_out/prof_pipe_r02 python /tmp/one.py > /dev/null 2>&1; echo "pipe prof rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_rw -s 4 -c 2 -o gpurun_out/prof_dense_r02 python tools/large_bench.py 4096 > /dev/null 2>&1; echo "dense prof rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_ -s 4 -c 2 -o gpurun_out/prof_dense_r02 python tools/large_bench.py 4096 > /dev/null 2>&1; echo "dense prof rc=$?"
 timeout 600 python tools/moe_sweep.py 1 2 4 8 16 32 64 > gpurun_out/sweep_r02.log 2>&1
 WORKLOAD=switch-c2048 timeout 900 python tools/moe_sweep.py 1 8 64 > gpurun_out/sweep_c2048_r02.log 2>&1
 timeout 600 python tools/step_trace.py 1 8 64 256 > gpurun_out/trace_r02.log 2>&1
