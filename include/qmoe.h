@@ -62,8 +62,7 @@ typedef struct qmoe_dict* qmoe_dict_t;
  *    starts; segment j starts at codeword s + j*n/G rounded UP to a multiple
  *    of 8 (clamped to the row end e), so inner segment boundaries are 16-byte
  *    group boundaries of the stream.
- *  row_id: reserved, must be NULL.
- *  colpts: column points for the decode-then-MMA pass (qmoe_colpoints). */
+ *  row_id, colpts: reserved, must be NULL. */
 typedef struct qmoe_matrix {
   const uint16_t* cw;
   const int32_t* row_off;
@@ -211,16 +210,6 @@ int qmoe_checkpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* 
                      const int32_t* d_row_off, int64_t rows, int64_t cols, int lg, uint16_t* d_ck,
                      int32_t* d_bad, void* stream);
 
-/* Column points of one RAW matrix (kernel-private, built once): for every
- * row r and chunk boundary column c = k * 2^chunk_log2 (k = 1 .. nb, nb =
- * ceil(cols / 2^chunk_log2) - 1), d_cp[r * nb + k - 1] = (index in the row of
- * the codeword holding column c) << 16 | (the column that codeword starts at).
- * Lets several lanes decode one column chunk of a row (qmoe_dense_moe_pass
- * uses 256-column chunks, chunk_log2 = 8). */
-int qmoe_colpoints(qmoe_dict_t dict, const uint32_t* d_table, const uint16_t* d_cw,
-                   const int32_t* d_row_off, int64_t rows, int64_t cols, int chunk_log2,
-                   uint32_t* d_cp, void* stream);
-
 /* Paper Listing 1 kept as the "paper design on B200"
  * baseline: warp per row, lanes 0..27 extract, decode words read through the
  * cache, shuffle reduction. If d_trace is non-NULL it receives, per codeword
@@ -358,11 +347,13 @@ int qmoe_ep_combine(const uint16_t* d_src_bf16, float* d_dst, int32_t n_rows, in
  * d_order[start_e .. start_e + d_expert_count[e]) (qmoe_moe_plan's outputs,
  * start_e = exclusive prefix of the counts), y[t][r] (y_mode as
  * qmoe_grouped_matvec) = bf16(sum_k W_e[r][k] x[t][k]) for all rows r of
- * W_e = d_mats[2e + pass] (RAW layout, rows x cols, colpts built with
- * chunk_log2 = 7 when cols > 128). Each 128-row block of an expert is decoded
- * once per block of tokens_per_block (32 or 64) tokens, 256 columns at a time,
- * into shared memory and multiplied on the tensor cores (tcgen05.mma, bf16 in,
- * fp32 accumulate in TMEM). */
+ * W_e = d_mats[2e + pass] (RAW layout, rows x cols). x must be bf16
+ * (x_dtype QMOE_X_BF16) with ldx % 8 == 0 and a 16-byte aligned base (else
+ * QMOE_EINVAL). Each 128-row block of an expert is decoded ONCE per block of
+ * tokens_per_block (32 or 64) tokens — a thread per row walks its codewords
+ * in order through a ring of two 64-column tiles in shared memory — and
+ * multiplied on the tensor cores (tcgen05.mma, bf16 in, fp32 accumulate in
+ * TMEM). */
 int qmoe_dense_moe_pass(qmoe_dict_t dict, const uint32_t* d_table, const qmoe_matrix* d_mats,
                         int32_t E, int32_t pass, const int32_t* d_expert_count,
                         const int32_t* d_order, int32_t rows, int32_t cols, const void* d_x,

@@ -95,7 +95,6 @@ _SIGS = {
     "qmoe_debug_empty_launch": (ctypes.c_int, [i32, i32, vp]),
     "qmoe_dense_moe_pass": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, i32, i32, vp, ctypes.c_int, i64, vp,
                                            ctypes.c_int, i64, i32, i32, vp]),
-    "qmoe_colpoints": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, ctypes.c_int, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

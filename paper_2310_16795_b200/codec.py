@@ -97,8 +97,6 @@ class DeviceMatrix:
         self.lg = 0
         # True when cached on a CompressedMatrix (shared with the drop-in API)
         self.shared = False
-        # column points for the decode-then-MMA pass (qmoe_colpoints), see build_colpoints
-        self.colpts = None
 
     @property
     def n_codewords(self) -> int:
@@ -142,24 +140,7 @@ class DeviceMatrix:
     def descriptor(self) -> tuple:
         """qmoe_matrix fields (include/qmoe.h)."""
         return (self.cw.data_ptr(), self.row_off.data_ptr(), self.row_minmax.data_ptr(),
-                self.ck.data_ptr() if self.ck is not None else 0, self.rows, self.cols, self.n_codewords, self.lg, 0,
-                self.colpts.data_ptr() if self.colpts is not None else 0)
-
-    COLPT_LOG2 = 7  # 128-column points (the decode-then-MMA pass uses 128- or 256-column chunks)
-
-    def build_colpoints(self, dic: Dictionary) -> None:
-        """Kernel-private column points (qmoe_colpoints): per row, the codeword
-        holding each 256-column chunk boundary and its start column, so several
-        lanes can decode one chunk of a row (decode-then-MMA pass)."""
-        torch = _torch()
-        nb = max(0, (self.cols + (1 << self.COLPT_LOG2) - 1) // (1 << self.COLPT_LOG2) - 1)
-        self.colpts = _lib.padded_empty(max(1, self.rows * nb), torch.int32, self.cw.device)
-        if nb == 0 or self.rows == 0:
-            return
-        table = self.codebook.table if self.codebook is not None else None
-        _lib.check(_lib.lib.qmoe_colpoints(dic.device_handle(self.cw.device.index), _lib.ptr(table), _lib.ptr(self.cw),
-                                           _lib.ptr(self.row_off), self.rows, self.cols, self.COLPT_LOG2,
-                                           _lib.ptr(self.colpts), _lib.stream_ptr()))
+                self.ck.data_ptr() if self.ck is not None else 0, self.rows, self.cols, self.n_codewords, self.lg, 0, 0)
 
     def mean_codewords_per_row(self) -> float:
         return self.n_codewords / max(1, self.rows)

@@ -3,20 +3,22 @@
 //
 // With t tokens per expert the streaming matvec re-decodes each expert matrix
 // ceil(t / 2) times; here every expert row block is decoded ONCE per step into
-// a dense bf16 tile in shared memory and multiplied on the tensor cores with
+// dense bf16 tiles in shared memory and multiplied on the tensor cores with
 // all of the expert's tokens (up to 64 per block).
 //
 //   work item   (expert e, 128-row block, token block of <= BN tokens); the
 //               persistent grid strides over the items; every CTA derives the
 //               item list from the dispatcher's expert counts (qmoe_moe_plan).
-//   decode      per 256-column chunk, 4 lanes per row split the chunk's
-//               codeword range of the row evenly (kernel-private column points),
-//               sum lengths, scan, and store the <= 3 non-zero bf16 levels of
-//               each codeword into a zero-filled tile whose 16-byte chunks are
-//               XOR-swizzled by row: the canonical SW128 K-major UMMA layout.
-//   mma         one thread issues tcgen05.mma (M 128, N BN, K 16) from shared
-//               memory descriptors into a TMEM accumulator, tcgen05.commit on
-//               an mbarrier; the token tile (bf16) is staged per chunk.
+//   decode      thread = row: it walks its row's codewords once, in order,
+//               through 64-column chunks; each codeword's <= 3 non-zero bf16
+//               levels go into a zero-filled tile whose 16-byte chunks are
+//               XOR-swizzled by row (the canonical SW128 K-major UMMA layout);
+//               a codeword straddling a chunk end writes its tail into the
+//               next tile of a two-tile ring.
+//   mma         one thread issues tcgen05.mma (M 128, N = the item's tokens
+//               rounded up to 16, K 16) from shared-memory descriptors into a
+//               TMEM accumulator, tcgen05.commit on the ring slot's mbarrier;
+//               the token tile (bf16) arrives by cp.async one chunk ahead.
 //   epilogue    per (row, token): bf16 RNE once (codec.py:243), y mode as the
 //               streaming kernel (relu -> bf16 hidden, or f32 store / add).
 //
@@ -34,8 +36,6 @@ using namespace qmoe_dev;
 
 namespace {
 
-constexpr int BK = 64;  // columns per chunk (128-byte bf16 rows)
-
 extern __shared__ __align__(128) uint8_t dsm[];
 
 struct DenseParams {
@@ -51,8 +51,7 @@ struct DenseParams {
   void* y;
   int y_mode;
   int64_t ldy;
-  int w_off, x_off, plan_off;  // byte offsets in dynamic shared memory
-  int cp_log2;                 // column-point granularity the matrices store (qmoe_colpoints)
+  int w_off, plan_off;  // byte offsets in dynamic shared memory
 };
 
 __device__ __forceinline__ uint32_t sbase() {
@@ -73,29 +72,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
-__device__ __forceinline__ uint16_t x_bf16_bits(const void* x, int bf16, int64_t i) {
-  if (bf16) return __ldg(reinterpret_cast<const unsigned short*>(x) + i);
-  return (uint16_t)(__float_as_uint(__ldg(reinterpret_cast<const float*>(x) + i)) >> 16);  // x is bf16-valued
-}
-
-// ------------------------------------------------------------------ tcgen05 kernel
-// Item = (expert e, 128-row block, <= BN-token block). For every 256-column
-// chunk of the rows:
-//   x tile   the chunk's columns of the item's token rows, bf16, staged as 4
-//            SW128 K-major blocks [BN rows x 128 B] (registers prefetched a
-//            chunk ahead, 16-byte loads);
-//   decode   4 lanes per row split the chunk's codeword range of their row
-//            evenly (column points give its first codeword and start column):
-//            pass 1 sums the entries' lengths, a 4-lane shuffle scan gives each
-//            lane its start column, pass 2 writes the <= 3 non-zero bf16 levels
-//            per codeword into the zero-filled W tile (4 SW128 blocks [128 rows
-//            x 128 B]) — equal work per lane, no divergent column walks;
-//   mma      one thread issues 16 tcgen05.mma (M 128, N BN, K 16) into the
-//            TMEM accumulator and commits to an mbarrier, awaited before the
-//            tiles are rewritten.
-// Epilogue: warps w, w+4, w+8, w+12 share TMEM lane quarter w%4 (rows) and read
-// BN/4 columns (tokens) each with tcgen05.ld.32x32b.
-
+// ------------------------------------------------------------------ tcgen05 helpers
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   // start >> 4 [0,14) | LBO 1 (unused, swizzled K-major) [16,30) | SBO 1024 B [32,46) |
   // version 1 [46,48) | SWIZZLE_128B = 2 [61,64)
@@ -118,40 +95,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
                  : "memory");
 }
 
-__device__ __forceinline__ uint4 x_chunk8(const void* x, int bf16, int64_t i) {
-  // 8 consecutive x values as bf16 (x is bf16-valued: f32 -> bf16 truncation is exact)
-  if (bf16) return __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + i));
-  const float4 a = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + i));
-  const float4 b = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + i) + 1);
-  auto pk = [](float lo, float hi) { return (__float_as_uint(lo) >> 16) | (__float_as_uint(hi) & 0xFFFF0000u); };
-  return make_uint4(pk(a.x, a.y), pk(a.z, a.w), pk(b.x, b.y), pk(b.z, b.w));
-}
-
-__device__ __forceinline__ uint4 x_chunk8_cols(const void* x, int bf16, int64_t i, int valid) {
-  // 8 x values from column c, of which only the first `valid` (= cols - c)
-  // belong to the row: the rest are zeroed — the row padding is never
-  // written (it may hold NaN / Inf bit patterns, and 0 * NaN would poison the
-  // MMA accumulators of every row)
-  if (valid >= 8) return x_chunk8(x, bf16, i);
-  uint32_t w[4] = {0u, 0u, 0u, 0u};  // the row's tail: element loads, nothing past the row
-  for (int e = 0; e < valid; ++e) w[e >> 1] |= (uint32_t)x_bf16_bits(x, bf16, i + e) << (16 * (e & 1));
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-// ------------------------------------------------------------------ row-walk kernel (v3)
-// Item = (expert e, 256-row block, <= BN-token block); thread = row; 128-column
-// chunks (2 SW128 K-blocks); two CTAs per SM, so one CTA's decode overlaps the
-// other's MMA wait and global-load latency.
-//   decode   each thread walks ITS row's codeword stream across the chunks
-//            (16-byte groups, three groups in flight): per codeword one table
-//            lookup and <= 3 shared stores of bf16 levels into its zero-filled
-//            tile row; a codeword that straddles the chunk end is revisited by
-//            the next chunk (values left of the chunk skipped), so no column
-//            points are needed and the work per row is exactly its codewords.
-//   mma      8 tcgen05.mma (2 M-blocks x 2 K-blocks x 4 K16 steps, N = BN) per
-//            chunk into 2 x BN TMEM columns, committed to an mbarrier that is
-//            awaited before the tiles are rewritten.
-
+// ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint4 ld_group_nc(const uint16_t* cw, int g) {
   // 8 codewords (16-byte aligned group g of the matrix's stream), read once
   uint4 a;
@@ -179,299 +123,27 @@ __device__ __forceinline__ uint32_t group_cw(const uint4& q, uint32_t u) {
   return (u & 1u) ? (w >> 16) : (w & 0xFFFFu);
 }
 
-template <int BN, int RW_ROWS, int RW_KC, int MINB>
-__global__ void __launch_bounds__(RW_ROWS, MINB) dense_rw_kernel(DenseParams P) {
-  constexpr int RW_THREADS = RW_ROWS;
-  constexpr int MB = RW_ROWS / 128, KB = RW_KC / 64;
-  constexpr uint32_t TMEM_COLS = MB * BN < 32 ? 32 : MB * BN;
-  __shared__ __align__(8) uint64_t tab_bar, mma_bar;
-  __shared__ int s_total;
-  __shared__ uint32_t s_tmem;
-  __shared__ int s_tok[64];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t base = sbase();
-  const uint32_t tab_s = base;
-  const uint32_t w_s = (base + P.w_off + 1023u) & ~1023u;  // KB blocks x 256 rows x 128 B
-  const uint32_t x_s = w_s + (uint32_t)KB * RW_ROWS * 128u;  // KB blocks x BN x 128 B
-  int* start = reinterpret_cast<int*>(dsm + P.plan_off);
-  int* ipre = start + P.E + 1;
-  const int E = P.E;
-  const int nrb = (P.rows + RW_ROWS - 1) / RW_ROWS;
-  const int nk = (P.cols + RW_KC - 1) / RW_KC;
-  const uint32_t tb_mb = (uint32_t)__cvta_generic_to_shared(&tab_bar);
-  const uint32_t mma_mb = (uint32_t)__cvta_generic_to_shared(&mma_bar);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 32) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_mb));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma_mb));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t bytes = (uint32_t)P.H * 4;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tb_mb), "r"(bytes) : "memory");
-    for (uint32_t o = 0; o < bytes; o += 32768u)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tab_s + o),
-          "l"(reinterpret_cast<const char*>(P.gtab) + o), "r"(min(32768u, bytes - o)), "r"(tb_mb)
-          : "memory");
-  }
-  if (warp == 2) {  // item prefix over experts: warp scan of per-expert item counts
-    int carry_t = 0, carry_i = 0;
-    for (int e0 = 0; e0 < E; e0 += 32) {
-      const int e = e0 + lane;
-      const int c = e < E ? __ldg(P.count + e) : 0;
-      const int ni = nrb * ((c + BN - 1) / BN);
-      int it = c, ii = ni;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int a = __shfl_up_sync(FULL_MASK, it, d), b = __shfl_up_sync(FULL_MASK, ii, d);
-        if (lane >= d) {
-          it += a;
-          ii += b;
-        }
-      }
-      if (e < E) {
-        start[e] = carry_t + it - c;
-        ipre[e] = carry_i + ii - ni;
-      }
-      carry_t += __shfl_sync(FULL_MASK, it, 31);
-      carry_i += __shfl_sync(FULL_MASK, ii, 31);
-    }
-    if (lane == 0) {
-      start[E] = carry_t;
-      ipre[E] = carry_i;
-      s_total = carry_i;
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  mbar_wait(tb_mb, 0);
-  const uint32_t tmem = s_tmem;
-  const int total = s_total;
-  const uint32_t H = (uint32_t)P.H;
-  const uint32_t rx = (uint32_t)(tid & 7) << 4;  // SW128 16-byte chunk swizzle of my row
-  const uint32_t wrow = w_s + (uint32_t)tid * 128u;
-  const uint32_t idesc = idesc_bf16_f32<BN>();
-  uint32_t mma_phase = 0;
-  constexpr int XP = BN * (RW_KC / 8);                  // 16-byte x pieces per chunk
-  constexpr int XV = (XP + RW_THREADS - 1) / RW_THREADS;  // ... per thread
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    int lo = 0, hi = E - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (ipre[mid] <= item) lo = mid;
-      else hi = mid - 1;
-    }
-    const int e = lo, local = item - ipre[e];
-    const int rb = local % nrb, tb = local / nrb;
-    const int cnt = start[e + 1] - start[e];
-    const int nt = min(BN, cnt - tb * BN);
-    const int tok0 = start[e] + tb * BN;
-    const qmoe_matrix& M = P.mats[2 * e + P.pass];
-    const uint16_t* cwp = M.cw;
-    const int r = rb * RW_ROWS + tid;
-    const bool valid = r < P.rows;
-    int s = 0, n = 0;
-    uint32_t wlo = 0, whi = 0;
-    if (valid) {
-      s = __ldg(M.row_off + r);
-      n = __ldg(M.row_off + r + 1) - s;
-      const uint32_t mm = __ldg(M.row_minmax + r);
-      wlo = mm & 0xFFFFu;
-      whi = mm >> 16;
-    }
-    if (tid < BN) s_tok[tid] = tid < nt ? __ldg(P.order + tok0 + tid) : 0;
-    // my row's codeword stream in groups of 8 (16-byte loads, two groups
-    // ahead). A group is looked up at once (8 independent lookups) and its
-    // codewords' start columns prefix-summed once; every chunk the group
-    // overlaps then writes its values in that chunk — no per-codeword
-    // dependence chain, and rows advance group by group in step.
-    const int glast = n > 0 ? (s + n - 1) >> 3 : (s >> 3);
-    int g = s >> 3;
-    uint4 q1 = make_uint4(0u, 0u, 0u, 0u), q2 = q1;
-    uint32_t ge[8];
-    int gc[9];  // start column of slot u; gc[8] = end of the group
-    bool more = n > 0;
-    auto open_group = [&](const uint4& q, int gstart_col) {
-      const int base = g * 8;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool in = base + u >= s && base + u < s + n;
-        ge[u] = in ? lookup_pred(group_cw(q, (uint32_t)u), tab_s, H, P.gtab) : 0x007F7F7Fu;  // no value, len 0
-      }
-      gc[0] = gstart_col;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) gc[u + 1] = gc[u] + (int)(ge[u] >> 28) * 2;
-    };
-    if (more) {
-      const uint4 q0 = ld_group_nc(cwp, g);
-      q1 = ld_group_nc(cwp, min(g + 1, glast));
-      q2 = ld_group_nc(cwp, min(g + 2, glast));
-      open_group(q0, 0);
-    }
-    __syncthreads();   // s_tok
-    uint4 xr[XV];
-    auto load_x = [&](int k0) {
-#pragma unroll
-      for (int v = 0; v < XV; ++v) {
-        const int idx = tid + v * RW_THREADS, nn = idx / (RW_KC / 8), c8 = idx % (RW_KC / 8);
-        xr[v] = (idx < XP && nn < nt && k0 + c8 * 8 < P.cols)
-                    ? x_chunk8_cols(P.x, P.x_bf16, (int64_t)s_tok[nn] * P.ldx + k0 + c8 * 8, P.cols - k0 - c8 * 8)
-                    : make_uint4(0u, 0u, 0u, 0u);
-      }
-    };
-    load_x(0);
-    for (int k = 0; k < nk; ++k) {
-      const int k0 = k * RW_KC;
-      if (k > 0) {  // the previous chunk's MMAs must be done reading W / X
-        mbar_wait(mma_mb, mma_phase);
-        mma_phase ^= 1u;
-      }
-#pragma unroll
-      for (int v = 0; v < XV; ++v) {
-        const int idx = tid + v * RW_THREADS, nn = idx / (RW_KC / 8), c8 = idx % (RW_KC / 8);
-        const uint32_t a = x_s + (uint32_t)(c8 >> 3) * (BN * 128u) + (uint32_t)nn * 128u +
-                           ((uint32_t)((c8 & 7) ^ (nn & 7)) << 4);
-        if (idx < XP)
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(xr[v].x), "r"(xr[v].y), "r"(xr[v].z),
-                       "r"(xr[v].w));
-      }
-      if (k + 1 < nk) load_x(k0 + RW_KC);
-#pragma unroll
-      for (int kb = 0; kb < KB; ++kb)
-#pragma unroll
-        for (int c16 = 0; c16 < 8; ++c16)
-          sts_zero16(wrow + (uint32_t)kb * (RW_ROWS * 128u) + 16u * (uint32_t)((c16 + lane) & 7));
-      // groups overlapping this chunk: write their values that fall in it
-      const int kend = k0 + RW_KC;
-      while (more && gc[0] < kend) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t en = ge[u];
-          const int b = gc[u] - k0;  // the codeword's start column in this chunk (may be < 0)
-#pragma unroll
-          for (int jj = 0; jj < 3; ++jj) {
-            const uint32_t f = __byte_perm(en, 0u, 0x4440u + jj);
-            const int vk = b + (int)(f >> 2);
-            if (f != 0x7Fu && (unsigned)vk < (unsigned)RW_KC) {
-              uint32_t a;
-              if constexpr (RW_KC == 64) {
-                a = wrow + (((uint32_t)vk * 2u) ^ rx);  // one SW128 K-block per chunk
-              } else {
-                a = wrow + (uint32_t)(vk >> 6) * (RW_ROWS * 128u) + ((((uint32_t)vk & 63u) * 2u) ^ rx);
-              }
-              sts_u16(a, ((en >> (24 + jj)) & 1u) ? whi : wlo);
-            }
-          }
-        }
-        if (gc[8] > kend) break;  // the group continues in the next chunk
-        if (g >= glast) {
-          more = false;
-          break;
-        }
-        ++g;
-        const uint4 q0 = q1;
-        q1 = q2;
-        q2 = ld_group_nc(cwp, min(g + 2, glast));
-        open_group(q0, gc[8]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb) {
-#pragma unroll
-          for (int kb = 0; kb < KB; ++kb) {
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              const uint64_t da =
-                  sw128_desc(w_s + (uint32_t)kb * (RW_ROWS * 128u) + (uint32_t)mb * (128u * 128u) + (uint32_t)ks * 32u);
-              const uint64_t db = sw128_desc(x_s + (uint32_t)kb * (BN * 128u) + (uint32_t)ks * 32u);
-              const uint32_t accf = (k > 0 || kb > 0 || ks > 0) ? 1u : 0u;
-              asm volatile(
-                  "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
-                      tmem + (uint32_t)mb * BN),
-                  "l"(da), "l"(db), "r"(idesc), "r"(accf));
-            }
-          }
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mma_mb)
-                     : "memory");
-      }
-    }
-    mbar_wait(mma_mb, mma_phase);
-    mma_phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    {  // epilogue: warp w reads TMEM lane quarter w % 4 of M-block w / 4, 32 tokens per load
-      const int quarter = warp & 3, mbk = warp >> 2;
-      const int row = rb * RW_ROWS + mbk * 128 + 32 * quarter + lane;
-#pragma unroll
-      for (int half = 0; half < (BN + 31) / 32; ++half) {
-        uint32_t v[32];
-        const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)mbk * BN + (uint32_t)half * 32u;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-              "=r"(v[30]), "=r"(v[31])
-            : "r"(ta));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < P.rows) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int nn = half * 32 + j;
-            if (nn >= nt) break;
-            const int64_t t = s_tok[nn];
-            const float vv = bf16_round_dev(__uint_as_float(v[j]));
-            if (P.y_mode == QMOE_Y_RELU_BF16) {
-              reinterpret_cast<uint16_t*>(P.y)[t * P.ldy + row] = (uint16_t)(__float_as_uint(fmaxf(vv, 0.f)) >> 16);
-            } else if (P.y_mode == QMOE_Y_STORE_F32) {
-              reinterpret_cast<float*>(P.y)[t * P.ldy + row] = vv + 0.f;
-            } else {
-              float* yp = reinterpret_cast<float*>(P.y) + t * P.ldy + row;
-              *yp = *yp + vv;
-            }
-          }
-        }
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // TMEM read before the next item's first MMA; token ids reused
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
-}
-
-
 // ------------------------------------------------------------------ decode-once kernel
 // Item = (expert e, 128-row block, <= BN-token block); thread = row; 64-column
-// chunks through a ring of NR = 3 W tiles (and 3 token tiles), so the decode
-// of chunk k overlaps the MMAs of chunk k - 1 and every codeword is decoded
-// exactly ONCE per item:
+// chunks through a ring of two W tiles (and two token tiles), every codeword
+// decoded exactly ONCE per item:
 //   codewords   a thread walks its row's codewords in order; chunk k takes
 //               the codewords that START before its end column. A codeword
 //               spans <= 30 columns, so its values land in tile k or k + 1
-//               (zero-filled one chunk ahead) — no revisits, no column points.
+//               (zero-filled before chunk k's decode) — no revisits.
 //   entries     looked up a group (8 codewords) at a time one refill ahead
 //               (registers), then staged in a per-thread ring of 16 entries in
 //               shared memory ([slot][thread]: conflict-free); refills happen
-//               at a warp-uniform point once per chunk, not inside the
-//               divergent per-codeword loop.
-//   mma         one thread issues 4 tcgen05.mma (M 128, N BN, K 16) per chunk
-//               and commits to the chunk's ring-slot mbarrier; slot k + 1's
-//               tile is rewritten only after MMA(k - 2) completed.
-template <int BN, int NR, int MINB, int GE>
-__global__ void __launch_bounds__(128, MINB) dense_dq_kernel(DenseParams P) {
+//               at a warp-uniform point, not inside the divergent per-codeword
+//               loop; the loop itself is branch-free (predicated stores).
+//   mma         one thread issues 4 tcgen05.mma (M 128, N = tokens rounded up
+//               to 16, K 16) per chunk and commits to the chunk's ring-slot
+//               mbarrier; slot k + 1 is rewritten only after MMA(k - 1).
+constexpr int DQ_NR = 2, DQ_CTAS = 3, DQ_GE = 16;  // ring slots, CTAs per SM, staged entries per thread
+
+template <int BN>
+__global__ void __launch_bounds__(128, DQ_CTAS) dense_dq_kernel(DenseParams P) {
+  constexpr int NR = DQ_NR, GE = DQ_GE;
   constexpr uint32_t WT = 128u * 128u;  // W tile: 128 rows x 64 bf16 columns (SW128)
   constexpr uint32_t XT = BN * 128u;    // token tile: BN rows x 64 bf16 columns
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
@@ -790,21 +462,11 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
   P.y_mode = y_mode;
   P.ldy = ldy;
   const int BN = tokens_per_block;
-  P.cp_log2 = 7;  // DeviceMatrix.build_colpoints: 128-column points
-  // row-walk kernel: 128 rows per item (= threads) x 64-column chunks x 4
-  // CTAs per SM (measured best of 128/256/512 x 64/128 x 1-4); the hot table
-  // gets the rest of shared memory (its hit rate matters: the codeword ranks
-  // are spread, 16K entries cover ~80%, 32K ~91%)
-#ifndef QMOE_DENSE_RW
-  if (P.x_bf16 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(d_x) & 15) == 0) {  // decode-once kernel: DQB CTAs per SM, ring of DQR W / token tiles, 16-entry rings
-#define QMOE_DQ_R 2
-#ifndef QMOE_DQ_B
-#define QMOE_DQ_B 3
-#endif
-#ifndef QMOE_DQ_GE
-#define QMOE_DQ_GE 16
-#endif
-    constexpr int DQB = QMOE_DQ_B, DQR = QMOE_DQ_R, DGE = QMOE_DQ_GE;
+  if (!P.x_bf16 || ldx % 8 != 0 || (reinterpret_cast<uintptr_t>(d_x) & 15) != 0)
+    return qmoe::fail(QMOE_EINVAL, "the dense pass needs bf16 x, ldx % 8 == 0 and a 16-byte aligned base");
+  {  // 3 CTAs of 128 threads per SM (measured best of 2-4 CTAs x 2-3 ring
+     // slots x 8/16 staged entries); the hot table gets the rest of shared memory
+    constexpr int DQB = DQ_CTAS, DQR = DQ_NR, DGE = DQ_GE;
     const size_t ring = 1024 + DQR * (size_t)128 * 128 + DQR * (size_t)BN * 128 + DGE * 128 * 4;
     const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
     const size_t per_cta = (size_t)d->max_smem_optin / DQB - 1024 - 1024;  // minus static shared memory
@@ -817,43 +479,17 @@ int qmoe_dense_moe_pass(qmoe_dict_t d, const uint32_t* d_table, const qmoe_matri
     const size_t smem = (size_t)P.plan_off + plan;
     const int grid = DQB * d->num_sms;
     if (BN == 64) {
-      CK(cudaFuncSetAttribute(dense_dq_kernel<64, DQR, DQB, DGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+      CK(cudaFuncSetAttribute(dense_dq_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
          "attr");
-      dense_dq_kernel<64, DQR, DQB, DGE><<<grid, 128, smem, S(stream)>>>(P);
+      dense_dq_kernel<64><<<grid, 128, smem, S(stream)>>>(P);
     } else {
-      CK(cudaFuncSetAttribute(dense_dq_kernel<32, DQR, DQB, DGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+      CK(cudaFuncSetAttribute(dense_dq_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
          "attr");
-      dense_dq_kernel<32, DQR, DQB, DGE><<<grid, 128, smem, S(stream)>>>(P);
+      dense_dq_kernel<32><<<grid, 128, smem, S(stream)>>>(P);
     }
     CK(cudaGetLastError(), "dense_dq_kernel launch");
     return QMOE_OK;
   }
-#endif
-  constexpr int RWR = 128, RWK = 64, RWB = 4;
-  const size_t wbytes = (size_t)RWR * RWK * 2 + 1024, xbytes = (size_t)(RWK / 64) * BN * 128;
-  const size_t plan = ((size_t)(2 * E + 2) * 4 + 127) & ~(size_t)127;
-  const size_t static_smem = 1024, per_cta = (size_t)d->max_smem_optin / RWB - (RWB > 1 ? 1024 : 0);
-  if (wbytes + xbytes + plan + static_smem + 4096 > per_cta)
-    return qmoe::fail(QMOE_EUNSUPPORTED, "too many experts for the dense pass");
-  int H = (int)((per_cta - wbytes - xbytes - plan - static_smem) / 4);
-  H = std::min(H, hot_entries > 0 ? hot_entries : QMOE_DICT_SIZE) & ~255;
-  P.H = std::max(H, 256);
-  P.w_off = P.H * 4;
-  P.x_off = P.w_off + (int)wbytes;
-  P.plan_off = P.x_off + (int)xbytes;
-  const size_t smem = (size_t)P.plan_off + plan;
-  const int grid = RWB * d->num_sms;
-  if (BN == 64) {
-    CK(cudaFuncSetAttribute(dense_rw_kernel<64, RWR, RWK, RWB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem), "attr");
-    dense_rw_kernel<64, RWR, RWK, RWB><<<grid, RWR, smem, S(stream)>>>(P);
-  } else {
-    CK(cudaFuncSetAttribute(dense_rw_kernel<32, RWR, RWK, RWB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem), "attr");
-    dense_rw_kernel<32, RWR, RWK, RWB><<<grid, RWR, smem, S(stream)>>>(P);
-  }
-  CK(cudaGetLastError(), "dense_rw_kernel launch");
-  return QMOE_OK;
 }
 
 }  // extern "C"

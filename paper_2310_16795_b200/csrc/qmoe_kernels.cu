@@ -557,31 +557,6 @@ __global__ void checkpoints_kernel(const uint32_t* __restrict__ tab, const uint1
   }
 }
 
-// ================================================================ column points
-// qmoe_colpoints (include/qmoe.h): thread per row; for every chunk boundary
-// column c = k * 2^kl (k >= 1) the codeword holding column c: its index in the
-// row (bits 16-31) and the column it starts at (bits 0-15). Boundaries past
-// the row's end point at the end (index n, column cols).
-__global__ void colpoints_kernel(const uint32_t* __restrict__ tab, const uint16_t* __restrict__ cw,
-                                 const int32_t* __restrict__ row_off, int64_t rows, int64_t cols, int kl, int nb,
-                                 uint32_t* __restrict__ cp, int32_t* bad) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int s = __ldg(row_off + r), n = __ldg(row_off + r + 1) - s;
-  int k = 1, off = 0;
-  for (int i = 0; i < n && k <= nb; ++i) {
-    const int len = int(__ldg(tab + __ldg(cw + s + i)) & 31u);
-    while (k <= nb && off + len > (k << kl)) {  // codeword i holds column k * 2^kl
-      cp[r * nb + k - 1] = ((uint32_t)i << 16) | (uint32_t)off;
-      ++k;
-    }
-    off += len;
-  }
-  for (; k <= nb; ++k) cp[r * nb + k - 1] = ((uint32_t)n << 16) | (uint32_t)min(off, 65535);
-  (void)cols;
-  (void)bad;
-}
-
 bool bad_dict(const qmoe_dict* d) { return d == nullptr || d->d_stab == nullptr; }
 
 }  // namespace
@@ -749,20 +724,6 @@ int qmoe_moe_plan(const int32_t* d_assign, int32_t T, int32_t E, const qmoe_matr
                                                  d_runs_wo, d_n,
                                                  d_expert_count, d_order, stage);
   CK(cudaGetLastError(), "moe_plan_kernel");
-  return QMOE_OK;
-}
-
-int qmoe_colpoints(qmoe_dict_t d, const uint32_t* d_table, const uint16_t* d_cw, const int32_t* d_row_off,
-                   int64_t rows, int64_t cols, int chunk_log2, uint32_t* d_cp, void* stream) {
-  if (bad_dict(d) || rows < 0 || cols < 0 || cols > 65535 || rows > INT32_MAX || chunk_log2 < 4 || chunk_log2 > 15 ||
-      !d_cp)
-    return qmoe::fail(QMOE_EINVAL, "bad argument (cols <= 65535, 4 <= chunk_log2 <= 15)");
-  if (!d->sparse_ok) return qmoe::fail(QMOE_EUNSUPPORTED, "column points need a <=3-non-zero dictionary");
-  const int nb = (int)((cols + (1 << chunk_log2) - 1) >> chunk_log2) - 1;
-  if (rows == 0 || nb <= 0) return QMOE_OK;
-  colpoints_kernel<<<(int)((rows + 127) / 128), 128, 0, S(stream)>>>(d_table ? d_table : d->d_mtab, d_cw, d_row_off,
-                                                                      rows, cols, chunk_log2, nb, d_cp, nullptr);
-  CK(cudaGetLastError(), "colpoints_kernel");
   return QMOE_OK;
 }
 

@@ -20,6 +20,7 @@ wo matvec through moepack.codec.fused_matvec) up to the matvec tolerance.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 
@@ -86,7 +87,6 @@ class CompressedMoELayer:
                 if m.ck is None and m.lg == 0 and self.max_lg[kind] > 0:
                     # checkpoints for 2^max_lg lanes per row; a run may use any 2^lg <= that
                     m.build_checkpoints(dic, lg=self.max_lg[kind])
-        self._colpts_ready = all(m.colpts is not None for m in list(wi) + list(wo))
         self.mats = None
         self._write_descriptors()
         self.tokens_per_unit = min(int(tokens_per_unit), _lib.NT_STREAM)
@@ -289,24 +289,10 @@ class CompressedMoELayer:
 
     def use_dense(self, T: int) -> bool:
         """Batched regime: each expert block decoded once and multiplied with
-        all its tokens on the tensor cores (qmoe_dense_moe_pass). Needs the
-        kernel-private column points, built on first use (not during a CUDA
-        graph capture: a capture before the first batched step keeps the
-        streaming path)."""
-        import torch
-
+        all its tokens on the tensor cores (qmoe_dense_moe_pass)."""
         if not self._sparse_path or self.dense_mode == "never":
             return False
-        want = self.dense_mode == "always" or T / self._runs_est(T) >= self.DENSE_MIN_TOKENS
-        if want and not self._colpts_ready:
-            if torch.cuda.is_current_stream_capturing():
-                return False
-            for m in list(self.wi) + list(self.wo):
-                if m.colpts is None:
-                    m.build_colpoints(self.dic)
-            self._write_descriptors()
-            self._colpts_ready = True
-        return want
+        return self.dense_mode == "always" or T / self._runs_est(T) >= self.DENSE_MIN_TOKENS
 
     def pass_dense(self, x, which: int, y, y_mode: int, stream=None) -> None:
         import torch
@@ -314,11 +300,17 @@ class CompressedMoELayer:
         T = self._T
         bn = 64 if T / self._runs_est(T) > 24 else 32
         rows, cols = (self.d_ff, self.d_model) if which == 0 else (self.d_model, self.d_ff)
-        xt = _lib.QMOE_X_BF16 if x.dtype == torch.bfloat16 else _lib.QMOE_X_F32
+        if x.dtype != torch.bfloat16 or x.stride(0) % 8 or x.data_ptr() % 16:
+            # the pass reads 16-byte bf16 pieces of token rows (x is bf16-valued:
+            # the layer input of the reference pipeline, or the bf16 hidden)
+            with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+                xb = torch.zeros((x.shape[0], (cols + 7) // 8 * 8), dtype=torch.bfloat16, device=x.device)
+                xb[:, :cols] = x[:, :cols]
+            x = xb
         _lib.check(_lib.lib.qmoe_dense_moe_pass(
             self.handle, self._table(), _lib.ptr(self.mats), self.E, which, _lib.ptr(self.expert_count),
-            _lib.ptr(self.order), rows, cols, _lib.ptr(x), xt, x.stride(0), _lib.ptr(y), y_mode, y.stride(0), bn,
-            0, _lib.stream_ptr(stream)))
+            _lib.ptr(self.order), rows, cols, _lib.ptr(x), _lib.QMOE_X_BF16, x.stride(0), _lib.ptr(y), y_mode,
+            y.stride(0), bn, 0, _lib.stream_ptr(stream)))
 
     def step(self, x, assign, out, stream=None, gate=None) -> None:
         """The whole step as one cooperative launch (qmoe_moe_step; with
