@@ -40,7 +40,7 @@ from .dictionary import (
     unpack_decode_words,
 )
 from .errors import ConfigError, CorruptionError, DictionaryMismatchError, MoepackError, TierCapacityError
-from .moe import CompressedMoELayer, CompressedMoEModel, load_moe_layer
+from .moe import CompressedMoELayer, CompressedMoEModel, forward_stream, load_moe_layer
 from .pipeline import DeviceRouter, RouterSim
 from .quantize import QuantGrid, TernaryMatrix, make_grid, reconstruction_levels, rtn_quantize, rtn_quantize_device
 from .stats import RateReport, compression_rate, natural_sparsity, sample_ternary, theoretical_limit

@@ -372,7 +372,7 @@ class CompressedMoELayer:
             out.mul_(gate[:, None])
         return out, assign, gate
 
-    GRAPH_CACHE = 8  # token counts with a captured host-API graph per layer
+    GRAPH_CACHE = 8  # (token count, path, slot) keys with a captured host-API graph per layer
     _HOST_STAGING = threading.local()  # per thread: (bytes, T, d_model) -> pinned (input, output) buffers
 
     def forward(self, x: np.ndarray, assign: np.ndarray) -> np.ndarray:
@@ -390,30 +390,51 @@ class CompressedMoELayer:
         T = int(x.shape[0])
         if x.ndim != 2 or x.shape[1] != self.d_model or a.shape != (T,):
             raise ValueError(f"expected x (T, {self.d_model}) and assign (T,)")
-        key = (T, self.use_dense(T))  # the captured graph holds one path
+        st = self._launch_host(x, a, slot=0, overlap=False)
+        st["done"].synchronize()
+        return st["yv"].copy()
+
+    def _launch_host(self, x: np.ndarray, a: np.ndarray, slot: int, overlap: bool) -> dict:
+        """Stage x / ids into the pinned buffers of `slot` and launch the step
+        (a CUDA graph captured on first use per (T, path, slot, overlap)),
+        recording its completion event. overlap=False: one graph holds the
+        input copy and the step (lowest latency for a blocking call);
+        overlap=True: the input copy runs on a copy stream, so it overlaps the
+        step in flight (forward_stream), and the graph holds the step only."""
+        import torch
+
+        T = int(x.shape[0])
+        key = (T, self.use_dense(T), slot)  # the captured graph holds one path
         st = self._stages.get(key)
         if st is None:
             st = self._host_stage(T, key)
         np.copyto(st["xv"], x)
         np.copyto(st["av"], a)
-        if st["graph"] is not None:
-            st["graph"].replay()
+        stream = torch.cuda.current_stream(self.device)
+        if overlap:
+            with torch.cuda.stream(st["copy_stream"]):
+                st["in_d"].copy_(st["in_h"], non_blocking=True)
+                st["in_ready"].record()
+            stream.wait_event(st["in_ready"])
+            body = st["step"]
         else:
-            stream = torch.cuda.current_stream(self.device)
-            st["body"]()  # first call for this T runs eagerly (lazy setup), then the graph is captured
+            body = st["copy_step"]
+        g = st["graphs"].get(overlap)
+        if g is not None:
+            g.replay()
+        else:
+            body()  # first call runs eagerly (lazy setup), then the graph is captured
             stream.synchronize()
             try:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    st["body"]()
-                st["graph"] = g
+                    body()
+                st["graphs"][overlap] = g
                 g.replay()
             except RuntimeError:  # capture not possible here: stay eager
-                st["graph"] = None
-                st["body"]()
+                body()
         st["done"].record()
-        st["done"].synchronize()
-        return st["yv"].copy()
+        return st
 
     def _host_stage(self, T: int, key) -> dict:
         """Pinned staging for T tokens: ONE input buffer (x f32 rows, then the
@@ -431,7 +452,7 @@ class CompressedMoELayer:
         # synchronous): a model's layers reuse host memory that stays in the
         # CPU caches
         shared = CompressedMoELayer._HOST_STAGING.__dict__.setdefault("bufs", {})  # per thread
-        hkey = (nb, T, self.d_model)
+        hkey = (nb, T, self.d_model, key[2])  # one set per pipeline slot (forward_stream)
         if hkey not in shared:
             shared[hkey] = (torch.empty(nb, dtype=torch.uint8, pin_memory=True),
                             torch.empty((T, self.d_model), dtype=torch.float32, pin_memory=True))
@@ -443,23 +464,39 @@ class CompressedMoELayer:
         direct = self.fused and not key[1]  # the fused step writes every output row (dropped ones: zero)
         y_d = None if direct else torch.empty((T, self.d_model), dtype=torch.float32, device=self.device)
 
-        def body():
-            in_d.copy_(in_h, non_blocking=True)
+        def step():  # the step only (its input copy enqueued separately)
             if direct:
                 self.forward_device(x_d, a_d, out=y_h)
             else:  # grouped / decode-then-MMA passes: device output, then one D2H copy
                 self.forward_device(x_d, a_d, out=y_d)
                 y_h.copy_(y_d, non_blocking=True)
 
+        def copy_step():
+            in_d.copy_(in_h, non_blocking=True)
+            step()
+
         st = {
-            "in_h": in_h, "in_d": in_d, "y_h": y_h, "body": body, "graph": None,
+            "in_h": in_h, "in_d": in_d, "y_h": y_h, "step": step, "copy_step": copy_step, "graphs": {},
             "xv": in_h[:xb].numpy().view(np.float32).reshape(T, self.d_model),
             "av": in_h[xb:xb + T * 4].numpy().view(np.int32),
             "yv": y_h.numpy(),
             "done": torch.cuda.Event(),
+            "in_ready": torch.cuda.Event(),
+            "copy_stream": self._copy_stream(),
         }
         self._stages[key] = st
         return st
+
+    _COPY_STREAMS = {}
+
+    def _copy_stream(self):
+        """One host-to-device copy stream per device (host API input copies)."""
+        import torch
+
+        key = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        if key not in CompressedMoELayer._COPY_STREAMS:
+            CompressedMoELayer._COPY_STREAMS[key] = torch.cuda.Stream(self.device)
+        return CompressedMoELayer._COPY_STREAMS[key]
 
     def touched_bytes(self, assign: np.ndarray) -> int:
         """Compressed bytes one step must stream: each distinct expert once."""
@@ -495,6 +532,34 @@ def load_moe_layer(wi_path: str, wo_path: str, dic: Dictionary, max_tokens: int 
     wi = read_stacked_device(wi_path, dic, d_ff, device)
     wo = read_stacked_device(wo_path, dic, d_model, device)
     return CompressedMoELayer(wi, wo, dic, max_tokens=max_tokens, **layer_kw)
+
+
+def forward_stream(items, depth: int = 2):
+    """Pipelined host API: `items` yields (layer, x, assign) — numpy tokens
+    (T, d_model) and expert ids, any CompressedMoELayer per item — and this
+    yields each step's numpy output rows in order, like layer.forward(x,
+    assign). Up to `depth` steps are in flight: while the GPU runs step i
+    (its H2D copy, fused step and output rows written to pinned host memory,
+    one CUDA graph), the host stages step i + 1's inputs into the other pinned
+    buffers and copies step i - 1's outputs out. Each pipeline slot has its own
+    pinned buffers and graphs; a layer serves one thread at a time."""
+    from collections import deque
+
+    pending = deque()
+    for i, (layer, x, assign) in enumerate(items):
+        if len(pending) == depth:  # the slot about to be reused: its step must be done
+            st = pending.popleft()
+            st["done"].synchronize()
+            yield st["yv"].copy()
+        x = np.ascontiguousarray(x, np.float32)
+        a = np.ascontiguousarray(assign, np.int32)
+        if x.ndim != 2 or x.shape[1] != layer.d_model or a.shape != (x.shape[0],):
+            raise ValueError(f"expected x (T, {layer.d_model}) and assign (T,)")
+        pending.append(layer._launch_host(x, a, slot=i % depth, overlap=True))
+    while pending:
+        st = pending.popleft()
+        st["done"].synchronize()
+        yield st["yv"].copy()
 
 
 class CompressedMoEModel:

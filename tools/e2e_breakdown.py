@@ -24,7 +24,7 @@ for _ in range(N):
 t1 = time.perf_counter()
 print(f"forward(): {(t1 - t0) / N * 1e6:.1f} us per call")
 st = next(iter(lay._stages.values()))
-g = st["graph"]
+g = st["graphs"][False]
 t0 = time.perf_counter()
 for _ in range(N):
     g.replay()

@@ -10,7 +10,7 @@ lay = build_layer(E, dm, dff, seed=0, dic=dic, device=dev, max_tokens=64)
 x = q.bf16_round(np.random.default_rng(0).normal(size=(64, dm)).astype(np.float32))
 a = q.RouterSim(E, rule="argmax", seed=0).assign(x)
 for _ in range(20): lay.forward(x, a)
-st = next(iter(lay._stages.values())); g = st["graph"]; s = torch.cuda.current_stream()
+st = next(iter(lay._stages.values())); g = st["graphs"][False]; s = torch.cuda.current_stream()
 N = 500
 def tm(fn):
     for _ in range(20): fn()
