@@ -773,6 +773,7 @@ struct StepParams {
   int plan_off;       // byte offset of the plan area in dynamic shared memory
   int w2;             // split weight of a 2-token run (a 1-token run weighs 8)
   int warp_plan;      // 1: single-warp sorting plan, 0: block-scan plan (see WARP_PLAN_*)
+  int phase_split;    // 1: half the CTAs run the wi phase, half the wo phase (small steps)
   const uint64_t* hash_mult;  // non-null: route in-kernel (RouterSim hash, bit-exact) instead of reading assign
   int32_t* assign_out;        // in-kernel routing: the ids (block 0 writes them), nullable
 };
@@ -1121,13 +1122,27 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
     __syncwarp();
     if (lane < 4) {  // task bounds of this CTA in both phases: {wi begin, wi end, wo begin, wo end}
       const int tpr = (lane < 2) ? S.tasks_wi : S.tasks_wo;
-      // target = total weighted tasks * k / grid; in double (exact product,
+      // phase split (small steps): CTAs [0, g1) take the wi range, the others
+      // the wo range, so the wo CTAs load their first tasks' metadata,
+      // codewords and entries while the wi CTAs run; otherwise every CTA
+      // takes a slice of both phases
+      const int g1 = S.phase_split ? (int)gridDim.x / 2 : 0;
+      int ng = (int)gridDim.x, k = blockIdx.x + (lane & 1);
+      if (g1) {
+        if (lane < 2) {
+          ng = g1;
+          k = min((int)blockIdx.x, g1) + ((int)blockIdx.x < g1 ? (lane & 1) : 0);
+        } else {
+          ng = (int)gridDim.x - g1;
+          k = max((int)blockIdx.x - g1, 0) + ((int)blockIdx.x >= g1 ? (lane & 1) : 0);
+        }
+      }
+      // target = total weighted tasks * k / ng; in double (exact product,
       // one rounding; every CTA evaluates the same k identically) — 64-bit
       // integer division is a long emulated sequence on the plan's critical path
-      const int k = blockIdx.x + (lane & 1);
       const int64_t num = (int64_t)wpre[nch] * tpr * k;
-      const int64_t target = num < INT_MAX ? (int64_t)((uint32_t)num / gridDim.x)  // the usual case: 32-bit
-                                           : (int64_t)__ddiv_rz((double)num, (double)gridDim.x);
+      const int64_t target = num < INT_MAX ? (int64_t)((uint32_t)num / (uint32_t)ng)  // the usual case: 32-bit
+                                           : (int64_t)__ddiv_rz((double)num, (double)ng);
       int lo = 0, hi = nch;  // last run with wpre[r] * tpr <= target
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -1141,7 +1156,7 @@ __global__ void __launch_bounds__(THREADS, 1) moe_step_kernel(StepParams S) {
         const int w = wpre[lo + 1] - wpre[lo];
         t = lo * tpr + min(tpr, (int)(target - (int64_t)wpre[lo] * tpr) / max(1, w));
       }
-      if ((lane & 1) && blockIdx.x == gridDim.x - 1) t = nch * tpr;
+      if ((lane & 1) && k == ng) t = nch * tpr;
       s_split[lane] = t;
     }
   }
@@ -1537,6 +1552,11 @@ static int moe_step_impl(qmoe_dict_t d, const uint32_t* d_table, const int32_t* 
   if (2 * slot <= 56 * 1024) xbytes = std::max(xbytes, 2 * slot);
   // the single-warp plan needs no per-expert arrays
   SP.warp_plan = T <= WARP_PLAN_MAX;
+  // phase split for the smallest steps, when the wi phase occupies under a
+  // third of the warps of half the grid (measured: Switch-base T = 1 / 2
+  // 14.5 / 14.9 -> 13.3 / 13.8 us; T = 4, 8 and the c2048 shape at T = 1,
+  // whose wi phase has 4x the tasks, are slower split)
+  SP.phase_split = T <= 2 && (int64_t)T * SP.tasks_wi <= 1024;
   const size_t ecells = SP.warp_plan ? 0 : (size_t)3 * E + 2;
   const size_t plan = ((ecells + 1 + 6 * (size_t)T + (d_hash_mult ? (size_t)T : 0)) * 4 + 15) & ~(size_t)15;
   const size_t static_smem = 2048;
