@@ -178,9 +178,13 @@ class CompressedMoELayer:
             out = []
             for kind, (rows, mg) in enumerate(((self.d_ff, self.mean_groups[0]), (self.d_model, self.mean_groups[1]))):
                 cap = min(m.lg for m in (self.wi if kind == 0 else self.wo))
-                lg = 0
+                # segments of at most ~8 groups (long rows: c2048), then more
+                # lanes while the step's lanes fill the GPU less than half
+                # (wi) / twice (wo: its runs start staggered behind wi's)
+                lg = min(cap, max(0, int(np.ceil(np.log2(max(1.0, mg / 8.0))))))
                 base_min = 2.0
-                while lg < cap and runs * rows * (1 << lg) < 2 * self.LANES:
+                fill = self.LANES // 2 if kind == 0 else 2 * self.LANES
+                while lg < cap and runs * rows * (1 << lg) < fill:
                     min_groups = base_min if runs * rows * (1 << lg) >= self.LANES // 4 else base_min / 2
                     if mg / (1 << (lg + 1)) < min_groups:
                         break
