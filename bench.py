@@ -46,7 +46,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default=None,
-                   help="BASELINE config (default: switch-base-128 on 1 GPU, switch-c2048 expert-sharded on N > 1)")
+                   help="BASELINE config (default: switch-base-128 as a plain process; switch-c2048 expert-sharded "
+                        "under torchrun, N >= 1, so the scaling series is one workload)")
     p.add_argument("--tokens", type=int, default=64)
     p.add_argument("--pool-factor", type=float, default=4.0, help="layer pool size in multiples of L2")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -557,8 +558,12 @@ def profiled_traffic():
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse()
+    # under torchrun (any N, N = 1 included) the run is the expert-parallel
+    # c2048 layer, so every point of a scaling series measures one workload;
+    # a plain process measures the single-GPU headline (Switch-base-128)
+    launched = "WORLD_SIZE" in os.environ
     if args.workload is None:
-        args.workload = "switch-c2048" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "switch-base-128"
+        args.workload = "switch-c2048" if launched else "switch-base-128"
     if args.impl == "reference":
         reference_arm(args)
         return
@@ -572,7 +577,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1 or args.force_ep:
+    if world > 1 or args.force_ep or (launched and args.workload == "switch-c2048"):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return ep_main(args, world, rank, local)
     dev = torch.device("cuda", local)
@@ -1061,7 +1066,8 @@ def ep_main(args, world, rank, local):
                     "h2d_bytes_per_step": int(xs[0].nbytes + asg[0].nbytes),
                     "d2h_bytes_per_step": int(T * d_model * 4), "tokens_per_s": T * world * args.steps / e2e_sec,
                     "api": "ExpertParallelMoE.forward(host tokens + ids copied in, outputs copied out)"},
-            "gpu_launches": args.steps, "cpu_baseline": None,
+            # per step: ep_slots_kernel, ep_rows_kernel, the fused local step, ep_combine_kernel
+            "gpu_launches": 4 * args.steps, "cpu_baseline": None,
             "clocks": dict(cs.summary(), window="sustained EP steps (0.5 s) into the timed region"),
         }))
     dist.destroy_process_group()
