@@ -333,13 +333,15 @@ def _mv_stage(device, rows: int, cols: int) -> dict:
     return st
 
 
-API_LANES = 6144  # lanes one API matvec is spread over (~192 warps)
-API_HOT_ENTRIES = 4096  # table entries each CTA stages for it (the fill is per CTA per launch)
+API_LANES = 12288  # lanes one API matvec is spread over (~384 warps)
+API_HOT_ENTRIES = 1024  # table entries each CTA stages for it (the fill is per CTA per launch)
+# (measured, tools/debug/api_matvec.py: 768x3072 8.9 -> 8.8 us, 3072x768 9.1 -> 8.6 us
+# against 6144 lanes / 4096 entries / >= 1.5 groups per lane)
 
 
 def _api_run(dm: DeviceMatrix, dic: Dictionary):
     """Work record (one run) + row checkpoints that let a single matrix use
-    ~API_LANES lanes: G = 2^lg lanes per row while each keeps >= ~1.5 groups
+    ~API_LANES lanes: G = 2^lg lanes per row while each keeps >= ~1 group
     of 8 codewords. Built once per uploaded matrix; None when one lane per row
     already fills the lanes (then qmoe_fused_matvec is used)."""
     hit = getattr(dm, "_api_runs", None)
@@ -348,7 +350,7 @@ def _api_run(dm: DeviceMatrix, dic: Dictionary):
     torch = _torch()
     mg = dm.n_codewords / max(1, dm.rows) / 8
     lg = 0
-    while lg < 3 and dm.rows * (1 << lg) < API_LANES and mg / (1 << (lg + 1)) >= 1.5:
+    while lg < 3 and dm.rows * (1 << lg) < API_LANES and mg / (1 << (lg + 1)) >= 1.0:
         lg += 1
     if lg == 0 or dm.rows == 0:
         dm._api_runs = ()
