@@ -118,6 +118,22 @@ def test_switch_large_128_dense_pass_vs_oracle(dic, odic):
     assert np.mean(d == 0) >= 0.99 and torch.linalg.norm(y - y2) <= 1e-2 * torch.linalg.norm(y)
 
 
+@pytest.mark.parametrize("E,d_model,d_ff,T", [(128, 768, 3072, 1024), (256, 2080, 6144, 2048)])
+def test_dense_pass_full_shapes_vs_oracle(dic, odic, E, d_model, d_ff, T):
+    """The decode-once tcgen05 pass at the Switch-base-128 shapes (wi 12
+    column chunks, wo 48) and the c2048 shapes (2080 columns: a partial last
+    chunk; 2080 rows: a partial last row block), 8 tokens per expert: its
+    auto-selected regime."""
+    layer = build_layer(E, d_model, d_ff, seed=24, dic=dic, max_tokens=T)
+    rng = np.random.default_rng(7)
+    x = q.bf16_round(rng.normal(size=(T, d_model)).astype(np.float32))
+    assign = q.RouterSim(E, rule="argmax", seed=0).assign(x)
+    assert layer.use_dense(T)
+    y = layer.forward_device(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(assign).cuda())
+    toks = np.sort(rng.choice(T, size=12, replace=False))
+    check_layer(layer, x, assign, y.cpu().numpy(), toks, odic)
+
+
 def test_c2048_shaped_layer_fused_step_vs_oracle(dic, odic):
     E, d_model, d_ff, T = 256, 2080, 6144, 8
     layer = build_layer(E, d_model, d_ff, seed=23, dic=dic, max_tokens=T)
