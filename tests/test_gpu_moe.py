@@ -102,13 +102,15 @@ def test_host_forward_graph_replays_fresh_inputs(dic, odic):
         assert np.mean(d == 0) >= 0.99
 
 
-def test_forward_stream_equals_forward(dic):
+@pytest.mark.parametrize("T", [24, 96])
+def test_forward_stream_equals_forward(dic, T):
     """The pipelined host API (two steps in flight, per-slot pinned buffers
     and graphs, layers alternating) returns, in order, exactly what one
     blocking forward() per step returns — no slot's inputs or outputs are
-    overwritten while its step is in flight."""
+    overwritten while its step is in flight. T = 96 (16 tokens per expert)
+    takes the decode-then-MMA path."""
     rng = np.random.default_rng(11)
-    E, d_model, d_ff, T = 6, 128, 384, 24
+    E, d_model, d_ff = 6, 128, 384
     layers = []
     for l in range(3):
         wi, wo = [], []
