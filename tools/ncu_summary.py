@@ -21,6 +21,7 @@ KEYS = {
     "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "registers": "launch__registers_per_thread",
     "inst_executed": "smsp__inst_executed.sum",
+    "thread_inst_per_inst": "smsp__thread_inst_executed_per_inst_executed.ratio",
     "grid": "launch__grid_size",
     "block": "launch__block_size",
 }
